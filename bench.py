@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark: LUBM-style query latency and join output rows/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--univ U] [--seed S]
+
+Workload (BASELINE.json configs[1]): LUBM-style synthetic store at scale U
+(default 10, ~1.38M triples, datagen/gsmgen) and queries Q1-Q14
+(datagen/queries/lubm, plain BGPs).  One "step" = the 14 queries executed
+once, each through the public drop-in API
+(``paper_1807_07691_b200.execute``), with L2 flushed before every step (the
+store is smaller than the 126 MB L2).
+
+* value          join output rows / s (sum over join steps of StepReport.rows,
+                 SURVEY.md §8(d)), device time (CUDA events around each query
+                 inside the library), whole job over all ranks
+* e2e            the same through execute() as a user calls it: host-side plan
+                 encoding, H2D of the query block from pinned memory, kernels,
+                 D2H of the result rows into host numpy arrays (wall clock)
+* roofline       dominant kernel class (join kernel), algorithmic bytes per
+                 SURVEY.md §8(d) / its measured event time vs MEASURED_PEAKS.json
+* cpu_baseline   the C oracle port (oracle/gsm_oracle.c, 1 core) on the same
+                 queries, bounded sample
+* --impl reference  the unmodified reference package (oracle/_ref) on the host
+                 cores, mode="parallel", worker_count=os.cpu_count()
+
+Multi-GPU (torchrun): every rank holds a replica of the store and serves its
+own copy of the query stream (weak scaling, no data-path collective); timing
+is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+if str(REPO) not in sys.path:
+    sys.path.insert(0, str(REPO))
+
+QDIR = REPO / "datagen" / "queries" / "lubm"
+W_ID = 4  # bytes per id
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--univ", type=int, default=10)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def _ensure_built():
+    lib = REPO / "paper_1807_07691_b200" / "_lib" / "libgsmat_b200.so"
+    if not lib.exists():
+        subprocess.run(["make", "-s", "-C", str(REPO / "paper_1807_07691_b200" / "csrc")], check=True)
+    subprocess.run(["make", "-s", "-C", str(REPO / "oracle")], check=True)
+
+
+def _gen_store(tmp: Path, univ: int, seed: int) -> Path:
+    out = tmp / f"lubm{univ}"
+    subprocess.run([str(REPO / "oracle" / "_build" / "gsmgen"), "lubm", "--univ", str(univ),
+                    "--seed", str(seed), "--out", str(out)], check=True, stdout=subprocess.DEVNULL)
+    return out
+
+
+def _queries():
+    return [(f.stem, f.read_text()) for f in sorted(QDIR.glob("*.rq"))]
+
+
+def _peaks():
+    try:
+        return json.loads((REPO / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 6
+                          for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _join_rows(rep_steps) -> int:
+    return sum(s.rows for s in rep_steps[1:])
+
+
+def _step_bytes(kind: str, L: int, a: int, E: int, O: int, out_a: int) -> int:
+    """Algorithmic HBM bytes of one join step."""
+    if kind == "expand":
+        return W_ID * L * a + 16 * L + W_ID * E + W_ID * O * out_a
+    if kind == "filter":
+        return W_ID * L * a + 16 * L + W_ID * L + W_ID * O * out_a
+    if kind == "cross":
+        return W_ID * O * out_a  # reads are O(|L|+|R|), dominated by the write
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    import paper_1807_07691_b200 as g
+    from paper_1807_07691_b200 import _lib
+
+    with tempfile.TemporaryDirectory() as tmp:
+        store_dir = _gen_store(Path(tmp), args.univ, args.seed)
+        store = g.load(store_dir, device=local)
+        queries = []
+        for name, text in _queries():
+            q = g.bind_constants(g.parse_query(text), store.dictionary)
+            queries.append((name, q, g.make_plan(q, store.stats)))
+        triples = store.triple_count
+        flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=f"cuda:{local}")  # 256 MB > L2
+
+        def one_step(collect):
+            flush.add_(1)
+            torch.cuda.synchronize()
+            per_q = []
+            t0 = time.perf_counter()
+            for name, q, plan in queries:
+                rep = g.ExecutionReport()
+                res = g.execute(q, plan, store, report=rep)
+                per_q.append((name, rep, len(res)))
+            wall = time.perf_counter() - t0
+            return wall, per_q
+
+        for _ in range(max(3, args.warmup)):
+            one_step(False)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        launches0 = _lib.kernel_launches()
+        steps = []
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                steps.append(one_step(True))
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        launches = _lib.kernel_launches() - launches0
+
+        dev_s = sum(rep.device_seconds for _, per_q in steps for _, rep, _ in per_q)
+        wall_s = sum(w for w, _ in steps)
+        rows = sum(_join_rows(rep.steps) for _, per_q in steps for _, rep, _ in per_q)
+        delta = sum(rep.intermediate_total for _, per_q in steps for _, rep, _ in per_q)
+        h2d = sum(rep.h2d_bytes for _, per_q in steps for _, rep, _ in per_q) / args.steps
+        d2h = sum(rep.d2h_bytes for _, per_q in steps for _, rep, _ in per_q) / args.steps
+
+        # roofline per kernel class from the per-step device events
+        cls: dict[str, list[float]] = {}
+        for _, per_q in steps:
+            for _, rep, _ in per_q:
+                for i in range(1, len(rep.steps)):
+                    k = rep.kinds[i]
+                    if k not in ("expand", "filter", "cross"):
+                        continue
+                    L = rep.steps[i - 1].rows
+                    a = rep.arities[i - 1]
+                    b = _step_bytes(k, L, a, rep.steps[i].prealloc_total, rep.steps[i].rows,
+                                    rep.arities[i])
+                    c = cls.setdefault(k, [0.0, 0.0, 0])
+                    c[0] += b
+                    c[1] += rep.steps[i].seconds
+                    c[2] += 1
+
+        lat = {}
+        for name, *_ in queries:
+            d = [rep.device_seconds for _, per_q in steps for n, rep, _ in per_q if n == name]
+            lat[name] = round(1e3 * statistics.median(d), 4)
+
+        if world > 1:
+            t = torch.tensor([dev_s, wall_s], dtype=torch.float64, device=f"cuda:{local}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            r = torch.tensor([rows], dtype=torch.float64, device=f"cuda:{local}")
+            torch.distributed.all_reduce(r)
+            dev_s, wall_s = float(t[0]), float(t[1])
+            rows_all = float(r[0])
+        else:
+            rows_all = float(rows)
+
+        if rank != 0:
+            torch.distributed.destroy_process_group()
+            return
+        peaks, peak_kind = _peaks()
+        dom = max(cls.items(), key=lambda kv: kv[1][1]) if cls else None
+        roof = None
+        if dom:
+            achieved = dom[1][0] / dom[1][1] / 1e9 if dom[1][1] > 0 else 0.0
+            traffic = None
+            tp = REPO / "profiles" / "ncu_traffic.json"
+            if tp.exists():
+                try:
+                    traffic = json.loads(tp.read_text()).get(dom[0])
+                except Exception:
+                    traffic = None
+            roof = {"bound": "hbm", "kernel": f"k_tilescan<{dom[0]}>", "achieved": round(achieved, 2),
+                    "peak": peaks["hbm_gbs"], "peak_source": peak_kind, "unit": "GB/s",
+                    "frac": round(achieved / peaks["hbm_gbs"], 5), "traffic": traffic,
+                    "launches": dom[1][2], "bytes_per_launch": int(dom[1][0] / max(1, dom[1][2])),
+                    "us_per_launch": round(1e6 * dom[1][1] / max(1, dom[1][2]), 3),
+                    "classes": {k: {"GBps": round(v[0] / v[1] / 1e9, 2) if v[1] else 0,
+                                    "launches": v[2], "ms": round(1e3 * v[1], 3)}
+                                for k, v in cls.items()}}
+
+        cpu = None
+        if not args.no_cpu_baseline:
+            cpu = cpu_baseline_port(store, queries, args.cpu_seconds)
+
+        value = rows_all / dev_s if dev_s > 0 else 0.0
+        line = {
+            "metric": "LUBM-style join output rows/sec (per-query latency in latency_ms)",
+            "value": round(value, 1),
+            "unit": "rows/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(3, args.warmup),
+            "ms_per_step": round(1e3 * dev_s / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic (datagen/gsmgen lubm, seeded)",
+            "config": {"workload": f"LUBM-style U={args.univ} ({triples} triples), Q1-Q14 "
+                                   "(datagen/queries/lubm), one step = 14 queries",
+                       "univ": args.univ, "seed": args.seed, "triples": triples,
+                       "l2": "flushed before every step (256 MB write)",
+                       "parallelism": f"replica x{world}"},
+            "e2e": {"value": round(rows_all / wall_s, 1) if wall_s > 0 else 0.0, "unit": "rows/s",
+                    "ms_per_step": round(1e3 * wall_s / args.steps, 4),
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "latency_ms": lat,
+            "join_rows_per_step": rows // args.steps,
+            "intermediate_rows_per_step": delta // args.steps,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+def cpu_baseline_port(store, queries, seconds):
+    """The C oracle (single-threaded restatement of the reference executor)."""
+    from oracle import oracle as orc
+
+    prep = orc.PreparedStore(store.matrices)
+    rows = 0
+    passes = 0
+    t0 = time.perf_counter()
+    while True:
+        for name, q, plan in queries:
+            _, srows, _ = orc.run(prep, [s.pattern for s in plan.steps], q.projection, q.distinct)
+            rows += sum(srows[1:])
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or passes >= 1000:
+            break
+    return {"value": round(rows / el, 1), "unit": "rows/s", "cores": 1, "kind": "port",
+            "sample": f"{passes} passes of Q1-Q14 on the same store ({el:.1f} s, C oracle)"}
+
+
+def run_reference(args):
+    rank, world, local = _dist()
+    if rank != 0:
+        return
+    ref = REPO / "oracle" / "_ref"
+    if ref.exists() and str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        from gsmat import executor, planner, qparser, storage
+    except Exception as exc:  # the reference package is not installed: time the C port
+        print(json.dumps({"impl": "reference", "unavailable": f"reference not importable: {exc}"}))
+        return
+    cores = os.cpu_count() or 1
+    with tempfile.TemporaryDirectory() as tmp:
+        store_dir = _gen_store(Path(tmp), args.univ, args.seed)
+        store = storage.load(store_dir)
+        queries = []
+        for name, text in _queries():
+            q = qparser.bind_constants(qparser.parse_query(text), store.dictionary)
+            queries.append((name, q, planner.make_plan(q, store.stats)))
+
+        def one_step():
+            rows = 0
+            t0 = time.perf_counter()
+            lat = {}
+            for name, q, plan in queries:
+                rep = executor.ExecutionReport()
+                tq = time.perf_counter()
+                executor.execute(q, plan, store, mode="parallel", worker_count=cores,
+                                 row_budget=1 << 62, report=rep)
+                lat[name] = time.perf_counter() - tq
+                rows += sum(s.rows for s in rep.steps[1:])
+            return time.perf_counter() - t0, rows, lat
+
+        for _ in range(max(3, args.warmup)):
+            one_step()
+        res = [one_step() for _ in range(args.steps)]
+        el = sum(r[0] for r in res)
+        rows = sum(r[1] for r in res)
+        value = rows / el
+        lat = {n: round(1e3 * statistics.median(r[2][n] for r in res), 3) for n, *_ in queries}
+        print(json.dumps({
+            "impl": "reference",
+            "metric": "LUBM-style join output rows/sec (per-query latency in latency_ms)",
+            "value": round(value, 1), "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(1e3 * el / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (datagen/gsmgen lubm, seeded)",
+            "config": {"workload": f"LUBM-style U={args.univ} ({store.triple_count} triples), "
+                                   "Q1-Q14, one step = 14 queries",
+                       "univ": args.univ, "seed": args.seed},
+            "latency_ms": lat,
+            "cpu_baseline": {"value": round(value, 1), "unit": "rows/s", "cores": cores,
+                             "kind": "reference",
+                             "sample": f"{args.steps} steps x Q1-Q14, gsmat.executor.execute "
+                                       f"mode=parallel worker_count={cores}"},
+            "e2e": {"value": round(value, 1), "unit": "rows/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }), flush=True)
+
+
+def main():
+    args = _args()
+    _ensure_built()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

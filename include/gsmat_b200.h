@@ -1,0 +1,172 @@
+/*
+ * gsmat_b200.h — C ABI of the B200-native gSMat join executor.
+ *
+ * The reference (arXiv 1807.07691's `gsmat` package, /root/reference/pkg) is
+ * pure Python and has no FFI; its seam for this path is the Python function
+ *
+ *     executor.execute(query, plan, store, mode="sequential", worker_count=1,
+ *                      row_budget=10**8, report=None) -> BindingTable
+ *     (/root/reference/pkg/src/gsmat/executor.py:296-304)
+ *
+ * over a loaded store (storage.load, storage.py:222-271).  The entry points
+ * below are exactly what a binding of that seam needs (the ctypes binding the
+ * package ships is paper_1807_07691_b200/_lib.py; a cgo/N-API stub is shown in
+ * INTEGRATION.md).  Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * Conventions
+ *   - Every function returns a gsm_status; 0 is success.  On failure
+ *     gsm_last_error() returns a thread-local message.  Status codes map to
+ *     the reference's exception classes (errors.py:4-53): see gsm_status.
+ *   - Node ids are the reference dictionary's dense 1-based ids
+ *     (dictionary.py:57-72); 0 is the "unknown constant" sentinel
+ *     (qparser.py:340,348).  Ids must be < 2^32.
+ *   - The library owns all device memory.  A store is immutable after
+ *     gsm_store_finalize and may be shared by any number of contexts; a
+ *     context (stream + arena) must be used by one host thread at a time.
+ */
+#ifndef GSMAT_B200_H
+#define GSMAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GSM_OK = 0,
+  GSM_ERR_VALUE = 1,           /* ValueError: bad mode / empty plan / bad argument      */
+  GSM_ERR_STORE_FORMAT = 2,    /* StoreFormatError (storage.py:193-271 checks)          */
+  GSM_ERR_UNKNOWN_PREDICATE = 3, /* UnknownPredicateError (storage.py:118-122)          */
+  GSM_ERR_RESOURCE = 4,        /* ResourceLimitError: row budget (executor.py:158-163,
+                                  192-193, 237-241) or device memory exhausted           */
+  GSM_ERR_CUDA = 5,            /* driver/runtime failure                                */
+  GSM_ERR_UNSORTED = 6         /* ValueError "pair list not sorted" (storage.py:44-45)  */
+} gsm_status;
+
+typedef struct gsm_store gsm_store;
+typedef struct gsm_context gsm_context;
+typedef struct gsm_result gsm_result;
+
+/* One triple pattern of the plan, in plan order (planner.py:73-83 PlanStep.pattern;
+ * fields of qparser.EncodedPattern, qparser.py:303-323).  Variables are small
+ * integers assigned by the caller (same name -> same index). */
+typedef struct {
+  int32_t s_var;    /* variable index >= 0, or -1 if the subject is a constant */
+  int32_t o_var;    /* variable index >= 0, or -1 if the object is a constant  */
+  uint32_t s_const; /* node id when s_var == -1                                */
+  uint32_t o_const; /* node id when o_var == -1                                */
+  int32_t pid;      /* predicate id; no matrix for pid -> the scan is empty     */
+  int32_t empty;    /* EncodedPattern.empty: unknown constant -> no rows        */
+} gsm_pattern;
+
+/* Budget semantics of the reference's two modes. */
+enum { GSM_BUDGET_SEQUENTIAL = 0, /* emitted rows of a join   (executor.py:192-193) */
+       GSM_BUDGET_PARALLEL = 1 }; /* pre-allocated E of a join (executor.py:237-241) */
+
+/* Per-step report (executor.py:67-91 StepReport/ExecutionReport).  Arrays of
+ * length n_steps, owned by the caller; any pointer may be NULL.  The scalar
+ * fields are outputs filled on success. */
+typedef struct {
+  int64_t* rows;           /* StepReport.rows: rows of the table after the step     */
+  int64_t* prealloc_total; /* StepReport.prealloc_total: E of the join, 0 for scans
+                              and cross products                                     */
+  float* device_ms;        /* device time of the step (CUDA events); NULL = skip    */
+  int32_t* kind;           /* GSM_STEP_* of each step                               */
+  int32_t* arity;          /* columns of the table after the step                   */
+  float total_device_ms;   /* out: device time of the whole query (first H2D copy
+                              to the last kernel), when device_ms != NULL           */
+  int64_t h2d_bytes;       /* out: host->device bytes copied for this query          */
+  int64_t d2h_bytes;       /* out: device->host bytes copied by gsm_execute          */
+  int64_t kernels;         /* out: kernels launched for this query                   */
+} gsm_report;
+
+/* Step kinds reported in gsm_report.kind (SURVEY.md §8 join taxonomy). */
+enum {
+  GSM_STEP_SCAN = 0,   /* first pattern: R1-R6 table scan                      */
+  GSM_STEP_EMPTY = 1,  /* right side has no matrix / unknown constant (R6)     */
+  GSM_STEP_EXPAND = 2, /* J1: one shared variable, neighbour expand            */
+  GSM_STEP_FILTER = 3, /* J2/J3: all right variables bound, membership filter  */
+  GSM_STEP_CROSS = 4,  /* J0: no shared variable, cross product                */
+  GSM_STEP_GATE = 5    /* J0 against a zero-arity (constant-constant) pattern  */
+};
+
+/* ---- device / store -------------------------------------------------- */
+
+/* Number of visible CUDA devices. */
+gsm_status gsm_device_count(int32_t* count);
+
+/* Replaces storage.load()'s in-memory Store (storage.py:106-112,222-271):
+ * creates an empty device store on `device` for node ids 1..node_count and
+ * predicate ids 1..max_pid. */
+gsm_status gsm_store_create(int32_t device, int64_t node_count, int32_t max_pid,
+                            gsm_store** out);
+
+/* Replaces PredicateMatrix(pid, so, os) (storage.py:56-72, fed by
+ * _pairs_from_bytes storage.py:193-200): uploads one predicate's pair arrays
+ * exactly as they sit in p<ID>.so / p<ID>.os (interleaved u64 LE pairs,
+ * `so` sorted by (s,o), `os` sorted by (o,s)), nnz pairs each.  The caller
+ * keeps ownership of the host buffers; they may be freed on return. */
+gsm_status gsm_store_put_predicate(gsm_store* store, int32_t pid, const uint64_t* so_pairs,
+                                   const uint64_t* os_pairs, int64_t nnz);
+
+/* Replaces PredicateMatrix.__post_init__ / build_aux (storage.py:38-53,66-72):
+ * builds the device row indexes (aux arrays, key -> segment lookup, diagonal
+ * lists) for every uploaded predicate and validates sortedness. */
+gsm_status gsm_store_finalize(gsm_store* store);
+
+/* Bytes of device memory held by the store. */
+gsm_status gsm_store_device_bytes(const gsm_store* store, int64_t* bytes);
+
+gsm_status gsm_store_free(gsm_store* store);
+
+/* ---- execution context ------------------------------------------------ */
+
+/* A stream plus an HBM arena for intermediate binding tables.  arena_bytes = 0
+ * picks a default (grown on demand up to the free device memory). */
+gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context** out);
+gsm_status gsm_context_free(gsm_context* ctx);
+
+/* Replaces executor.execute (executor.py:296-368) for mode="gpu":
+ * evaluates `n_steps` patterns in plan order as a left-deep chain of SM-based
+ * joins on the device, then projects onto `proj` (variable indices, n_proj of
+ * them) and applies DISTINCT when `distinct` != 0.  Join variables, cross
+ * products and output schemas follow executor.py:340-356.  A budget violation
+ * returns GSM_ERR_RESOURCE with the reference's message.
+ *
+ * part_index/part_count partition the FIRST step's rows into part_count
+ * contiguous ranges and evaluate only range part_index (multi-GPU row
+ * partitioning; 0/1 = whole query).  The union over all parts of the results
+ * is the bag of the whole query (before DISTINCT). */
+gsm_status gsm_execute(gsm_context* ctx, const gsm_pattern* steps, int32_t n_steps,
+                       const int32_t* proj, int32_t n_proj, int32_t distinct,
+                       int64_t row_budget, int32_t budget_mode, int64_t part_index,
+                       int64_t part_count, gsm_report* report, gsm_result** out);
+
+/* ---- results ---------------------------------------------------------- */
+
+/* Shape of the projected result: n_rows x n_cols (BindingTable.rows). */
+gsm_status gsm_result_shape(const gsm_result* res, int64_t* n_rows, int32_t* n_cols);
+
+/* Copies the result rows, row-major uint32 ids, into host memory
+ * (n_rows * n_cols * 4 bytes). */
+gsm_status gsm_result_copy(const gsm_result* res, uint32_t* host_rows);
+
+/* Device pointer of the row-major result (valid until gsm_result_free). */
+gsm_status gsm_result_device_ptr(const gsm_result* res, uint64_t* device_ptr);
+
+gsm_status gsm_result_free(gsm_result* res);
+
+/* ---- diagnostics ------------------------------------------------------ */
+
+/* Thread-local message of the last failing call (empty string if none). */
+const char* gsm_last_error(void);
+
+/* Number of kernels this library launched since load (all threads). */
+int64_t gsm_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GSMAT_B200_H */

@@ -1,0 +1,47 @@
+"""B200-native gSMat (arXiv 1807.07691) SM-based join executor.
+
+Drop-in for the reference package's load/index/query path
+(/root/reference/pkg/src/gsmat/__init__.py:5-29): ``load`` puts the
+predicate-partitioned store in HBM, ``execute(..., mode="gpu")`` runs a plan
+as a chain of sm_100a CUDA kernels and returns a ``BindingTable``.
+"""
+
+from .errors import (
+    GsmatError,
+    ParseError,
+    ResourceLimitError,
+    StoreFormatError,
+    UnknownIdError,
+    UnknownPredicateError,
+    UnsupportedFeatureError,
+)
+from .executor import DEFAULT_ROW_BUDGET, BindingTable, ExecutionReport, StepReport, execute
+from .frontend import Plan, QueryGraph, TriplePattern, bind_constants, make_plan, parse_query
+from .storage import DeviceStore, StatEntry, from_store, load
+
+__all__ = [
+    "BindingTable",
+    "DEFAULT_ROW_BUDGET",
+    "DeviceStore",
+    "ExecutionReport",
+    "GsmatError",
+    "ParseError",
+    "Plan",
+    "QueryGraph",
+    "ResourceLimitError",
+    "StatEntry",
+    "StepReport",
+    "StoreFormatError",
+    "TriplePattern",
+    "UnknownIdError",
+    "UnknownPredicateError",
+    "UnsupportedFeatureError",
+    "bind_constants",
+    "execute",
+    "from_store",
+    "load",
+    "make_plan",
+    "parse_query",
+]
+
+__version__ = "0.1.0"

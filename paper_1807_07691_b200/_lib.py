@@ -1,0 +1,161 @@
+"""ctypes binding of libgsmat_b200.so (the C ABI in include/gsmat_b200.h).
+
+There is no CPU fallback: importing the executor without the built library,
+or calling it on a machine without a CUDA device, raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+from . import errors
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgsmat_b200.so"
+
+GSM_OK = 0
+GSM_ERR_VALUE = 1
+GSM_ERR_STORE_FORMAT = 2
+GSM_ERR_UNKNOWN_PREDICATE = 3
+GSM_ERR_RESOURCE = 4
+GSM_ERR_CUDA = 5
+GSM_ERR_UNSORTED = 6
+
+GSM_BUDGET_SEQUENTIAL = 0
+GSM_BUDGET_PARALLEL = 1
+
+STEP_KINDS = ("scan", "empty", "expand", "filter", "cross", "gate")  # GSM_STEP_*
+
+#: Every symbol include/gsmat_b200.h declares (checked by tests/test_capi.py).
+EXPORTS = (
+    "gsm_device_count",
+    "gsm_store_create",
+    "gsm_store_put_predicate",
+    "gsm_store_finalize",
+    "gsm_store_device_bytes",
+    "gsm_store_free",
+    "gsm_context_create",
+    "gsm_context_free",
+    "gsm_execute",
+    "gsm_result_shape",
+    "gsm_result_copy",
+    "gsm_result_device_ptr",
+    "gsm_result_free",
+    "gsm_last_error",
+    "gsm_kernel_launches",
+)
+
+
+class Pattern(C.Structure):
+    """gsm_pattern"""
+
+    _fields_ = [
+        ("s_var", C.c_int32),
+        ("o_var", C.c_int32),
+        ("s_const", C.c_uint32),
+        ("o_const", C.c_uint32),
+        ("pid", C.c_int32),
+        ("empty", C.c_int32),
+    ]
+
+
+class Report(C.Structure):
+    """gsm_report"""
+
+    _fields_ = [
+        ("rows", C.POINTER(C.c_int64)),
+        ("prealloc_total", C.POINTER(C.c_int64)),
+        ("device_ms", C.POINTER(C.c_float)),
+        ("kind", C.POINTER(C.c_int32)),
+        ("arity", C.POINTER(C.c_int32)),
+        ("total_device_ms", C.c_float),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
+        ("kernels", C.c_int64),
+    ]
+
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    """Load the CUDA library (once).  Raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()' or "
+                "make -C paper_1807_07691_b200/csrc)"
+            )
+        L = C.CDLL(os.fspath(LIB_PATH))
+        vp = C.c_void_p
+        i32, i64 = C.c_int32, C.c_int64
+        P = C.POINTER
+        sig = {
+            "gsm_device_count": (i32, [P(i32)]),
+            "gsm_store_create": (i32, [i32, i64, i32, P(vp)]),
+            "gsm_store_put_predicate": (i32, [vp, i32, vp, vp, i64]),
+            "gsm_store_finalize": (i32, [vp]),
+            "gsm_store_device_bytes": (i32, [vp, P(i64)]),
+            "gsm_store_free": (i32, [vp]),
+            "gsm_context_create": (i32, [vp, i64, P(vp)]),
+            "gsm_context_free": (i32, [vp]),
+            "gsm_execute": (
+                i32,
+                [vp, P(Pattern), i32, P(i32), i32, i32, i64, i32, i64, i64, P(Report), P(vp)],
+            ),
+            "gsm_result_shape": (i32, [vp, P(i64), P(i32)]),
+            "gsm_result_copy": (i32, [vp, vp]),
+            "gsm_result_device_ptr": (i32, [vp, P(C.c_uint64)]),
+            "gsm_result_free": (i32, [vp]),
+            "gsm_last_error": (C.c_char_p, []),
+            "gsm_kernel_launches": (i64, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+        return L
+
+
+def last_error() -> str:
+    msg = lib().gsm_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(status: int) -> None:
+    """Map a gsm_status to the reference's exception classes."""
+    if status == GSM_OK:
+        return
+    msg = last_error()
+    if status == GSM_ERR_RESOURCE:
+        raise errors.ResourceLimitError(msg)
+    if status == GSM_ERR_STORE_FORMAT:
+        raise errors.StoreFormatError(msg)
+    if status == GSM_ERR_UNKNOWN_PREDICATE:
+        pid = int(msg.rsplit(" ", 1)[-1]) if msg and msg.rsplit(" ", 1)[-1].isdigit() else -1
+        raise errors.UnknownPredicateError(pid)
+    if status in (GSM_ERR_VALUE, GSM_ERR_UNSORTED):
+        raise ValueError(msg)
+    raise errors.DeviceError(msg or f"gsm status {status}")
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    st = lib().gsm_device_count(C.byref(n))
+    if st != GSM_OK:
+        return 0
+    return int(n.value)
+
+
+def kernel_launches() -> int:
+    return int(lib().gsm_kernel_launches())

@@ -1,0 +1,1010 @@
+// gsm_exec.cu — the SM-based join chain on the device.
+//
+// Replaces executor.execute / scan / sm_join / parallel_sm_join /
+// cross_product / preallocate (/root/reference/pkg/src/gsmat/executor.py:94-368).
+//
+// One query = one stream-ordered launch sequence with no host round trip
+// between plan steps:
+//   resolve   constant-endpoint scans (R2/R3/R5) -> device table descriptors
+//   per step  J1 expand | J2/J3 filter | J0 cross | gate  (one kernel each)
+//   pack      projection into a row-major u32 result
+// followed by one sync that returns the per-step counters (the report and the
+// budget checks), then optional DISTINCT and the result hand-off.
+//
+// Every join kernel is a single pass of "count -> scan -> scatter" (the
+// paper's Alg. 4 N/P pre-allocation, executor.py:197-215) fused into one
+// persistent kernel: tiles of 1024 left rows compute their candidate counts
+// (the N of each row), a decoupled look-back publishes tile prefixes (P), and
+// the same block scatters its rows' outputs into [P, P+N) with a
+// load-balanced output-slot -> row binary search, so hub rows of the
+// power-law tail are spread over all 256 threads of the tile.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gsm_internal.cuh"
+
+namespace gsm {
+
+constexpr int TS_THREADS = 256;
+constexpr int TS_ITEMS = 4;
+constexpr int TS_TILE = TS_THREADS * TS_ITEMS;
+constexpr u64 LB_MASK = (1ull << 40) - 1;
+constexpr u32 EPOCH_MAX = (1u << 22) - 1;
+
+struct TileSync {
+  u64* status;   // one word per tile: epoch:22 | flag:2 | value:40
+  u32* counter;  // dynamic tile counter (zeroed per query)
+  u32 epoch;
+};
+
+__device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 ld_acquire_u64(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 lb_word(u32 epoch, u32 flag, i64 v) {
+  u64 x = v < 0 ? 0 : (u64)v;
+  if (x > LB_MASK) x = LB_MASK;
+  return ((u64)epoch << 42) | ((u64)flag << 40) | x;
+}
+
+// Decoupled look-back: returns the exclusive prefix of tile t.
+__device__ i64 lookback(const TileSync& ts, u32 t, i64 agg) {
+  if (t == 0) {
+    st_release_u64(ts.status, lb_word(ts.epoch, 2, agg));
+    return 0;
+  }
+  st_release_u64(ts.status + t, lb_word(ts.epoch, 1, agg));
+  i64 excl = 0;
+  i64 j = (i64)t - 1;
+  for (;;) {
+    u64 w = ld_acquire_u64(ts.status + j);
+    u32 ep = (u32)(w >> 42), fl = (u32)(w >> 40) & 3u;
+    if (ep != ts.epoch || fl == 0) continue;
+    excl += (i64)(w & LB_MASK);
+    if (fl == 2) break;
+    --j;
+  }
+  st_release_u64(ts.status + t, lb_word(ts.epoch, 2, excl + agg));
+  return excl;
+}
+
+// ---------------------------------------------------------------------------
+// The fused count/scan/scatter kernel, parameterised by a row policy P:
+//   P::prepare(DTable& smem)   copy the input descriptor into shared memory
+//   P::rows(smem)              number of input rows (device-resident)
+//   P::count(smem, r, aux, e)  candidates of row r (aux: per-row state)
+//   P::emit(smem, r, aux, j, g) write candidate j of row r to output slot g
+//   P::finish(total)           publish the output row count
+//   P::kAccumE                 accumulate e into st->e (filters)
+// ---------------------------------------------------------------------------
+template <class P>
+__global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
+  __shared__ i64 s_pre[TS_TILE + 1];
+  __shared__ u32 s_aux[TS_TILE];
+  __shared__ i64 s_wsum[TS_THREADS / 32];
+  __shared__ i64 s_base;
+  __shared__ u32 s_tile;
+  __shared__ DTable s_in;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  p.prepare(s_in);
+  __syncthreads();
+  const i64 n = p.rows(s_in);
+  const i64 ntiles = (n + TS_TILE - 1) / TS_TILE;
+  if (ntiles == 0) {
+    if (blockIdx.x == 0 && tid == 0) p.finish(0);
+    return;
+  }
+  i64 e_acc = 0;
+  for (;;) {
+    if (tid == 0) s_tile = atomicAdd(ts.counter, 1u);
+    __syncthreads();
+    const u32 t = s_tile;
+    if ((i64)t >= ntiles) break;
+    const i64 base = (i64)t * TS_TILE;
+#pragma unroll
+    for (int i = 0; i < TS_ITEMS; i++) {
+      const int rl = i * TS_THREADS + tid;
+      const i64 r = base + rl;
+      u32 aux = 0, c = 0;
+      if (r < n) c = p.count(s_in, r, aux, e_acc);
+      s_aux[rl] = aux;
+      s_pre[rl] = c;
+    }
+    __syncthreads();
+    i64 v[TS_ITEMS], sum = 0;
+#pragma unroll
+    for (int i = 0; i < TS_ITEMS; i++) {
+      v[i] = s_pre[tid * TS_ITEMS + i];
+      sum += v[i];
+    }
+    i64 x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      i64 y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    i64 run = x - sum;
+    for (int w = 0; w < warp; w++) run += s_wsum[w];
+#pragma unroll
+    for (int i = 0; i < TS_ITEMS; i++) {
+      s_pre[tid * TS_ITEMS + i] = run;
+      run += v[i];
+    }
+    if (tid == TS_THREADS - 1) s_pre[TS_TILE] = run;
+    __syncthreads();
+    const i64 total = s_pre[TS_TILE];
+    if (tid == 0) s_base = lookback(ts, t, total);
+    __syncthreads();
+    const i64 gbase = s_base;
+    for (i64 k = tid; k < total; k += TS_THREADS) {
+      int lo = 0, hi = TS_TILE;  // s_pre[lo] <= k < s_pre[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pre[mid] <= k) lo = mid; else hi = mid;
+      }
+      p.emit(s_in, base + lo, s_aux[lo], k - s_pre[lo], gbase + k);
+    }
+    if ((i64)t == ntiles - 1 && tid == 0) p.finish(gbase + total);
+    __syncthreads();
+  }
+  if (P::kAccumE) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) e_acc += __shfl_xor_sync(0xffffffffu, e_acc, o);
+    if (lane == 0 && e_acc) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->e), (unsigned long long)e_acc);
+  }
+}
+
+__device__ __forceinline__ void copy_desc(DTable& dst, const DTable* src, int ncols) {
+  const int tid = threadIdx.x;
+  if (tid == 0) dst.n = src->n;
+  if (tid < ncols) dst.col[tid] = src->col[tid];
+}
+
+// J1: one shared variable with a two-variable right pattern -> neighbour expand
+// (sm_join / parallel_sm_join without secondary variables, executor.py:168-194,
+// 218-280).  New column = the other endpoint, read from the CSR/CSC segment.
+struct ExpandP {
+  static constexpr bool kAccumE = false;
+  const DTable* L;
+  Orient R;
+  int li, a;
+  u32* out;
+  i64 cap;
+  DTable* O;
+  StepStat* st;
+  __device__ void prepare(DTable& s) const { copy_desc(s, L, a); }
+  __device__ i64 rows(const DTable& s) const { return s.n; }
+  __device__ u32 count(const DTable& s, i64 r, u32& aux, i64&) const {
+    const uint2 sg = seg_lookup(R, __ldg(s.col[li] + r));
+    aux = sg.x;
+    return sg.y;
+  }
+  __device__ void emit(const DTable& s, i64 r, u32 aux, i64 j, i64 g) const {
+    if (g >= cap) return;
+#pragma unroll 4
+    for (int c = 0; c < a; c++) out[(i64)c * cap + g] = __ldg(s.col[c] + r);
+    out[(i64)a * cap + g] = __ldg(R.dst + aux + j);
+  }
+  __device__ void finish(i64 total) const {
+    O->n = total < cap ? total : cap;
+    st->e = total;
+    st->rows = total;
+    st->overflow = total > cap;
+  }
+};
+
+// J2 / J3: every shared variable is already bound -> membership filter.
+//   F_PAIR  (?s p ?o), both shared: (L[li], L[lj]) in M      E = |segment of J[0]|
+//   F_CONST (?s p C) / (C p ?o):    (L[li], C) in M           E = kept rows
+//   F_SELF  (?x p ?x):              (L[li], L[li]) in M       E = kept rows
+enum { F_PAIR = 0, F_CONST = 1, F_SELF = 2 };
+struct FilterP {
+  static constexpr bool kAccumE = true;
+  const DTable* L;
+  Orient R;
+  int li, lj, a, mode;
+  u32 cval;
+  u32* out;
+  i64 cap;
+  DTable* O;
+  StepStat* st;
+  __device__ void prepare(DTable& s) const { copy_desc(s, L, a); }
+  __device__ i64 rows(const DTable& s) const { return s.n; }
+  __device__ u32 count(const DTable& s, i64 r, u32& aux, i64& e) const {
+    const u32 key = __ldg(s.col[li] + r);
+    const uint2 sg = seg_lookup(R, key);
+    const u32 target = mode == F_PAIR ? __ldg(s.col[lj] + r) : mode == F_CONST ? cval : key;
+    const u32 keep = sg.y ? (u32)sorted_contains(R.dst + sg.x, sg.y, target) : 0u;
+    e += mode == F_PAIR ? (i64)sg.y : (i64)keep;
+    aux = 0;
+    return keep;
+  }
+  __device__ void emit(const DTable& s, i64 r, u32, i64, i64 g) const {
+    if (g >= cap) return;
+#pragma unroll 4
+    for (int c = 0; c < a; c++) out[(i64)c * cap + g] = __ldg(s.col[c] + r);
+  }
+  __device__ void finish(i64 total) const {
+    O->n = total < cap ? total : cap;
+    st->rows = total;
+    st->overflow = total > cap;
+  }
+};
+
+// DISTINCT over packed row-major rows: a row survives iff it wins the CAS
+// into an open-addressing set keyed by the whole tuple (executor.py:360-367).
+struct DistinctP {
+  static constexpr bool kAccumE = false;
+  const u32* in;
+  const StepStat* nsrc;  // input row count = nsrc->rows (capped by cap_in)
+  i64 cap_in;
+  int k;
+  u32* slots;
+  u32 mask;
+  u32* out;
+  StepStat* st;
+  __device__ void prepare(DTable&) const {}
+  __device__ i64 rows(const DTable&) const {
+    i64 n = nsrc->rows;
+    return n < cap_in ? n : cap_in;
+  }
+  __device__ u32 count(const DTable&, i64 r, u32& aux, i64&) const {
+    const u32* row = in + r * k;
+    u32 h = 0x9E3779B9u;
+    for (int c = 0; c < k; c++) h = hash32(h ^ row[c]) + (u32)c;
+    h &= mask;
+    aux = 0;
+    for (;;) {
+      u32 cur = slots[h];
+      if (cur == 0xFFFFFFFFu) {
+        u32 prev = atomicCAS(slots + h, 0xFFFFFFFFu, (u32)r);
+        if (prev == 0xFFFFFFFFu) return 1u;
+        cur = prev;
+      }
+      const u32* other = in + (i64)cur * k;
+      bool eq = true;
+      for (int c = 0; c < k && eq; c++) eq = other[c] == row[c];
+      if (eq) return 0u;
+      h = (h + 1) & mask;
+    }
+  }
+  __device__ void emit(const DTable&, i64 r, u32, i64, i64 g) const {
+    for (int c = 0; c < k; c++) out[g * k + c] = in[r * k + c];
+  }
+  __device__ void finish(i64 total) const { st->rows = total; }
+};
+
+// J0: cross product (executor.py:155-165).  Row g = L[g / |R|] ++ R[g % |R|].
+// stat: e = |L|, pad = |R| (for the budget message); rows = |L|*|R|.
+__global__ void k_cross(const DTable* L, const DTable* R, int a, int b, u32* out, i64 cap,
+                        i64 budget, DTable* O, StepStat* st) {
+  const i64 nl = L->n, nr = R->n;
+  // |L|*|R| saturated at 2^62 (nl, nr < 2^40 in practice)
+  const __int128 t128 = (__int128)nl * (__int128)nr;
+  const i64 total = t128 > ((__int128)1 << 62) ? ((i64)1 << 62) : (i64)t128;
+  const bool skip = total > budget;  // the host raises ResourceLimitError
+  const i64 lim = skip ? 0 : (total < cap ? total : cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    O->n = lim;
+    st->e = nl;
+    st->pad = nr;
+    st->rows = total;
+    st->overflow = !skip && total > cap;
+  }
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 g = (i64)blockIdx.x * blockDim.x + threadIdx.x; g < lim; g += stride) {
+    const i64 i = g / nr, j = g - i * nr;
+    for (int c = 0; c < a; c++) out[(i64)c * cap + g] = __ldg(L->col[c] + i);
+    for (int c = 0; c < b; c++) out[(i64)(a + c) * cap + g] = __ldg(R->col[c] + j);
+  }
+}
+
+// J0 against a zero-arity right table (a constant-constant pattern, R5):
+// the result is the left table itself or nothing -> descriptor aliasing.
+__global__ void k_gate(const DTable* L, const DTable* R, int a, DTable* O, StepStat* st) {
+  const int tid = threadIdx.x;
+  const i64 nl = L->n, nr = R->n;
+  if (tid < a) O->col[tid] = L->col[tid];
+  if (tid == 0) {
+    const i64 total = nr ? nl : 0;
+    O->n = total;
+    st->e = nl;
+    st->pad = nr;
+    st->rows = total;
+  }
+}
+
+// Constant-endpoint scans (executor.py:115-126): one thread per job.
+enum { J_SEG = 0, J_CONTAINS = 1 };
+struct ResolveJob {
+  Orient R;
+  u32 k1, k2;
+  int kind;
+  int table;
+  int stat;  // step whose rows to record, -1 = none
+  int pad;
+};
+struct ResolveArgs {
+  ResolveJob job[GSM_MAX_STEPS];
+  int njobs;
+};
+__global__ void k_resolve(ResolveArgs args, DTable* tables, StepStat* stats) {
+  const int i = threadIdx.x;
+  if (i >= args.njobs) return;
+  const ResolveJob& jb = args.job[i];
+  const uint2 sg = seg_lookup(jb.R, jb.k1);
+  i64 n;
+  if (jb.kind == J_SEG) {
+    n = sg.y;
+    tables[jb.table].col[0] = const_cast<u32*>(jb.R.dst) + sg.x;
+  } else {
+    n = (sg.y && sorted_contains(jb.R.dst + sg.x, sg.y, jb.k2)) ? 1 : 0;
+  }
+  tables[jb.table].n = n;
+  if (jb.stat >= 0) stats[jb.stat].rows = n;
+}
+
+// Multi-GPU row partitioning of the first table: keep rows [n*i/k, n*(i+1)/k).
+__global__ void k_slice(DTable* T, int a, i64 part, i64 parts, StepStat* st) {
+  const i64 n = T->n;
+  const i64 lo = (i64)((__int128)n * part / parts), hi = (i64)((__int128)n * (part + 1) / parts);
+  __syncthreads();
+  if (threadIdx.x < a) T->col[threadIdx.x] += lo;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T->n = hi - lo;
+    st->rows = hi - lo;
+  }
+}
+
+struct ProjArgs {
+  int col[GSM_MAX_VARS];
+};
+// Projection (executor.py:358-359) into row-major u32 rows.
+__global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* out, i64 cap_rows, StepStat* st) {
+  i64 n = T->n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rows = n;
+    st->overflow = n > cap_rows;
+  }
+  if (n > cap_rows) n = cap_rows;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride)
+    for (int c = 0; c < k; c++) out[r * k + c] = __ldg(T->col[pj.col[c]] + r);
+}
+
+}  // namespace gsm
+
+// ===========================================================================
+// Host orchestration
+// ===========================================================================
+using namespace gsm;
+
+namespace {
+
+constexpr int MAX_TABLES = 2 * GSM_MAX_STEPS + 2;
+
+// Device query block: everything a query's kernels read/write besides the
+// store and the arena.  Uploaded in one H2D copy, read back in one D2H copy.
+struct QueryBlock {
+  StepStat stats[GSM_MAX_STEPS + 2];
+  u32 counters[GSM_MAX_STEPS + 4];
+  DTable tables[MAX_TABLES];
+};
+
+enum Home { H_NONE = 0, H_STORE = 1, H_A = 2, H_B = 3 };
+
+enum StepKind { S_SCAN = 0, S_EMPTY, S_EXPAND, S_FILTER, S_CROSS, S_GATE };
+
+struct StepPlan {
+  StepKind kind;
+  std::vector<int> schema;
+  int out_table = -1;
+};
+
+}  // namespace
+
+struct gsm_context {
+  gsm_store* store = nullptr;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  QueryBlock* d_block = nullptr;
+  QueryBlock* h_block = nullptr;  // pinned
+  u64* d_status = nullptr;
+  size_t n_status = 0;
+  u32 epoch = 0;
+  u32* d_slots = nullptr;
+  size_t n_slots = 0;
+  int grid_ts = 296;
+  cudaEvent_t ev[GSM_MAX_STEPS + 2] = {};
+  cudaEvent_t ev_q0 = nullptr, ev_q1 = nullptr;  // whole-query device time
+};
+
+namespace {
+
+gsm_status ctx_set_arena(gsm_context* c, size_t bytes) {
+  if (c->arena) {
+    cudaFree(c->arena);
+    c->arena = nullptr;
+  }
+  if (c->d_status) {
+    cudaFree(c->d_status);
+    c->d_status = nullptr;
+  }
+  bytes = (bytes + 255) & ~(size_t)255;
+  GSM_CUDA(cudaMalloc(&c->arena, bytes));
+  c->arena_bytes = bytes;
+  size_t half = bytes / 2;
+  size_t max_rows = std::max<size_t>(half / 4, c->store->max_nnz) + 1;
+  c->n_status = max_rows / TS_TILE + 2;
+  GSM_CUDA(cudaMalloc(&c->d_status, c->n_status * sizeof(u64)));
+  GSM_CUDA(cudaMemset(c->d_status, 0, c->n_status * sizeof(u64)));
+  c->epoch = 0;
+  return GSM_OK;
+}
+
+u32 next_epoch(gsm_context* c) {
+  if (++c->epoch > EPOCH_MAX) {
+    cudaMemsetAsync(c->d_status, 0, c->n_status * sizeof(u64), c->stream);
+    c->epoch = 1;
+  }
+  return c->epoch;
+}
+
+int index_of(const std::vector<int>& v, int x) {
+  for (size_t i = 0; i < v.size(); i++)
+    if (v[i] == x) return (int)i;
+  return -1;
+}
+
+// Right-pattern schema (executor.py:101-110).
+std::vector<int> pattern_schema(const gsm_pattern& p) {
+  bool sv = p.s_var >= 0, ov = p.o_var >= 0;
+  if (sv && ov) return p.s_var == p.o_var ? std::vector<int>{p.s_var} : std::vector<int>{p.s_var, p.o_var};
+  if (sv) return {p.s_var};
+  if (ov) return {p.o_var};
+  return {};
+}
+
+struct Exec {
+  gsm_context* c;
+  const gsm_pattern* steps;
+  int n;
+  QueryBlock* hb;
+  std::vector<StepPlan> plan;
+  std::vector<Home> home;  // per table
+  std::vector<int> arity;  // per table
+  int ntables = 0;
+  ResolveArgs res{};
+  size_t half;
+
+  const PredDev* pred(const gsm_pattern& p) const {
+    if (p.empty || p.pid < 1 || p.pid > c->store->max_pid) return nullptr;
+    const PredDev& d = c->store->preds[p.pid];
+    return d.present ? &d : nullptr;
+  }
+  char* buf(Home h) const { return c->arena + (h == H_B ? half : 0); }
+  int new_table(int a, Home h) {
+    int t = ntables++;
+    home.push_back(h);
+    arity.push_back(a);
+    DTable& d = hb->tables[t];
+    d.n = 0;
+    for (int i = 0; i < GSM_MAX_VARS; i++) d.col[i] = nullptr;
+    if (h == H_A || h == H_B) {
+      i64 cap = cap_for(a);
+      for (int i = 0; i < a; i++) d.col[i] = reinterpret_cast<u32*>(buf(h)) + (i64)i * cap;
+    }
+    return t;
+  }
+  i64 cap_for(int a) const { return a == 0 ? ((i64)1 << 62) : (i64)(half / (4 * (size_t)a)); }
+  static Home other(Home h) { return h == H_A ? H_B : H_A; }
+
+  // Zero-copy table for a pattern read as a whole table (first step, or the
+  // right side of a cross product).  Returns table index.
+  int scan_table(const gsm_pattern& p, int stat) {
+    std::vector<int> sch = pattern_schema(p);
+    const PredDev* m = pred(p);
+    int t = new_table((int)sch.size(), H_STORE);
+    DTable& d = hb->tables[t];
+    if (!m) {  // R6: empty flag or no matrix -> zero rows, schema kept
+      d.n = 0;
+      if (stat >= 0) hb->stats[stat].rows = 0;
+      return t;
+    }
+    bool sv = p.s_var >= 0, ov = p.o_var >= 0;
+    if (sv && ov && p.s_var != p.o_var) {  // R1: so_pairs
+      d.n = m->so.nnz;
+      d.col[0] = const_cast<u32*>(m->so.src);
+      d.col[1] = const_cast<u32*>(m->so.dst);
+      if (stat >= 0) hb->stats[stat].rows = d.n;
+    } else if (sv && ov) {  // R4: diagonal
+      d.n = m->ndiag;
+      d.col[0] = const_cast<u32*>(m->diag);
+      if (stat >= 0) hb->stats[stat].rows = d.n;
+    } else {
+      ResolveJob& j = res.job[res.njobs++];
+      j.table = t;
+      j.stat = stat;
+      if (sv) {  // R2 (?s p C): pairs_for_object(C) -> s values (os segment)
+        j.kind = J_SEG;
+        j.R = m->os;
+        j.k1 = p.o_const;
+      } else if (ov) {  // R3 (C p ?o): pairs_for_subject(C) -> o values
+        j.kind = J_SEG;
+        j.R = m->so;
+        j.k1 = p.s_const;
+      } else {  // R5 (C p C'): contains
+        j.kind = J_CONTAINS;
+        j.R = m->so;
+        j.k1 = p.s_const;
+        j.k2 = p.o_const;
+      }
+    }
+    return t;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context** out) {
+  *out = nullptr;
+  if (!store || !store->finalized) return set_error(GSM_ERR_VALUE, "store missing or not finalized");
+  GSM_CUDA(cudaSetDevice(store->device));
+  gsm_context* c = new gsm_context();
+  c->store = store;
+  c->device = store->device;
+  auto fail = [&](gsm_status st) {
+    gsm_context_free(c);
+    return st;
+  };
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(cuda_error(e, "cudaStreamCreate"));
+  if ((e = cudaMalloc(&c->d_block, sizeof(QueryBlock))) != cudaSuccess)
+    return fail(cuda_error(e, "cudaMalloc(query block)"));
+  if ((e = cudaMallocHost(&c->h_block, sizeof(QueryBlock))) != cudaSuccess)
+    return fail(cuda_error(e, "cudaMallocHost(query block)"));
+  for (auto& ev : c->ev)
+    if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(cuda_error(e, "cudaEventCreate"));
+  if ((e = cudaEventCreate(&c->ev_q0)) != cudaSuccess || (e = cudaEventCreate(&c->ev_q1)) != cudaSuccess)
+    return fail(cuda_error(e, "cudaEventCreate"));
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  size_t want = arena_bytes > 0 ? (size_t)arena_bytes
+                                : std::min<size_t>((size_t)1 << 32, free_b / 4);
+  gsm_status st = ctx_set_arena(c, want);
+  if (st != GSM_OK) return fail(st);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tilescan<ExpandP>, TS_THREADS, 0);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  c->grid_ts = sms * std::max(1, std::min(occ, 4));
+  *out = c;
+  return GSM_OK;
+}
+
+gsm_status gsm_context_free(gsm_context* c) {
+  if (!c) return GSM_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->arena) cudaFree(c->arena);
+  if (c->d_status) cudaFree(c->d_status);
+  if (c->d_block) cudaFree(c->d_block);
+  if (c->h_block) cudaFreeHost(c->h_block);
+  if (c->d_slots) cudaFree(c->d_slots);
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->ev_q0) cudaEventDestroy(c->ev_q0);
+  if (c->ev_q1) cudaEventDestroy(c->ev_q1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return GSM_OK;
+}
+
+static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
+                           int32_t n_proj, int64_t budget, int64_t part, int64_t parts,
+                           bool timing, Exec& ex, int& pack_stat, i64& pack_cap, u32*& pack_out,
+                           bool& overflow, int& kernels, i64& h2d) {
+  kernels = 0;
+  QueryBlock* hb = c->h_block;
+  ex.c = c;
+  ex.steps = steps;
+  ex.n = n;
+  ex.hb = hb;
+  ex.half = c->arena_bytes / 2;
+  ex.plan.assign(n, StepPlan());
+  memset(hb->stats, 0, sizeof(hb->stats));
+  memset(hb->counters, 0, sizeof(hb->counters));
+
+  DTable* dT = c->d_block->tables;
+  StepStat* dS = c->d_block->stats;
+  u32* dC = c->d_block->counters;
+
+  // ---- step 0: scan ----
+  int cur = ex.scan_table(steps[0], 0);
+  std::vector<int> schema = pattern_schema(steps[0]);
+  ex.plan[0].kind = S_SCAN;
+  ex.plan[0].schema = schema;
+  ex.plan[0].out_table = cur;
+
+  // ---- plan the joins (executor.py:340-356) and build right tables ----
+  struct Launch {
+    StepKind kind;
+    int step, left, right, out;
+    ExpandP ep;
+    FilterP fp;
+    int a, b;
+  };
+  std::vector<Launch> launches;
+  for (int s = 1; s < n; s++) {
+    const gsm_pattern& p = steps[s];
+    std::vector<int> rs = pattern_schema(p);
+    std::vector<int> jv;
+    for (int v : schema)
+      if (index_of(rs, v) >= 0) jv.push_back(v);
+    const PredDev* m = ex.pred(p);
+    Launch L{};
+    L.step = s;
+    L.left = cur;
+    std::vector<int> out_schema = schema;
+    if (jv.empty()) {
+      for (int v : rs) out_schema.push_back(v);
+    } else {
+      for (int v : rs)
+        if (index_of(schema, v) < 0) out_schema.push_back(v);
+    }
+    if ((int)out_schema.size() > GSM_MAX_VARS)
+      return set_error(GSM_ERR_VALUE, "query binds more than " + std::to_string(GSM_MAX_VARS) + " variables");
+    const int a = (int)schema.size();
+    if (!m) {
+      // R6 right side: the join (or cross product) is empty, E = 0.
+      L.kind = S_EMPTY;
+      L.out = ex.new_table((int)out_schema.size(), H_NONE);
+    } else if (jv.empty()) {
+      int rt = ex.scan_table(p, -1);
+      L.right = rt;
+      if (rs.empty()) {
+        L.kind = S_GATE;
+        L.out = ex.new_table(a, ex.home[cur]);
+      } else {
+        L.kind = S_CROSS;
+        L.out = ex.new_table((int)out_schema.size(), Exec::other(ex.home[cur]));
+        L.a = a;
+        L.b = (int)rs.size();
+      }
+    } else {
+      Home oh = Exec::other(ex.home[cur]);
+      bool sv = p.s_var >= 0, ov = p.o_var >= 0;
+      if (sv && ov && p.s_var != p.o_var && jv.size() == 1) {
+        L.kind = S_EXPAND;
+        L.out = ex.new_table((int)out_schema.size(), oh);
+        ExpandP& e = L.ep;
+        bool on_s = jv[0] == p.s_var;
+        e.R = on_s ? m->so : m->os;
+        e.li = index_of(schema, jv[0]);
+        e.a = a;
+        e.L = dT + cur;
+        e.out = reinterpret_cast<u32*>(ex.buf(oh));
+        e.cap = ex.cap_for((int)out_schema.size());
+        e.O = dT + L.out;
+        e.st = dS + s;
+      } else {
+        L.kind = S_FILTER;
+        L.out = ex.new_table(a, oh);
+        FilterP& f = L.fp;
+        f.a = a;
+        f.L = dT + cur;
+        f.out = reinterpret_cast<u32*>(ex.buf(oh));
+        f.cap = ex.cap_for(a);
+        f.O = dT + L.out;
+        f.st = dS + s;
+        f.li = index_of(schema, jv[0]);
+        f.lj = -1;
+        f.cval = 0;
+        if (sv && ov && p.s_var != p.o_var) {  // J2: first join var drives (executor.py:141-145)
+          f.mode = F_PAIR;
+          bool on_s = jv[0] == p.s_var;
+          f.R = on_s ? m->so : m->os;
+          f.lj = index_of(schema, on_s ? p.o_var : p.s_var);
+        } else if (sv && ov) {  // R4 (?x p ?x)
+          f.mode = F_SELF;
+          f.R = m->so;
+        } else if (sv) {  // R2 (?s p C): (s, C) in M
+          f.mode = F_CONST;
+          f.R = m->so;
+          f.cval = p.o_const;
+        } else {  // R3 (C p ?o): (C, o) in M
+          f.mode = F_CONST;
+          f.R = m->os;
+          f.cval = p.s_const;
+        }
+      }
+    }
+    ex.plan[s].kind = L.kind;
+    ex.plan[s].schema = out_schema;
+    ex.plan[s].out_table = L.out;
+    launches.push_back(L);
+    schema = out_schema;
+    cur = L.out;
+  }
+
+  // ---- projection target ----
+  int pj_idx[GSM_MAX_VARS];
+  if (n_proj > GSM_MAX_VARS) return set_error(GSM_ERR_VALUE, "too many projected variables");
+  for (int j = 0; j < n_proj; j++) {
+    pj_idx[j] = index_of(schema, proj[j]);
+    if (pj_idx[j] < 0) return set_error(GSM_ERR_VALUE, "projected variable is not bound by the plan");
+  }
+  Home ph = ex.home[cur] == H_A ? H_B : H_A;
+  pack_out = reinterpret_cast<u32*>(ex.buf(ph));
+  pack_cap = n_proj ? (i64)(ex.half / (4 * (size_t)n_proj)) : ((i64)1 << 62);
+  pack_stat = n;
+
+  // ---- upload the query block (stats, counters, used descriptors) ----
+  size_t used = offsetof(QueryBlock, tables) + sizeof(DTable) * (size_t)ex.ntables;
+  cudaStream_t st = c->stream;
+  if (timing) GSM_CUDA(cudaEventRecord(c->ev_q0, st));
+  GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
+  h2d = (i64)used;
+
+  if (timing) GSM_CUDA(cudaEventRecord(c->ev[0], st));
+  if (ex.res.njobs > 0) {
+    k_resolve<<<1, 64, 0, st>>>(ex.res, dT, dS);
+    count_launch();
+        kernels++;
+  }
+  if (parts > 1) {
+    k_slice<<<1, 64, 0, st>>>(dT + ex.plan[0].out_table, (int)ex.plan[0].schema.size(), part, parts,
+                              dS + 0);
+    count_launch();
+        kernels++;
+  }
+  if (timing) GSM_CUDA(cudaEventRecord(c->ev[1], st));
+  int counter = 0;
+  for (auto& L : launches) {
+    switch (L.kind) {
+      case S_EMPTY:
+        break;  // descriptor n = 0 and zero stats were uploaded
+      case S_EXPAND: {
+        TileSync ts{c->d_status, dC + counter++, next_epoch(c)};
+        k_tilescan<ExpandP><<<c->grid_ts, TS_THREADS, 0, st>>>(L.ep, ts);
+        count_launch();
+        kernels++;
+        break;
+      }
+      case S_FILTER: {
+        TileSync ts{c->d_status, dC + counter++, next_epoch(c)};
+        k_tilescan<FilterP><<<c->grid_ts, TS_THREADS, 0, st>>>(L.fp, ts);
+        count_launch();
+        kernels++;
+        break;
+      }
+      case S_CROSS: {
+        Home oh = ex.home[L.out];
+        k_cross<<<c->grid_ts, 256, 0, st>>>(dT + L.left, dT + L.right, L.a, L.b,
+                                             reinterpret_cast<u32*>(ex.buf(oh)),
+                                             ex.cap_for(L.a + L.b), budget, dT + L.out, dS + L.step);
+        count_launch();
+        kernels++;
+        break;
+      }
+      case S_GATE:
+        k_gate<<<1, 64, 0, st>>>(dT + L.left, dT + L.right, ex.arity[L.left], dT + L.out, dS + L.step);
+        count_launch();
+        kernels++;
+        break;
+      default:
+        break;
+    }
+    if (timing) GSM_CUDA(cudaEventRecord(c->ev[L.step + 1], st));
+  }
+  ProjArgs pa{};
+  for (int j = 0; j < n_proj; j++) pa.col[j] = pj_idx[j];
+  k_pack<<<c->grid_ts, 256, 0, st>>>(dT + cur, pa, n_proj, pack_out, pack_cap, dS + pack_stat);
+  count_launch();
+        kernels++;
+  GSM_CUDA(cudaGetLastError());
+  GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(hb->stats), cudaMemcpyDeviceToHost, st));
+  GSM_CUDA(cudaStreamSynchronize(st));
+
+  overflow = false;
+  for (int s = 1; s < n; s++)
+    if (hb->stats[s].overflow) overflow = true;
+  if (hb->stats[pack_stat].overflow) overflow = true;
+  return GSM_OK;
+}
+
+gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
+                       int32_t n_proj, int32_t distinct, int64_t budget, int32_t budget_mode,
+                       int64_t part, int64_t parts, gsm_report* rep, gsm_result** out) {
+  *out = nullptr;
+  if (!c) return set_error(GSM_ERR_VALUE, "null context");
+  if (n <= 0) return set_error(GSM_ERR_VALUE, "cannot execute an empty plan");
+  if (n > GSM_MAX_STEPS) return set_error(GSM_ERR_VALUE, "plan has more than 64 steps");
+  if (n_proj < 0 || (n_proj > 0 && !proj)) return set_error(GSM_ERR_VALUE, "bad projection");
+  if (parts < 1 || part < 0 || part >= parts) return set_error(GSM_ERR_VALUE, "bad partition");
+  if (budget_mode != GSM_BUDGET_SEQUENTIAL && budget_mode != GSM_BUDGET_PARALLEL)
+    return set_error(GSM_ERR_VALUE, "bad budget mode");
+  for (int s = 0; s < n; s++) {
+    const gsm_pattern& p = steps[s];
+    if (p.s_var >= GSM_MAX_VARS || p.o_var >= GSM_MAX_VARS || p.s_var < -1 || p.o_var < -1)
+      return set_error(GSM_ERR_VALUE, "variable index out of range");
+  }
+  GSM_CUDA(cudaSetDevice(c->device));
+  const bool timing = rep && rep->device_ms;
+
+  Exec ex{};
+  int pack_stat = 0;
+  i64 pack_cap = 0;
+  u32* pack_out = nullptr;
+  bool overflow = false;
+  int kernels = 0;
+  i64 h2d = 0;
+  for (int attempt = 0;; attempt++) {
+    ex = Exec{};
+    gsm_status stt = run_once(c, steps, n, proj, n_proj, budget, part, parts, timing, ex, pack_stat,
+                              pack_cap, pack_out, overflow, kernels, h2d);
+    if (stt != GSM_OK) return stt;
+    const QueryBlock* hb = c->h_block;
+    // Budget checks in plan order (executor.py:158-163, 192-193, 237-241).
+    // A step's counters are exact as long as no earlier step overflowed.
+    i64 need_rows = 0;
+    int need_arity = 1;
+    bool ovf = false;
+    for (int s = 1; s < n && !ovf; s++) {
+      const StepStat& q = hb->stats[s];
+      StepKind k = ex.plan[s].kind;
+      char msg[256];
+      if (k == S_CROSS || k == S_GATE) {
+        i64 nl = q.e, nr = q.pad, tot = 0;
+        bool big = __builtin_mul_overflow(nl, nr, &tot);
+        if (big || tot > budget) {
+          snprintf(msg, sizeof msg, "cross product of %lld x %lld rows exceeds budget %lld",
+                   (long long)nl, (long long)nr, (long long)budget);
+          return set_error(GSM_ERR_RESOURCE, msg);
+        }
+      } else if (k == S_EXPAND || k == S_FILTER) {
+        if (budget_mode == GSM_BUDGET_PARALLEL && q.e > budget) {
+          snprintf(msg, sizeof msg, "pre-allocated join region of %lld rows exceeds budget %lld",
+                   (long long)q.e, (long long)budget);
+          return set_error(GSM_ERR_RESOURCE, msg);
+        }
+        if (budget_mode == GSM_BUDGET_SEQUENTIAL && q.rows > budget) {
+          snprintf(msg, sizeof msg, "join output exceeds row budget %lld", (long long)budget);
+          return set_error(GSM_ERR_RESOURCE, msg);
+        }
+      }
+      if (q.overflow) {
+        ovf = true;
+        need_rows = q.rows;
+        need_arity = (int)ex.plan[s].schema.size();
+      }
+    }
+    if (!ovf && hb->stats[pack_stat].overflow) {
+      ovf = true;
+      need_rows = hb->stats[pack_stat].rows;
+      need_arity = n_proj;
+    }
+    if (!ovf) break;
+    // Intermediate table larger than the arena half: grow and re-run.
+    size_t need = (size_t)need_rows * 4 * (size_t)std::max(need_arity, 1) * 2;
+    size_t grow = std::max(need + need / 4, c->arena_bytes * 2);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    size_t avail = free_b + c->arena_bytes;
+    if (attempt >= 8 || need > (avail * 9) / 10) {
+      char msg[256];
+      snprintf(msg, sizeof msg,
+               "intermediate result of %lld rows x %d columns exceeds device memory",
+               (long long)need_rows, need_arity);
+      return set_error(GSM_ERR_RESOURCE, msg);
+    }
+    grow = std::min(grow, (avail * 9) / 10);
+    gsm_status s2 = ctx_set_arena(c, grow);
+    if (s2 != GSM_OK) return s2;
+  }
+
+  const QueryBlock* hb = c->h_block;
+  if (rep) {
+    for (int s = 0; s < n; s++) {
+      StepKind k = ex.plan[s].kind;
+      if (rep->kind) rep->kind[s] = (int32_t)k;
+      if (rep->arity) rep->arity[s] = (int32_t)ex.plan[s].schema.size();
+      if (rep->rows) rep->rows[s] = hb->stats[s].rows;
+      if (rep->prealloc_total)
+        rep->prealloc_total[s] = (k == S_EXPAND || k == S_FILTER) ? hb->stats[s].e : 0;
+      if (rep->device_ms) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev[s], c->ev[s + 1]);
+        rep->device_ms[s] = ms;
+      }
+    }
+  }
+
+  i64 nrows = hb->stats[pack_stat].rows;
+  gsm_result* r = new gsm_result();
+  r->device = c->device;
+  r->k = n_proj;
+  cudaStream_t st = c->stream;
+  if (distinct && nrows > 1) {
+    size_t cap = 16;
+    while (cap < 2 * (size_t)nrows) cap <<= 1;
+    if (cap > c->n_slots) {
+      if (c->d_slots) cudaFree(c->d_slots);
+      c->d_slots = nullptr;
+      cudaError_t e = cudaMalloc(&c->d_slots, cap * 4);
+      if (e != cudaSuccess) {
+        delete r;
+        c->n_slots = 0;
+        return cuda_error(e, "cudaMalloc(distinct slots)");
+      }
+      c->n_slots = cap;
+    }
+    u32* tmp = nullptr;
+    cudaError_t e = cudaMalloc(&tmp, std::max<size_t>(4, (size_t)nrows * n_proj * 4));
+    if (e != cudaSuccess) {
+      delete r;
+      return cuda_error(e, "cudaMalloc(result)");
+    }
+    GSM_CUDA(cudaMemsetAsync(c->d_slots, 0xFF, cap * 4, st));
+    DistinctP dp{};
+    dp.in = pack_out;
+    dp.nsrc = c->d_block->stats + pack_stat;
+    dp.cap_in = pack_cap;
+    dp.k = n_proj;
+    dp.slots = c->d_slots;
+    dp.mask = (u32)(cap - 1);
+    dp.out = tmp;
+    dp.st = c->d_block->stats + pack_stat + 1;
+    GSM_CUDA(cudaMemsetAsync(c->d_block->counters + GSM_MAX_STEPS + 2, 0, 4, st));
+    TileSync ts{c->d_status, c->d_block->counters + GSM_MAX_STEPS + 2, next_epoch(c)};
+    k_tilescan<DistinctP><<<c->grid_ts, TS_THREADS, 0, st>>>(dp, ts);
+    count_launch();
+    kernels++;
+    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
+    StepStat ds{};
+    GSM_CUDA(cudaMemcpyAsync(&c->h_block->stats[pack_stat + 1], dp.st, sizeof(StepStat),
+                             cudaMemcpyDeviceToHost, st));
+    GSM_CUDA(cudaStreamSynchronize(st));
+    ds = c->h_block->stats[pack_stat + 1];
+    r->n = ds.rows;
+    r->rows = tmp;
+  } else {
+    r->n = nrows;
+    size_t bytes = (size_t)nrows * n_proj * 4;
+    cudaError_t e = cudaMalloc(&r->rows, std::max<size_t>(bytes, 4));
+    if (e != cudaSuccess) {
+      delete r;
+      return cuda_error(e, "cudaMalloc(result)");
+    }
+    if (bytes) GSM_CUDA(cudaMemcpyAsync(r->rows, pack_out, bytes, cudaMemcpyDeviceToDevice, st));
+    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
+    GSM_CUDA(cudaStreamSynchronize(st));
+  }
+  if (rep) {
+    rep->kernels = kernels;
+    rep->h2d_bytes = h2d;
+    rep->d2h_bytes = (i64)sizeof(c->h_block->stats) + (distinct && nrows > 1 ? (i64)sizeof(StepStat) : 0);
+    rep->total_device_ms = 0.f;
+    if (timing) cudaEventElapsedTime(&rep->total_device_ms, c->ev_q0, c->ev_q1);
+  }
+  *out = r;
+  return GSM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,28 @@
+// gsm_internal.cuh — host-side objects behind the C ABI handles.
+#pragma once
+#include <vector>
+
+#include "gsm_common.cuh"
+
+struct gsm_store {
+  int device = 0;
+  i64 node_count = 0;
+  int max_pid = 0;
+  std::vector<gsm::PredDev> preds;  // indexed by pid (0 unused)
+  std::vector<void*> allocations;
+  i64 bytes = 0;
+  u32 max_nnz = 0;
+  bool finalized = false;
+  u32* d_flag = nullptr;  // validation scratch: [0] min unsorted-key pos, [1] min unsorted-value pos, [2] id overflow
+};
+
+struct gsm_result {
+  int device = 0;
+  i64 n = 0;
+  int k = 0;
+  u32* rows = nullptr;  // device, row-major n x k
+};
+
+namespace gsm {
+cudaError_t store_alloc(gsm_store* s, void** p, size_t bytes);
+}

@@ -1,0 +1,309 @@
+// gsm_store.cu — HBM-resident predicate matrices and their row indexes.
+//
+// Replaces storage.PredicateMatrix / build_aux / Store.matrices
+// (/root/reference/pkg/src/gsmat/storage.py:38-122).  The pair files are
+// uploaded as-is (u64 LE pairs, storage.py:183-200) and narrowed to u32
+// columns on the device; all index structures are built by device kernels.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+
+#include "gsm_internal.cuh"
+
+namespace gsm {
+
+cudaError_t store_alloc(gsm_store* s, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes ? bytes : 4);
+  if (e == cudaSuccess) {
+    s->allocations.push_back(*p);
+    s->bytes += (i64)bytes;
+  }
+  return e;
+}
+
+// Split interleaved u64 pairs into u32 key/value columns and validate order.
+// flag[0]: min position with key < previous key (build_aux's ValueError,
+// storage.py:44-45); flag[1]: min position whose value breaks ascending order
+// inside a key run; flag[2]: an id >= 2^32.
+__global__ void k_narrow_pairs(const u64* __restrict__ pairs, u32* __restrict__ src,
+                               u32* __restrict__ dst, i64 chunk_begin, i64 n,
+                               u32* __restrict__ flag) {
+  i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    ulonglong2 pr = reinterpret_cast<const ulonglong2*>(pairs)[i];
+    if ((pr.x >> 32) | (pr.y >> 32)) atomicExch(flag + 2, 1u);
+    src[chunk_begin + i] = (u32)pr.x;
+    dst[chunk_begin + i] = (u32)pr.y;
+  }
+}
+
+__global__ void k_check_sorted(const u32* __restrict__ src, const u32* __restrict__ dst, i64 n,
+                               u32* __restrict__ flag) {
+  i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = 1 + (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 a = src[i - 1], b = src[i];
+    if (b < a) atomicMin(flag + 0, (u32)i);
+    else if (b == a && dst[i] < dst[i - 1]) atomicMin(flag + 1, (u32)i);
+  }
+}
+
+__device__ __forceinline__ u32 lower_bound_u32(const u32* a, u32 n, u32 v) {
+  u32 lo = 0, hi = n;
+  while (lo < hi) {
+    u32 mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Dense key index: doff[v] = first position with src >= v, v in [0, maxkey+1].
+__global__ void k_dense_index(const u32* __restrict__ src, u32 nnz, u32* __restrict__ doff,
+                              u32 nkeys) {
+  u32 stride = gridDim.x * blockDim.x;
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < nkeys; v += stride)
+    doff[v] = lower_bound_u32(src, nnz, v);
+}
+
+__global__ void k_count_heads(const u32* __restrict__ src, u32 nnz, u32* __restrict__ out) {
+  u32 stride = gridDim.x * blockDim.x, c = 0;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride)
+    c += (i == 0 || src[i] != src[i - 1]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// Hash key index: one {key, begin, len} slot per aux-array entry.
+__global__ void k_hash_index(const u32* __restrict__ src, u32 nnz, u32* __restrict__ slots,
+                             u32 mask) {
+  u32 stride = gridDim.x * blockDim.x;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    u32 key = src[i];
+    if (i != 0 && src[i - 1] == key) continue;
+    u32 end = i + lower_bound_u32(src + i, nnz - i, key + 1);
+    u32 h = hash32(key) & mask;
+    for (;;) {
+      u32 prev = atomicCAS(slots + 4 * h, 0u, key);
+      if (prev == 0u) {
+        slots[4 * h + 1] = i;
+        slots[4 * h + 2] = end - i;
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+struct DiagFlag {
+  const u32* src;
+  const u32* dst;
+  __device__ bool operator()(const u32& i) const { return src[i] == dst[i]; }
+};
+
+__global__ void k_gather_u32(const u32* __restrict__ idx, const u32* __restrict__ n_dev,
+                             const u32* __restrict__ vals, u32* __restrict__ out) {
+  u32 n = *n_dev;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = vals[idx[i]];
+}
+
+static int grid_for(i64 n, int threads = 256) {
+  i64 b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)b;
+}
+
+static gsm_status build_orient(gsm_store* s, Orient& o) {
+  if (o.nnz == 0) return GSM_OK;
+  // distinct keys (len of the aux array, storage.py:38-53)
+  u32* d_cnt;
+  GSM_CUDA(cudaMalloc(&d_cnt, 4));
+  GSM_CUDA(cudaMemset(d_cnt, 0, 4));
+  k_count_heads<<<grid_for(o.nnz), 256>>>(o.src, o.nnz, d_cnt);
+  count_launch();
+  GSM_CUDA(cudaMemcpy(&o.nrows, d_cnt, 4, cudaMemcpyDeviceToHost));
+  cudaFree(d_cnt);
+  size_t cap = 16;
+  while (cap < 2 * (size_t)o.nrows) cap <<= 1;
+  size_t hash_bytes = cap * 16, dense_bytes = 4 * ((size_t)s->node_count + 2);
+  if (dense_bytes <= 2 * hash_bytes) {
+    u32* doff;
+    GSM_CUDA(store_alloc(s, (void**)&doff, dense_bytes));
+    u32 nkeys = (u32)(s->node_count + 2);
+    k_dense_index<<<grid_for(nkeys), 256>>>(o.src, o.nnz, doff, nkeys);
+    count_launch();
+    o.doff = doff;
+    o.maxkey = (u32)(s->node_count);
+  } else {
+    u32* slots;
+    GSM_CUDA(store_alloc(s, (void**)&slots, hash_bytes));
+    GSM_CUDA(cudaMemset(slots, 0, hash_bytes));
+    k_hash_index<<<grid_for(o.nnz), 256>>>(o.src, o.nnz, slots, (u32)(cap - 1));
+    count_launch();
+    o.hs = reinterpret_cast<const uint4*>(slots);
+    o.hmask = (u32)(cap - 1);
+  }
+  GSM_CUDA(cudaGetLastError());
+  return GSM_OK;
+}
+
+static gsm_status build_diag(gsm_store* s, PredDev& p) {
+  const Orient& o = p.so;
+  if (o.nnz == 0) return GSM_OK;
+  u32 *d_idx, *d_n;
+  GSM_CUDA(cudaMalloc(&d_idx, 4 * (size_t)o.nnz));
+  GSM_CUDA(cudaMalloc(&d_n, 4));
+  thrust::counting_iterator<u32> it(0);
+  size_t tmp_bytes = 0;
+  DiagFlag f{o.src, o.dst};
+  cub::DeviceSelect::If(nullptr, tmp_bytes, it, d_idx, d_n, (int)o.nnz, f);
+  void* tmp;
+  GSM_CUDA(cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 4));
+  cub::DeviceSelect::If(tmp, tmp_bytes, it, d_idx, d_n, (int)o.nnz, f);
+  count_launch(2);
+  u32 nd = 0;
+  GSM_CUDA(cudaMemcpy(&nd, d_n, 4, cudaMemcpyDeviceToHost));
+  u32* diag;
+  GSM_CUDA(store_alloc(s, (void**)&diag, 4 * (size_t)nd));
+  if (nd) {
+    k_gather_u32<<<grid_for(nd), 256>>>(d_idx, d_n, o.src, diag);
+    count_launch();
+  }
+  p.diag = diag;
+  p.ndiag = nd;
+  cudaFree(tmp);
+  cudaFree(d_idx);
+  cudaFree(d_n);
+  GSM_CUDA(cudaGetLastError());
+  return GSM_OK;
+}
+
+}  // namespace gsm
+
+using namespace gsm;
+
+extern "C" {
+
+gsm_status gsm_store_create(int32_t device, int64_t node_count, int32_t max_pid, gsm_store** out) {
+  *out = nullptr;
+  if (node_count < 0 || node_count > 0xFFFFFFF0LL)
+    return set_error(GSM_ERR_VALUE, "node_count must be in [0, 2^32-16)");
+  if (max_pid < 0) return set_error(GSM_ERR_VALUE, "max_pid must be >= 0");
+  int ndev = 0;
+  GSM_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return set_error(GSM_ERR_VALUE, "device index out of range");
+  GSM_CUDA(cudaSetDevice(device));
+  gsm_store* s = new gsm_store();
+  s->device = device;
+  s->node_count = node_count;
+  s->max_pid = max_pid;
+  s->preds.resize((size_t)max_pid + 1);
+  cudaError_t e = cudaMalloc(&s->d_flag, 16);
+  if (e != cudaSuccess) {
+    delete s;
+    return cuda_error(e, "cudaMalloc(flags)");
+  }
+  *out = s;
+  return GSM_OK;
+}
+
+gsm_status gsm_store_put_predicate(gsm_store* s, int32_t pid, const uint64_t* so_pairs,
+                                   const uint64_t* os_pairs, int64_t nnz) {
+  if (!s) return set_error(GSM_ERR_VALUE, "null store");
+  if (s->finalized) return set_error(GSM_ERR_VALUE, "store already finalized");
+  if (pid < 1 || pid > s->max_pid) return set_error(GSM_ERR_UNKNOWN_PREDICATE, "no matrix for predicate id " + std::to_string(pid));
+  if (nnz < 0 || nnz >= 0xFFFFFFF0LL)
+    return set_error(GSM_ERR_VALUE, "predicate pair count must be < 2^32");
+  if (nnz > 0 && (!so_pairs || !os_pairs)) return set_error(GSM_ERR_VALUE, "null pair array");
+  GSM_CUDA(cudaSetDevice(s->device));
+  PredDev& p = s->preds[pid];
+  if (p.present) return set_error(GSM_ERR_VALUE, "predicate uploaded twice");
+  p.present = 1;
+  const i64 CHUNK = 1 << 24;  // 16M pairs = 256 MiB staging
+  u64* stage = nullptr;
+  if (nnz > 0) GSM_CUDA(cudaMalloc(&stage, 16 * (size_t)std::min<i64>(nnz, CHUNK)));
+  const uint64_t* hosts[2] = {so_pairs, os_pairs};
+  Orient* ors[2] = {&p.so, &p.os};
+  for (int w = 0; w < 2; w++) {
+    Orient& o = *ors[w];
+    u32 *src, *dst;
+    GSM_CUDA(store_alloc(s, (void**)&src, 4 * (size_t)nnz));
+    GSM_CUDA(store_alloc(s, (void**)&dst, 4 * (size_t)nnz));
+    o.src = src;
+    o.dst = dst;
+    o.nnz = (u32)nnz;
+    u32 init[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u};
+    GSM_CUDA(cudaMemcpy(s->d_flag, init, 16, cudaMemcpyHostToDevice));
+    for (i64 b = 0; b < nnz; b += CHUNK) {
+      i64 m = std::min<i64>(CHUNK, nnz - b);
+      GSM_CUDA(cudaMemcpy(stage, hosts[w] + 2 * b, 16 * (size_t)m, cudaMemcpyHostToDevice));
+      k_narrow_pairs<<<grid_for(m), 256>>>(stage, src, dst, b, m, s->d_flag);
+      count_launch();
+    }
+    if (nnz > 1) {
+      k_check_sorted<<<grid_for(nnz), 256>>>(src, dst, nnz, s->d_flag);
+      count_launch();
+    }
+    u32 flags[4];
+    GSM_CUDA(cudaMemcpy(flags, s->d_flag, 16, cudaMemcpyDeviceToHost));
+    const char* file = w == 0 ? "so" : "os";
+    if (flags[2]) {
+      cudaFree(stage);
+      return set_error(GSM_ERR_STORE_FORMAT, "p" + std::to_string(pid) + "." + file +
+                                                 ": node id >= 2^32 is not supported");
+    }
+    if (flags[0] != 0xFFFFFFFFu) {
+      cudaFree(stage);
+      return set_error(GSM_ERR_UNSORTED, "pair list not sorted at position " + std::to_string(flags[0]));
+    }
+    if (flags[1] != 0xFFFFFFFFu) {
+      cudaFree(stage);
+      return set_error(GSM_ERR_STORE_FORMAT,
+                       "p" + std::to_string(pid) + "." + file +
+                           ": pairs not sorted by (key, value) at position " +
+                           std::to_string(flags[1]));
+    }
+  }
+  if (stage) cudaFree(stage);
+  s->max_nnz = std::max<u32>(s->max_nnz, (u32)nnz);
+  GSM_CUDA(cudaGetLastError());
+  return GSM_OK;
+}
+
+gsm_status gsm_store_finalize(gsm_store* s) {
+  if (!s) return set_error(GSM_ERR_VALUE, "null store");
+  if (s->finalized) return GSM_OK;
+  GSM_CUDA(cudaSetDevice(s->device));
+  for (int pid = 1; pid <= s->max_pid; pid++) {
+    PredDev& p = s->preds[pid];
+    if (!p.present) continue;
+    gsm_status st;
+    if ((st = build_orient(s, p.so)) != GSM_OK) return st;
+    if ((st = build_orient(s, p.os)) != GSM_OK) return st;
+    if ((st = build_diag(s, p)) != GSM_OK) return st;
+  }
+  GSM_CUDA(cudaDeviceSynchronize());
+  s->finalized = true;
+  return GSM_OK;
+}
+
+gsm_status gsm_store_device_bytes(const gsm_store* s, int64_t* bytes) {
+  if (!s) return set_error(GSM_ERR_VALUE, "null store");
+  *bytes = s->bytes;
+  return GSM_OK;
+}
+
+gsm_status gsm_store_free(gsm_store* s) {
+  if (!s) return GSM_OK;
+  cudaSetDevice(s->device);
+  for (void* p : s->allocations) cudaFree(p);
+  if (s->d_flag) cudaFree(s->d_flag);
+  delete s;
+  return GSM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,236 @@
+"""The drop-in executor: ``execute(query, plan, store, mode="gpu", ...)``.
+
+Same signature, argument meaning, result type and error behaviour as the
+reference's ``gsmat.executor.execute``
+(/root/reference/pkg/src/gsmat/executor.py:296-368), but the whole plan runs
+as a chain of hand-written sm_100a kernels (csrc/gsm_exec.cu) over the
+HBM-resident store, through the C ABI in include/gsmat_b200.h.
+
+* ``query``/``plan`` may come from the reference (``gsmat.qparser`` /
+  ``gsmat.planner``) or from :mod:`.frontend`; only the attributes the
+  reference's execute reads are used (patterns' s/p/o/empty/source,
+  ``plan.steps[i].pattern``, ``projection``, ``distinct``).
+* ``store`` is a :class:`.storage.DeviceStore` (``storage.load``) or a
+  reference ``Store`` (uploaded once and cached).
+* ``mode``: "gpu" (default) evaluates with the parallel mode's pre-allocation
+  budget rule (executor.py:237-241); "sequential"/"parallel" also run on the
+  GPU and select that mode's budget rule (executor.py:192-193 / 237-241).
+  There is no CPU path.
+* The result is a :class:`BindingTable` whose ``rows`` are the projected id
+  tuples (bag; row order is not contractual); ``array`` holds
+  the same rows as an (n, k) uint32 numpy array without building tuples.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .storage import DeviceStore, from_store
+
+DEFAULT_ROW_BUDGET = 10**8
+_MODES = ("gpu", "sequential", "parallel")
+
+
+class BindingTable:
+    """An n-ary relation over variables, bag semantics (executor.py:40-49)."""
+
+    def __init__(self, schema, rows=None, sorted_by=None, array=None):
+        self.schema = tuple(schema)
+        self.sorted_by = sorted_by
+        self._rows = list(rows) if rows is not None else None
+        self._array = array
+
+    @property
+    def rows(self) -> list[tuple[int, ...]]:
+        if self._rows is None:
+            a = self._array
+            if a is None:
+                self._rows = []
+            elif a.shape[1] == 0:
+                self._rows = [()] * a.shape[0]
+            else:
+                self._rows = list(map(tuple, a.tolist()))
+        return self._rows
+
+    @rows.setter
+    def rows(self, value) -> None:
+        self._rows = list(value)
+        self._array = None
+
+    @property
+    def array(self) -> np.ndarray:
+        if self._array is None:
+            rows = self._rows or []
+            self._array = np.asarray(rows, dtype=np.uint64).reshape(len(rows), len(self.schema))
+        return self._array
+
+    def __len__(self) -> int:
+        if self._rows is not None:
+            return len(self._rows)
+        return 0 if self._array is None else int(self._array.shape[0])
+
+    def __eq__(self, other) -> bool:
+        if not hasattr(other, "schema") or not hasattr(other, "rows"):
+            return NotImplemented
+        return tuple(self.schema) == tuple(other.schema) and self.rows == list(other.rows)
+
+    def __repr__(self) -> str:
+        return f"BindingTable(schema={self.schema!r}, rows={len(self)} rows)"
+
+
+@dataclass
+class StepReport:
+    pattern_text: str
+    rows: int
+    prealloc_total: int
+    seconds: float
+
+
+@dataclass
+class ExecutionReport:
+    """executor.ExecutionReport (executor.py:74-91); seconds are device time.
+
+    Extra device-side fields (not in the reference): per-step ``kinds`` and
+    ``arities``, the whole-query ``device_seconds``, the bytes copied each way
+    (``h2d_bytes``, ``d2h_bytes``, result rows included) and ``kernels``.
+    """
+
+    steps: list[StepReport] = field(default_factory=list)
+    preparations: int = 0
+    uses: int = 0
+    kinds: list[str] = field(default_factory=list)
+    arities: list[int] = field(default_factory=list)
+    device_seconds: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    kernels: int = 0
+
+    @property
+    def intermediate_total(self) -> int:
+        return sum(s.rows for s in self.steps)
+
+    def lines(self) -> list[str]:
+        out = [
+            f"{i}\t{s.pattern_text}\t{s.rows}\t{s.prealloc_total}\t{s.seconds:.6f}"
+            for i, s in enumerate(self.steps, start=1)
+        ]
+        out.append(f"preparations\t{self.preparations}\tuses\t{self.uses}")
+        return out
+
+
+def _pattern_text(pattern) -> str:
+    src = getattr(pattern, "source", None)
+    return src.text() if src is not None and hasattr(src, "text") else repr(pattern)
+
+
+def compile_plan(query, plan):
+    """Plan -> (gsm_pattern array, projection var indices, var names).
+
+    Variables get small integer ids in order of first appearance in the plan.
+    """
+    steps = [st.pattern for st in plan.steps]
+    var_id: dict[str, int] = {}
+    arr = (_lib.Pattern * len(steps))()
+    for i, pat in enumerate(steps):
+        rec = arr[i]
+        for end in ("s", "o"):
+            term = getattr(pat, end)
+            if isinstance(term, str):
+                vid = var_id.setdefault(term, len(var_id))
+                setattr(rec, f"{end}_var", vid)
+                setattr(rec, f"{end}_const", 0)
+            else:
+                setattr(rec, f"{end}_var", -1)
+                tid = int(term)
+                setattr(rec, f"{end}_const", tid if 0 <= tid < 2**32 else 0)
+        rec.pid = int(pat.p) if 0 <= int(pat.p) < 2**31 else 0
+        rec.empty = 1 if getattr(pat, "empty", False) else 0
+    proj = []
+    for v in query.projection:
+        if v not in var_id:
+            raise ValueError(f"projected variable {v} is not bound by the plan")
+        proj.append(var_id[v])
+    proj_arr = (C.c_int32 * max(1, len(proj)))(*proj)
+    return steps, arr, proj_arr, len(proj)
+
+
+def execute(
+    query,
+    plan,
+    store,
+    mode: str = "gpu",
+    worker_count: int = 1,
+    row_budget: int = DEFAULT_ROW_BUDGET,
+    report: ExecutionReport | None = None,
+    *,
+    partition: tuple[int, int] = (0, 1),
+) -> BindingTable:
+    """Evaluate a plan on the GPU and project onto the query's projection.
+
+    ``worker_count`` is accepted for signature compatibility (the grid is
+    sized from the device).  ``partition=(i, k)`` evaluates only the i-th of
+    k contiguous slices of the first step's rows (multi-GPU row partitioning,
+    see :mod:`.distributed`).
+    """
+    if mode not in _MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if not plan.steps:
+        raise ValueError("cannot execute an empty plan")
+    dstore = store if isinstance(store, DeviceStore) else from_store(store)
+    steps, arr, proj_arr, nproj = compile_plan(query, plan)
+    n = len(steps)
+    budget_mode = _lib.GSM_BUDGET_SEQUENTIAL if mode == "sequential" else _lib.GSM_BUDGET_PARALLEL
+    budget = min(int(row_budget), (1 << 63) - 1)
+
+    rep_struct = None
+    rows_buf = pre_buf = ms_buf = kind_buf = ar_buf = None
+    if report is not None:
+        rows_buf = (C.c_int64 * n)()
+        pre_buf = (C.c_int64 * n)()
+        ms_buf = (C.c_float * n)()
+        kind_buf = (C.c_int32 * n)()
+        ar_buf = (C.c_int32 * n)()
+        rep_struct = _lib.Report(rows_buf, pre_buf, ms_buf, kind_buf, ar_buf)
+
+    L = _lib.lib()
+    res = C.c_void_p()
+    part, parts = partition
+    st = L.gsm_execute(
+        dstore.context(), arr, n, proj_arr, nproj, 1 if query.distinct else 0, budget,
+        budget_mode, int(part), int(parts), C.byref(rep_struct) if rep_struct is not None else None,
+        C.byref(res),
+    )
+    _lib.check(st)
+    try:
+        nrows = C.c_int64(0)
+        ncols = C.c_int32(0)
+        _lib.check(L.gsm_result_shape(res, C.byref(nrows), C.byref(ncols)))
+        out = np.empty((int(nrows.value), int(ncols.value)), dtype=np.uint32)
+        if out.size:
+            _lib.check(L.gsm_result_copy(res, out.ctypes.data))
+    finally:
+        L.gsm_result_free(res)
+
+    if report is not None:
+        # matrix_of(): one preparation per distinct pid, one use per step (executor.py:315-325)
+        seen: set[int] = set()
+        for pat in steps:
+            if pat.p not in seen:
+                seen.add(pat.p)
+                report.preparations += 1
+            report.uses += 1
+        for i, pat in enumerate(steps):
+            report.steps.append(
+                StepReport(_pattern_text(pat), int(rows_buf[i]), int(pre_buf[i]), float(ms_buf[i]) / 1e3)
+            )
+            report.kinds.append(_lib.STEP_KINDS[kind_buf[i]])
+            report.arities.append(int(ar_buf[i]))
+        report.device_seconds += rep_struct.total_device_ms / 1e3
+        report.h2d_bytes += int(rep_struct.h2d_bytes)
+        report.d2h_bytes += int(rep_struct.d2h_bytes) + out.nbytes
+        report.kernels += int(rep_struct.kernels)
+    return BindingTable(tuple(query.projection), array=out)

@@ -1,0 +1,234 @@
+"""HBM-resident store: the drop-in for ``gsmat.storage.load`` / ``Store``.
+
+``load(directory)`` reads a store directory in the reference's persist()
+format (/root/reference/pkg/src/gsmat/storage.py:203-271),
+applies the same validation with the same StoreFormatError messages
+(storage.py:222-271), and uploads every predicate's pair arrays to the GPU
+once (the paper's "mark data that requires multiple transfer", §6.3).  The
+device builds the aux-array indexes (gsm_store_finalize).
+
+``from_store(store)`` uploads a reference in-memory ``Store`` (as built by
+``gsmat.storage.build_store``) so the reference's own objects can be handed
+to :func:`paper_1807_07691_b200.executor.execute` unchanged.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import weakref
+from pathlib import Path
+from typing import Iterator, NamedTuple
+
+import numpy as np
+
+from . import _lib
+from .dictionary import StoreDictionary
+from .errors import StoreFormatError, UnknownPredicateError
+
+MAGIC = "GSMAT1"
+META_FILE = "meta"
+STATS_FILE = "stats.tsv"
+
+
+class StatEntry(NamedTuple):
+    """storage.StatEntry (storage.py:100-103)."""
+
+    cardinality: int
+    distinct_subjects: int
+    distinct_objects: int
+
+
+class PairMatrix:
+    """Host view of one predicate (read-only numpy arrays, u64 pairs).
+
+    ``so_pairs``/``os_pairs`` are (nnz, 2) uint64 arrays in the file order
+    (storage.py:74-78); the device copy lives in the gsm_store.
+    """
+
+    def __init__(self, pid: int, so: np.ndarray, os_: np.ndarray):
+        self.pid = pid
+        self.so = so
+        self.os = os_
+
+    @property
+    def cardinality(self) -> int:
+        return int(self.so.shape[0])
+
+    @property
+    def so_pairs(self) -> list[tuple[int, int]]:
+        return [tuple(r) for r in self.so.tolist()]
+
+    @property
+    def os_pairs(self) -> list[tuple[int, int]]:
+        return [tuple(r) for r in self.os.tolist()]
+
+
+class DeviceStore:
+    """A store whose predicate matrices are resident on one CUDA device."""
+
+    def __init__(self, dictionary, matrices: dict[int, PairMatrix], stats: dict[int, StatEntry],
+                 node_count: int, device: int = 0):
+        self.dictionary = dictionary
+        self.matrices = matrices
+        self.stats = stats
+        self.device = device
+        self.node_count = int(node_count)
+        self._handle = C.c_void_p()
+        self._ctx = threading.local()
+        self._contexts: list[C.c_void_p] = []
+        self._ctx_lock = threading.Lock()
+        L = _lib.lib()
+        max_pid = max(matrices) if matrices else 0
+        _lib.check(L.gsm_store_create(device, self.node_count, max_pid, C.byref(self._handle)))
+        self._finalizer = weakref.finalize(self, DeviceStore._release, self._handle.value,
+                                           self._contexts)
+        for pid in sorted(matrices):
+            m = matrices[pid]
+            so = np.ascontiguousarray(m.so, dtype=np.uint64)
+            os_ = np.ascontiguousarray(m.os, dtype=np.uint64)
+            _lib.check(L.gsm_store_put_predicate(self._handle, pid, so.ctypes.data,
+                                                 os_.ctypes.data, so.shape[0]))
+        _lib.check(L.gsm_store_finalize(self._handle))
+
+    @staticmethod
+    def _release(handle, contexts) -> None:
+        try:
+            L = _lib.lib()
+            for c in contexts:
+                L.gsm_context_free(c)
+            contexts.clear()
+            if handle:
+                L.gsm_store_free(C.c_void_p(handle))
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+    # -- reference Store surface (storage.py:106-162) -----------------------
+    @property
+    def triple_count(self) -> int:
+        return sum(m.cardinality for m in self.matrices.values())
+
+    def matrix_for(self, pid: int) -> PairMatrix:
+        try:
+            return self.matrices[pid]
+        except KeyError:
+            raise UnknownPredicateError(pid) from None
+
+    def triples(self) -> Iterator[tuple[int, int, int]]:
+        for pid in sorted(self.matrices):
+            for s, o in self.matrices[pid].so.tolist():
+                yield (s, pid, o)
+
+    # -- device side --------------------------------------------------------
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._handle
+
+    def device_bytes(self) -> int:
+        v = C.c_int64(0)
+        _lib.check(_lib.lib().gsm_store_device_bytes(self._handle, C.byref(v)))
+        return int(v.value)
+
+    def context(self, arena_bytes: int = 0) -> C.c_void_p:
+        """Per-thread execution context (stream + HBM arena)."""
+        ctx = getattr(self._ctx, "handle", None)
+        if ctx is None:
+            ctx = C.c_void_p()
+            _lib.check(_lib.lib().gsm_context_create(self._handle, int(arena_bytes), C.byref(ctx)))
+            with self._ctx_lock:
+                self._contexts.append(ctx)
+            self._ctx.handle = ctx
+        return ctx
+
+    def close(self) -> None:
+        self._finalizer()
+
+
+def _read_pairs(path: Path) -> np.ndarray:
+    """_pairs_from_bytes (storage.py:193-200) as an (n, 2) uint64 array."""
+    size = path.stat().st_size
+    if size % 16 != 0:
+        raise StoreFormatError(f"truncated pair file {path}: {size} bytes")
+    arr = np.fromfile(path, dtype="<u8")
+    return arr.reshape(-1, 2)
+
+
+def load(directory: Path | str, device: int = 0) -> DeviceStore:
+    """storage.load (storage.py:222-271) into device memory."""
+    directory = Path(directory)
+    meta_path = directory / META_FILE
+    if not meta_path.exists():
+        raise StoreFormatError(f"no store at {directory}: missing {META_FILE}")
+    lines = meta_path.read_text(encoding="ascii").splitlines()
+    if not lines or lines[0] != MAGIC:
+        found = lines[0] if lines else "<empty>"
+        raise StoreFormatError(f"bad magic in {meta_path}: expected {MAGIC}, found {found}")
+    if len(lines) < 4:
+        raise StoreFormatError(f"truncated meta file {meta_path}")
+    triple_count, pred_count, node_count = (int(x) for x in lines[1:4])
+
+    dictionary = StoreDictionary(directory)
+    if dictionary.node_count != node_count:
+        raise StoreFormatError(
+            f"meta declares {node_count} nodes but dictionary has {dictionary.node_count}"
+        )
+    stats_path = directory / STATS_FILE
+    if not stats_path.exists():
+        raise StoreFormatError(f"missing {stats_path}")
+    stats: dict[int, StatEntry] = {}
+    for raw in stats_path.read_text(encoding="ascii").splitlines():
+        pid_s, card, ds, do = raw.split("\t")
+        stats[int(pid_s)] = StatEntry(int(card), int(ds), int(do))
+    if len(stats) != pred_count:
+        raise StoreFormatError(f"meta declares {pred_count} predicates but stats has {len(stats)}")
+
+    matrices: dict[int, PairMatrix] = {}
+    total = 0
+    for pid in stats:
+        so_path = directory / f"p{pid}.so"
+        os_path = directory / f"p{pid}.os"
+        if not so_path.exists() or not os_path.exists():
+            raise StoreFormatError(f"missing pair files for predicate {pid}")
+        so = _read_pairs(so_path)
+        os_ = _read_pairs(os_path)
+        if so.shape[0] != stats[pid].cardinality:
+            raise StoreFormatError(
+                f"{so_path}: {so.shape[0]} pairs but stats declares {stats[pid].cardinality}"
+            )
+        if os_.shape[0] != so.shape[0]:
+            raise StoreFormatError(f"{os_path}: {os_.shape[0]} pairs but {so_path} has {so.shape[0]}")
+        matrices[pid] = PairMatrix(pid, so, os_)
+        total += so.shape[0]
+    if total != triple_count:
+        raise StoreFormatError(f"meta declares {triple_count} triples but store holds {total}")
+    return DeviceStore(dictionary, matrices, stats, node_count, device=device)
+
+
+# Reference Store objects are unhashable dataclasses: cache by id() and keep
+# a weak reference to detect a recycled id.
+_UPLOADED: dict[int, tuple["weakref.ref", DeviceStore]] = {}
+
+
+def from_store(store, device: int = 0) -> DeviceStore:
+    """Upload a reference ``gsmat.storage.Store`` (cached per store object)."""
+    if isinstance(store, DeviceStore):
+        return store
+    hit = _UPLOADED.get(id(store))
+    if hit is not None and hit[0]() is store and hit[1].device == device:
+        return hit[1]
+    matrices: dict[int, PairMatrix] = {}
+    for pid, m in store.matrices.items():
+        so = np.asarray(m.so_pairs, dtype=np.uint64).reshape(-1, 2)
+        os_ = np.asarray(m.os_pairs, dtype=np.uint64).reshape(-1, 2)
+        matrices[int(pid)] = PairMatrix(int(pid), so, os_)
+    stats = {int(k): StatEntry(*v) for k, v in store.stats.items()}
+    node_count = store.dictionary.node_count
+    if matrices:
+        node_count = max(node_count, int(max((int(m.so.max()) if m.so.size else 0) for m in matrices.values())))
+    dev = DeviceStore(store.dictionary, matrices, stats, node_count, device=device)
+    key = id(store)
+    try:
+        _UPLOADED[key] = (weakref.ref(store, lambda _r, k=key: _UPLOADED.pop(k, None)), dev)
+    except TypeError:  # not weak-referenceable: no caching
+        pass
+    return dev

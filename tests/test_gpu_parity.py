@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA executor (through the C ABI) vs the reference goldens
+and the C oracle.  Bit-exact: same multiset of id tuples, same counts, same
+per-step report (rows, prealloc_total), same budget errors and messages.
+"""
+
+from __future__ import annotations
+
+from collections import Counter
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, lubm_queries
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+import paper_1807_07691_b200 as g  # noqa: E402
+from paper_1807_07691_b200 import frontend  # noqa: E402
+
+
+def _plan(store, text):
+    q = frontend.bind_constants(frontend.parse_query(text), store.dictionary)
+    return q, frontend.make_plan(q, store.stats)
+
+
+def _bag(rows):
+    return Counter(tuple(int(v) for v in r) for r in rows)
+
+
+@pytest.fixture(scope="module")
+def dg():
+    return g.load(GOLDEN / "d_g")
+
+
+def test_library_is_native_and_loaded():
+    from paper_1807_07691_b200 import _lib
+
+    assert _lib.device_count() >= 1
+    assert _lib.LIB_PATH.exists()
+
+
+def test_dg_goldens(dg, golden_dg):
+    for case in golden_dg:
+        exp = case["expected"]
+        budget = case["budget"] if case["budget"] is not None else 10**8
+        q, plan = _plan(dg, case["query"])
+        rep = g.ExecutionReport()
+        if "error" in exp:
+            with pytest.raises(g.ResourceLimitError) as ei:
+                g.execute(q, plan, dg, mode=case["mode"], row_budget=budget, report=rep)
+            assert str(ei.value) == exp["message"], case["name"]
+            continue
+        res = g.execute(q, plan, dg, mode=case["mode"], row_budget=budget, report=rep)
+        assert list(res.schema) == exp["schema"], case["name"]
+        assert _bag(res.rows) == _bag(exp["rows"]), case["name"]
+        assert [s.rows for s in rep.steps] == exp["step_rows"], case["name"]
+        assert [s.prealloc_total for s in rep.steps] == exp["step_prealloc"], case["name"]
+        assert (rep.preparations, rep.uses) == (exp["preparations"], exp["uses"]), case["name"]
+
+
+def test_worked_example_exact(dg):
+    """test_acceptance.py:58-66 / test_executor.py:153-160."""
+    q, plan = _plan(dg, "SELECT ?x ?y ?z ?w WHERE { ?x <:follows> ?y . ?y <:follows> ?z . "
+                        "?x <:likes> ?w . ?z <:likes> ?w . }")
+    res = g.execute(q, plan, dg)
+    assert res.schema == ("?x", "?y", "?z", "?w")
+    assert res.rows == [(1, 4, 6, 3)]
+
+
+def test_c3_campaign(golden_c3, store_factory):
+    """The reference's 200-trial oracle-equivalence campaign, on the GPU."""
+    for t in golden_c3:
+        d = store_factory("powerlaw", triples=t["triples"], predicates=t["predicates"],
+                          zipf=t["zipf"], seed=t["seed"])
+        store = g.load(d)
+        q, plan = _plan(store, t["query"])
+        for mode in ("sequential", "parallel"):
+            rep = g.ExecutionReport()
+            res = g.execute(q, plan, store, mode=mode, report=rep)
+            assert len(res) == t["count"], t["trial"]
+            assert [str(v) for v in orc.fingerprint_array(res.array)] == t["fingerprint"], t["trial"]
+            if "rows" in t:
+                assert _bag(res.rows) == _bag(t["rows"]), t["trial"]
+            assert [s.rows for s in rep.steps] == t["step_rows"], t["trial"]
+            assert [s.prealloc_total for s in rep.steps] == t["step_prealloc"], t["trial"]
+        store.close()
+
+
+def test_lubm1_goldens(golden_lubm1, store_factory):
+    store = g.load(store_factory("lubm", univ=1, seed=0))
+    texts = dict(lubm_queries())
+    for gl in golden_lubm1:
+        q, plan = _plan(store, texts[gl["name"]])
+        rep = g.ExecutionReport()
+        res = g.execute(q, plan, store, report=rep)
+        assert len(res) == gl["count"], gl["name"]
+        assert [str(v) for v in orc.fingerprint_array(res.array)] == gl["fingerprint"], gl["name"]
+        if "rows" in gl:
+            assert _bag(res.rows) == _bag(gl["rows"]), gl["name"]
+        assert [s.rows for s in rep.steps] == gl["step_rows"], gl["name"]
+        assert [s.prealloc_total for s in rep.steps] == gl["step_prealloc"], gl["name"]
+
+
+def _oracle_compare(store, text, **kw):
+    q, plan = _plan(store, text)
+    prep = orc.PreparedStore(store.matrices)
+    rows, srows, spre = orc.run(prep, [s.pattern for s in plan.steps], q.projection, q.distinct)
+    rep = g.ExecutionReport()
+    res = g.execute(q, plan, store, report=rep, **kw)
+    exp = np.asarray(rows, dtype=np.uint64).reshape(len(rows), len(q.projection))
+    got = res.array.astype(np.uint64)
+    assert got.shape == exp.shape
+    # exact multiset equality: lexicographic sort of both
+    if got.shape[0] and got.shape[1]:
+        ko = np.lexsort(got.T[::-1])
+        ke = np.lexsort(exp.T[::-1])
+        assert np.array_equal(got[ko], exp[ke])
+    assert [s.rows for s in rep.steps] == srows
+    assert [s.prealloc_total for s in rep.steps] == spre
+    return res
+
+
+@pytest.mark.parametrize("univ", [10])
+def test_lubm_vs_oracle(univ, store_factory):
+    store = g.load(store_factory("lubm", univ=univ, seed=0))
+    for name, text in lubm_queries():
+        _oracle_compare(store, text)
+
+
+def test_partition_union_is_whole(store_factory):
+    store = g.load(store_factory("lubm", univ=2, seed=1))
+    for name, text in lubm_queries():
+        q, plan = _plan(store, text)
+        if q.distinct:
+            continue
+        whole = g.execute(q, plan, store)
+        for k in (2, 3, 8):
+            parts = [g.execute(q, plan, store, partition=(i, k)).array for i in range(k)]
+            cat = np.concatenate(parts, axis=0)
+            assert orc.fingerprint_array(cat) == orc.fingerprint_array(whole.array), (name, k)
+
+
+def test_hub_skew_and_cycles(store_factory):
+    """Power-law store (generate.py model): chains through hubs, triangles (J2)."""
+    store = g.load(store_factory("powerlaw", triples=200000, predicates=8, seed=7))
+    for text in (
+        "SELECT * WHERE { ?x <p1> ?y . ?y <p2> ?z . }",
+        "SELECT * WHERE { ?x <p1> ?y . ?y <p2> ?z . ?z <p1> ?x . }",
+        "SELECT * WHERE { ?x <p1> ?y . ?x <p2> ?z . ?x <p3> ?w . }",
+        "SELECT DISTINCT ?y WHERE { ?x <p1> ?y . ?y <p1> ?z . }",
+        "SELECT * WHERE { ?x <p1> ?x . }",
+        "SELECT * WHERE { ?x <p8> ?y . ?z <p7> ?w . }",
+        "SELECT ?z WHERE { <n1> <p1> ?y . ?y <p1> ?z . }",
+    ):
+        _oracle_compare(store, text)
+
+
+def test_budget_and_arena_growth(store_factory):
+    store = g.load(store_factory("powerlaw", triples=100000, predicates=4, seed=3))
+    text = "SELECT * WHERE { ?x <p1> ?y . ?y <p1> ?z . }"
+    q, plan = _plan(store, text)
+    full = g.execute(q, plan, store)
+    with pytest.raises(g.ResourceLimitError, match="pre-allocated join region"):
+        g.execute(q, plan, store, row_budget=len(full) - 1)
+    with pytest.raises(g.ResourceLimitError, match="join output exceeds row budget"):
+        g.execute(q, plan, store, mode="sequential", row_budget=len(full) - 1)
+    assert len(g.execute(q, plan, store, row_budget=len(full))) == len(full)
+
+
+def test_reference_objects_drop_in():
+    """Hand the reference's own Store/EncodedQuery/Plan to the GPU executor."""
+    gsmat = pytest.importorskip("gsmat")
+    from gsmat import planner, qparser, storage
+
+    st = storage.load(GOLDEN / "d_g")
+    text = "SELECT * WHERE { ?a <:follows> ?b . ?b <:related> ?c . }"
+    q = qparser.bind_constants(qparser.parse_query(text), st.dictionary)
+    plan = planner.make_plan(q, st.stats)
+    ref = gsmat.executor.execute(q, plan, st)
+    got = g.execute(q, plan, st, mode="gpu")
+    assert _bag(got.rows) == _bag(ref.rows)
+    with pytest.raises(gsmat.errors.ResourceLimitError):
+        g.execute(q, plan, st, row_budget=0)
