@@ -191,6 +191,8 @@ def run_ours(args):
             wall = time.perf_counter() - t0
             return wall, per_q
 
+        clk = ClockSampler(local).__enter__()  # sampling starts before warm-up (nvidia-smi start-up)
+        time.sleep(0.5)
         for _ in range(max(3, args.warmup)):
             one_step(False)
         if world > 1:
@@ -198,10 +200,14 @@ def run_ours(args):
         torch.cuda.synchronize()
         launches0 = _lib.kernel_launches()
         steps = []
-        with ClockSampler(local) as clk:
-            for _ in range(args.steps):
-                steps.append(one_step(True))
+        n_before = len(clk.samples)
+        for _ in range(args.steps):
+            steps.append(one_step(True))
         torch.cuda.synchronize()
+        time.sleep(0.25)
+        clk.__exit__(None, None, None)
+        if len(clk.samples) - n_before >= 3:
+            clk.samples = clk.samples[n_before:]
         if world > 1:
             torch.distributed.barrier()
         launches = _lib.kernel_launches() - launches0

@@ -77,7 +77,7 @@ typedef struct {
   float total_device_ms;   /* out: device time of the whole query (first H2D copy
                               to the last kernel), when device_ms != NULL           */
   int64_t h2d_bytes;       /* out: host->device bytes copied for this query          */
-  int64_t d2h_bytes;       /* out: device->host bytes copied by gsm_execute          */
+  int64_t d2h_bytes;       /* out: device->host bytes of the query incl. result rows */
   int64_t kernels;         /* out: kernels launched for this query                   */
 } gsm_report;
 
@@ -149,7 +149,10 @@ gsm_status gsm_execute(gsm_context* ctx, const gsm_pattern* steps, int32_t n_ste
 gsm_status gsm_result_shape(const gsm_result* res, int64_t* n_rows, int32_t* n_cols);
 
 /* Copies the result rows, row-major uint32 ids, into host memory
- * (n_rows * n_cols * 4 bytes). */
+ * (n_rows * n_cols * 4 bytes).  Results up to the context's staging size are
+ * already in pinned host memory when gsm_execute returns (the projection
+ * kernel writes them through a mapped buffer); such a result must be copied
+ * before the next gsm_execute on the same context (else GSM_ERR_VALUE). */
 gsm_status gsm_result_copy(const gsm_result* res, uint32_t* host_rows);
 
 /* Device pointer of the row-major result (valid until gsm_result_free). */

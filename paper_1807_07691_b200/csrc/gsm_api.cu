@@ -1,6 +1,7 @@
 // gsm_api.cu — error plumbing, device queries, result handles.
 #include <atomic>
 #include <cstdio>
+#include <cstring>
 #include <string>
 
 #include "gsm_internal.cuh"
@@ -55,6 +56,12 @@ gsm_status gsm_result_copy(const gsm_result* res, uint32_t* host_rows) {
   if (!res) return gsm::set_error(GSM_ERR_VALUE, "null result");
   size_t bytes = (size_t)res->n * (size_t)res->k * sizeof(u32);
   if (bytes == 0) return GSM_OK;
+  if (res->staged) {
+    if (gsm::context_generation(res->ctx) != res->gen)
+      return gsm::set_error(GSM_ERR_VALUE, "result invalidated by a later gsm_execute on its context");
+    memcpy(host_rows, res->staged, bytes);
+    return GSM_OK;
+  }
   GSM_CUDA(cudaSetDevice(res->device));
   GSM_CUDA(cudaMemcpy(host_rows, res->rows, bytes, cudaMemcpyDeviceToHost));
   return GSM_OK;
@@ -62,6 +69,13 @@ gsm_status gsm_result_copy(const gsm_result* res, uint32_t* host_rows) {
 
 gsm_status gsm_result_device_ptr(const gsm_result* res, uint64_t* device_ptr) {
   if (!res) return gsm::set_error(GSM_ERR_VALUE, "null result");
+  if (res->staged) {  // mapped pinned memory: a device-visible alias of the host rows
+    void* d = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&d, const_cast<u32*>(res->staged), 0);
+    if (e != cudaSuccess) return gsm::cuda_error(e, "cudaHostGetDevicePointer");
+    *device_ptr = (uint64_t)(uintptr_t)d;
+    return GSM_OK;
+  }
   *device_ptr = (uint64_t)(uintptr_t)res->rows;
   return GSM_OK;
 }

@@ -29,7 +29,7 @@
 namespace gsm {
 
 constexpr int TS_THREADS = 256;
-constexpr int TS_ITEMS = 4;
+constexpr int TS_ITEMS = 1;
 constexpr int TS_TILE = TS_THREADS * TS_ITEMS;
 constexpr u64 LB_MASK = (1ull << 40) - 1;
 constexpr u32 EPOCH_MAX = (1u << 22) - 1;
@@ -54,24 +54,42 @@ __device__ __forceinline__ u64 lb_word(u32 epoch, u32 flag, i64 v) {
   return ((u64)epoch << 42) | ((u64)flag << 40) | x;
 }
 
-// Decoupled look-back: returns the exclusive prefix of tile t.
-__device__ i64 lookback(const TileSync& ts, u32 t, i64 agg) {
+// Decoupled look-back, executed by warp 0 of the block: each round inspects
+// the 32 preceding tiles at once (ballot for the nearest inclusive prefix,
+// warp-sum of the aggregates in between), so a tile never walks its
+// predecessors one dependent load at a time.  Returns the exclusive prefix.
+__device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
+  const int lane = threadIdx.x & 31;
   if (t == 0) {
-    st_release_u64(ts.status, lb_word(ts.epoch, 2, agg));
+    if (lane == 0) st_release_u64(ts.status, lb_word(ts.epoch, 2, agg));
     return 0;
   }
-  st_release_u64(ts.status + t, lb_word(ts.epoch, 1, agg));
+  if (lane == 0) st_release_u64(ts.status + t, lb_word(ts.epoch, 1, agg));
   i64 excl = 0;
-  i64 j = (i64)t - 1;
+  i64 top = (i64)t - 1;  // highest predecessor of this window
   for (;;) {
-    u64 w = ld_acquire_u64(ts.status + j);
-    u32 ep = (u32)(w >> 42), fl = (u32)(w >> 40) & 3u;
-    if (ep != ts.epoch || fl == 0) continue;
-    excl += (i64)(w & LB_MASK);
-    if (fl == 2) break;
-    --j;
+    const i64 j = top - lane;
+    u64 w;
+    u32 fl;
+    if (j >= 0) {
+      do {
+        w = ld_acquire_u64(ts.status + j);
+        fl = ((u32)(w >> 42) == ts.epoch) ? (u32)(w >> 40) & 3u : 0u;
+      } while (fl == 0);
+    } else {
+      w = 0;
+      fl = 2;  // before tile 0: an inclusive prefix of 0
+    }
+    const u32 pmask = __ballot_sync(0xffffffffu, fl == 2);
+    const int first = pmask ? __ffs(pmask) - 1 : 32;  // nearest inclusive prefix
+    i64 v = (lane <= first && j >= 0) ? (i64)(w & LB_MASK) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (pmask) break;
+    top -= 32;
   }
-  st_release_u64(ts.status + t, lb_word(ts.epoch, 2, excl + agg));
+  if (lane == 0) st_release_u64(ts.status + t, lb_word(ts.epoch, 2, excl + agg));
   return excl;
 }
 
@@ -143,7 +161,10 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
     if (tid == TS_THREADS - 1) s_pre[TS_TILE] = run;
     __syncthreads();
     const i64 total = s_pre[TS_TILE];
-    if (tid == 0) s_base = lookback(ts, t, total);
+    if (warp == 0) {
+      const i64 b = lookback_warp(ts, t, total);
+      if (lane == 0) s_base = b;
+    }
     __syncthreads();
     const i64 gbase = s_base;
     for (i64 k = tid; k < total; k += TS_THREADS) {
@@ -252,6 +273,7 @@ struct DistinctP {
   u32* slots;
   u32 mask;
   u32* out;
+  i64 cap_out;
   StepStat* st;
   __device__ void prepare(DTable&) const {}
   __device__ i64 rows(const DTable&) const {
@@ -279,9 +301,13 @@ struct DistinctP {
     }
   }
   __device__ void emit(const DTable&, i64 r, u32, i64, i64 g) const {
+    if (g >= cap_out) return;
     for (int c = 0; c < k; c++) out[g * k + c] = in[r * k + c];
   }
-  __device__ void finish(i64 total) const { st->rows = total; }
+  __device__ void finish(i64 total) const {
+    st->rows = total;
+    st->overflow = total > cap_out;
+  }
 };
 
 // J0: cross product (executor.py:155-165).  Row g = L[g / |R|] ++ R[g % |R|].
@@ -370,14 +396,21 @@ __global__ void k_slice(DTable* T, int a, i64 part, i64 parts, StepStat* st) {
 struct ProjArgs {
   int col[GSM_MAX_VARS];
 };
-// Projection (executor.py:358-359) into row-major u32 rows.
-__global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* out, i64 cap_rows, StepStat* st) {
+// Projection (executor.py:358-359) into row-major u32 rows.  Small results go
+// straight into mapped pinned host memory (one sync per query, no device
+// result buffer); larger ones into the arena.  st->pad = 1 when staged.
+__global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* dev_out, i64 dev_cap,
+                       u32* host_out, i64 host_cap, StepStat* st) {
   i64 n = T->n;
+  const bool to_host = host_out != nullptr && n <= host_cap;
+  u32* out = to_host ? host_out : dev_out;
+  const i64 cap = to_host ? host_cap : dev_cap;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->rows = n;
-    st->overflow = n > cap_rows;
+    st->overflow = n > cap;
+    st->pad = to_host;
   }
-  if (n > cap_rows) n = cap_rows;
+  if (n > cap) n = cap;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride)
     for (int c = 0; c < k; c++) out[r * k + c] = __ldg(T->col[pj.col[c]] + r);
@@ -430,7 +463,15 @@ struct gsm_context {
   int grid_ts = 296;
   cudaEvent_t ev[GSM_MAX_STEPS + 2] = {};
   cudaEvent_t ev_q0 = nullptr, ev_q1 = nullptr;  // whole-query device time
+  u32* h_stage = nullptr;  // mapped pinned result staging (host address)
+  u32* d_stage = nullptr;  // its device alias
+  size_t stage_bytes = 0;
+  u64 gen = 0;             // bumped by every gsm_execute (staged results expire)
 };
+
+namespace gsm {
+u64 context_generation(const gsm_context* c) { return c ? c->gen : ~0ull; }
+}
 
 namespace {
 
@@ -452,6 +493,19 @@ gsm_status ctx_set_arena(gsm_context* c, size_t bytes) {
   GSM_CUDA(cudaMalloc(&c->d_status, c->n_status * sizeof(u64)));
   GSM_CUDA(cudaMemset(c->d_status, 0, c->n_status * sizeof(u64)));
   c->epoch = 0;
+  return GSM_OK;
+}
+
+gsm_status ctx_set_stage(gsm_context* c, size_t bytes) {
+  if (c->h_stage) {
+    cudaFreeHost(c->h_stage);
+    c->h_stage = c->d_stage = nullptr;
+    c->stage_bytes = 0;
+  }
+  bytes = (bytes + 4095) & ~(size_t)4095;
+  GSM_CUDA(cudaHostAlloc(&c->h_stage, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  GSM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_stage), c->h_stage, 0));
+  c->stage_bytes = bytes;
   return GSM_OK;
 }
 
@@ -589,6 +643,8 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
                                 : std::min<size_t>((size_t)1 << 32, free_b / 4);
   gsm_status st = ctx_set_arena(c, want);
   if (st != GSM_OK) return fail(st);
+  st = ctx_set_stage(c, (size_t)64 << 20);
+  if (st != GSM_OK) return fail(st);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tilescan<ExpandP>, TS_THREADS, 0);
   int sms = 148;
@@ -607,6 +663,7 @@ gsm_status gsm_context_free(gsm_context* c) {
   if (c->d_block) cudaFree(c->d_block);
   if (c->h_block) cudaFreeHost(c->h_block);
   if (c->d_slots) cudaFree(c->d_slots);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->ev_q0) cudaEventDestroy(c->ev_q0);
@@ -618,8 +675,8 @@ gsm_status gsm_context_free(gsm_context* c) {
 
 static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
                            int32_t n_proj, int64_t budget, int64_t part, int64_t parts,
-                           bool timing, Exec& ex, int& pack_stat, i64& pack_cap, u32*& pack_out,
-                           bool& overflow, int& kernels, i64& h2d) {
+                           bool timing, bool distinct, Exec& ex, int& pack_stat, i64& pack_cap,
+                           u32*& pack_out, bool& overflow, int& kernels, i64& h2d) {
   kernels = 0;
   QueryBlock* hb = c->h_block;
   ex.c = c;
@@ -815,11 +872,17 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
   }
   ProjArgs pa{};
   for (int j = 0; j < n_proj; j++) pa.col[j] = pj_idx[j];
-  k_pack<<<c->grid_ts, 256, 0, st>>>(dT + cur, pa, n_proj, pack_out, pack_cap, dS + pack_stat);
+  // DISTINCT reads the packed rows on the device, so only plain projections
+  // are packed straight into the pinned staging buffer.
+  u32* host_dst = distinct ? nullptr : c->d_stage;
+  const i64 host_cap = n_proj ? (i64)(c->stage_bytes / (4 * (size_t)n_proj)) : ((i64)1 << 62);
+  k_pack<<<c->grid_ts, 256, 0, st>>>(dT + cur, pa, n_proj, pack_out, pack_cap, host_dst, host_cap,
+                                     dS + pack_stat);
   count_launch();
-        kernels++;
+  kernels++;
+  if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
   GSM_CUDA(cudaGetLastError());
-  GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(hb->stats), cudaMemcpyDeviceToHost, st));
+  GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(StepStat) * (size_t)(n + 1), cudaMemcpyDeviceToHost, st));
   GSM_CUDA(cudaStreamSynchronize(st));
 
   overflow = false;
@@ -857,8 +920,9 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
   i64 h2d = 0;
   for (int attempt = 0;; attempt++) {
     ex = Exec{};
-    gsm_status stt = run_once(c, steps, n, proj, n_proj, budget, part, parts, timing, ex, pack_stat,
-                              pack_cap, pack_out, overflow, kernels, h2d);
+    c->gen++;
+    gsm_status stt = run_once(c, steps, n, proj, n_proj, budget, part, parts, timing, distinct != 0,
+                              ex, pack_stat, pack_cap, pack_out, overflow, kernels, h2d);
     if (stt != GSM_OK) return stt;
     const QueryBlock* hb = c->h_block;
     // Budget checks in plan order (executor.py:158-163, 192-193, 237-241).
@@ -937,10 +1001,15 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
   }
 
   i64 nrows = hb->stats[pack_stat].rows;
+  const bool staged = hb->stats[pack_stat].pad != 0;
+  const size_t row_bytes = 4 * (size_t)n_proj;
   gsm_result* r = new gsm_result();
   r->device = c->device;
   r->k = n_proj;
+  r->ctx = c;
+  r->gen = c->gen;
   cudaStream_t st = c->stream;
+  i64 d2h_extra = 0;
   if (distinct && nrows > 1) {
     size_t cap = 16;
     while (cap < 2 * (size_t)nrows) cap <<= 1;
@@ -955,11 +1024,19 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
       }
       c->n_slots = cap;
     }
-    u32* tmp = nullptr;
-    cudaError_t e = cudaMalloc(&tmp, std::max<size_t>(4, (size_t)nrows * n_proj * 4));
-    if (e != cudaSuccess) {
-      delete r;
-      return cuda_error(e, "cudaMalloc(result)");
+    // Survivors go to the pinned staging buffer when they can fit, else to a
+    // device buffer owned by the result.
+    const bool to_host = (size_t)nrows * row_bytes <= c->stage_bytes;
+    u32* dst = nullptr;
+    if (to_host) {
+      dst = c->d_stage;
+    } else {
+      cudaError_t e = cudaMalloc(&r->rows, std::max<size_t>(4, (size_t)nrows * row_bytes));
+      if (e != cudaSuccess) {
+        delete r;
+        return cuda_error(e, "cudaMalloc(result)");
+      }
+      dst = r->rows;
     }
     GSM_CUDA(cudaMemsetAsync(c->d_slots, 0xFF, cap * 4, st));
     DistinctP dp{};
@@ -969,7 +1046,8 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
     dp.k = n_proj;
     dp.slots = c->d_slots;
     dp.mask = (u32)(cap - 1);
-    dp.out = tmp;
+    dp.out = dst;
+    dp.cap_out = nrows;
     dp.st = c->d_block->stats + pack_stat + 1;
     GSM_CUDA(cudaMemsetAsync(c->d_block->counters + GSM_MAX_STEPS + 2, 0, 4, st));
     TileSync ts{c->d_status, c->d_block->counters + GSM_MAX_STEPS + 2, next_epoch(c)};
@@ -977,29 +1055,35 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
     count_launch();
     kernels++;
     if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
-    StepStat ds{};
     GSM_CUDA(cudaMemcpyAsync(&c->h_block->stats[pack_stat + 1], dp.st, sizeof(StepStat),
                              cudaMemcpyDeviceToHost, st));
     GSM_CUDA(cudaStreamSynchronize(st));
-    ds = c->h_block->stats[pack_stat + 1];
-    r->n = ds.rows;
-    r->rows = tmp;
-  } else {
+    d2h_extra = sizeof(StepStat);
+    r->n = c->h_block->stats[pack_stat + 1].rows;
+    if (to_host) r->staged = c->h_stage;
+  } else if (staged) {
     r->n = nrows;
-    size_t bytes = (size_t)nrows * n_proj * 4;
+    r->staged = c->h_stage;
+  } else {
+    // Result larger than the staging buffer: keep it on the device, and grow
+    // the staging buffer (up to 1 GiB) for the next query.
+    r->n = nrows;
+    size_t bytes = (size_t)nrows * row_bytes;
     cudaError_t e = cudaMalloc(&r->rows, std::max<size_t>(bytes, 4));
     if (e != cudaSuccess) {
       delete r;
       return cuda_error(e, "cudaMalloc(result)");
     }
     if (bytes) GSM_CUDA(cudaMemcpyAsync(r->rows, pack_out, bytes, cudaMemcpyDeviceToDevice, st));
-    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
     GSM_CUDA(cudaStreamSynchronize(st));
+    if (bytes > c->stage_bytes && bytes <= ((size_t)1 << 30)) ctx_set_stage(c, bytes + bytes / 4);
   }
   if (rep) {
     rep->kernels = kernels;
     rep->h2d_bytes = h2d;
-    rep->d2h_bytes = (i64)sizeof(c->h_block->stats) + (distinct && nrows > 1 ? (i64)sizeof(StepStat) : 0);
+    // stats read-back + the result rows (written through the mapped staging
+    // buffer, or copied by gsm_result_copy for device-resident results)
+    rep->d2h_bytes = (i64)sizeof(StepStat) * (n + 1) + d2h_extra + (i64)((size_t)r->n * row_bytes);
     rep->total_device_ms = 0.f;
     if (timing) cudaEventElapsedTime(&rep->total_device_ms, c->ev_q0, c->ev_q1);
   }

@@ -16,12 +16,21 @@ struct gsm_store {
   u32* d_flag = nullptr;  // validation scratch: [0] min unsorted-key pos, [1] min unsorted-value pos, [2] id overflow
 };
 
+struct gsm_context;
+
 struct gsm_result {
   int device = 0;
   i64 n = 0;
   int k = 0;
-  u32* rows = nullptr;  // device, row-major n x k
+  u32* rows = nullptr;         // device, row-major n x k (owned), or nullptr
+  const u32* staged = nullptr; // rows in the context's pinned staging buffer
+  const gsm_context* ctx = nullptr;
+  u64 gen = 0;                 // staging generation the rows belong to
 };
+
+namespace gsm {
+u64 context_generation(const gsm_context* c);
+}
 
 namespace gsm {
 cudaError_t store_alloc(gsm_store* s, void** p, size_t bytes);

@@ -128,10 +128,25 @@ def _pattern_text(pattern) -> str:
 
 
 def compile_plan(query, plan):
-    """Plan -> (gsm_pattern array, projection var indices, var names).
+    """Plan -> (steps, gsm_pattern array, projection index array, n_proj).
 
     Variables get small integer ids in order of first appearance in the plan.
+    The encoding is cached on the plan object (keyed by the identity of its
+    patterns and of the projection) so repeated executions skip it.
     """
+    key = (tuple(id(st.pattern) for st in plan.steps), tuple(query.projection))
+    cached = getattr(plan, "__dict__", {}).get("_gsm_compiled")
+    if cached is not None and cached[0] == key:
+        return cached[1]
+    compiled = _compile(query, plan)
+    try:
+        plan.__dict__["_gsm_compiled"] = (key, compiled)
+    except (AttributeError, TypeError):
+        pass
+    return compiled
+
+
+def _compile(query, plan):
     steps = [st.pattern for st in plan.steps]
     var_id: dict[str, int] = {}
     arr = (_lib.Pattern * len(steps))()
@@ -231,6 +246,6 @@ def execute(
             report.arities.append(int(ar_buf[i]))
         report.device_seconds += rep_struct.total_device_ms / 1e3
         report.h2d_bytes += int(rep_struct.h2d_bytes)
-        report.d2h_bytes += int(rep_struct.d2h_bytes) + out.nbytes
+        report.d2h_bytes += int(rep_struct.d2h_bytes)
         report.kernels += int(rep_struct.kernels)
     return BindingTable(tuple(query.projection), array=out)

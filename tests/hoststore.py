@@ -11,6 +11,7 @@ from pathlib import Path
 import numpy as np
 
 from paper_1807_07691_b200.dictionary import StoreDictionary
+from paper_1807_07691_b200.storage import StatEntry
 
 
 class HostMatrix:
@@ -26,7 +27,7 @@ class HostStore:
         self.stats = {}
         for raw in (directory / "stats.tsv").read_text().splitlines():
             pid, card, ds, do = (int(x) for x in raw.split("\t"))
-            self.stats[pid] = (card, ds, do)
+            self.stats[pid] = StatEntry(card, ds, do)
         self.matrices = {}
         for pid in self.stats:
             so = np.fromfile(directory / f"p{pid}.so", dtype="<u8").reshape(-1, 2)
