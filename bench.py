@@ -60,7 +60,41 @@ def _args():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--only-probe", action="store_true", help="run only the kernel probe (ncu)")
     return ap.parse_args()
+
+
+# Kernel-at-scale probe on the same store: self-joins whose expand step writes
+# tens of millions of rows, so the join kernel's HBM roofline is measured
+# where bandwidth (not launch latency) decides.  Not part of `value`.
+PROBES = [
+    ("memberOf_coworkers", "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
+     "SELECT ?d WHERE { ?x ub:memberOf ?d . ?y ub:memberOf ?d . }"),
+    ("takesCourse_classmates", "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
+     "SELECT ?c WHERE { ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }"),
+]
+
+
+def run_probe(g, store, peaks, reps=5):
+    out = {}
+    for name, text in PROBES:
+        q = g.bind_constants(g.parse_query(text), store.dictionary)
+        plan = g.make_plan(q, store.stats)
+        best = None
+        for _ in range(reps):
+            rep = g.ExecutionReport()
+            g.execute(q, plan, store, report=rep, row_budget=1 << 62)
+            st = rep.steps[1]
+            L, a = rep.steps[0].rows, rep.arities[0]
+            b = _step_bytes(rep.kinds[1], L, a, st.prealloc_total, st.rows, rep.arities[1])
+            if best is None or st.seconds < best[1]:
+                best = (b, st.seconds, st.rows, rep.kinds[1])
+        gbs = best[0] / best[1] / 1e9
+        out[name] = {"kernel": f"k_tilescan<{best[3]}>", "rows_out": best[2],
+                     "bytes": best[0], "us": round(1e6 * best[1], 1), "achieved_GBps": round(gbs, 1),
+                     "frac": round(gbs / peaks["hbm_gbs"], 4)}
+    return out
 
 
 def _dist():
@@ -178,6 +212,9 @@ def run_ours(args):
             queries.append((name, q, g.make_plan(q, store.stats)))
         triples = store.triple_count
         flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=f"cuda:{local}")  # 256 MB > L2
+        if args.only_probe:
+            print(json.dumps(run_probe(g, store, _peaks()[0], reps=2)))
+            return
 
         def one_step(collect):
             flush.add_(1)
@@ -275,6 +312,7 @@ def run_ours(args):
                                     "launches": v[2], "ms": round(1e3 * v[1], 3)}
                                 for k, v in cls.items()}}
 
+        probe = None if args.no_probe else run_probe(g, store, peaks)
         cpu = None
         if not args.no_cpu_baseline:
             cpu = cpu_baseline_port(store, queries, args.cpu_seconds)
@@ -305,6 +343,7 @@ def run_ours(args):
             "join_rows_per_step": rows // args.steps,
             "intermediate_rows_per_step": delta // args.steps,
             "roofline": roof,
+            "roofline_probe": probe,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

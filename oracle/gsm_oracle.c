@@ -346,10 +346,25 @@ static int64_t distinct_rows(int64_t* rows, int64_t n, int k) {
 
 /* executor.py:296-368.  budget_mode: 0 = sequential, 1 = parallel semantics.
  * step_rows/step_prealloc: per plan step (StepReport.rows / prealloc_total). */
+int orc_execute_part(const orc_pred* preds, int32_t max_pid, const orc_pattern* pats, int32_t n,
+                     const int32_t* proj, int32_t nproj, int32_t distinct, int64_t budget,
+                     int32_t budget_mode, int64_t part, int64_t parts, int64_t* step_rows,
+                     int64_t* step_prealloc, int64_t** out_rows, int64_t* out_n);
+
 int orc_execute(const orc_pred* preds, int32_t max_pid, const orc_pattern* pats, int32_t n,
                 const int32_t* proj, int32_t nproj, int32_t distinct, int64_t budget,
                 int32_t budget_mode, int64_t* step_rows, int64_t* step_prealloc,
                 int64_t** out_rows, int64_t* out_n) {
+  return orc_execute_part(preds, max_pid, pats, n, proj, nproj, distinct, budget, budget_mode, 0, 1,
+                          step_rows, step_prealloc, out_rows, out_n);
+}
+
+/* Row partitioning (the multi-GPU split of gsm_execute): only rows
+ * [n*part/parts, n*(part+1)/parts) of the first table enter the chain. */
+int orc_execute_part(const orc_pred* preds, int32_t max_pid, const orc_pattern* pats, int32_t n,
+                     const int32_t* proj, int32_t nproj, int32_t distinct, int64_t budget,
+                     int32_t budget_mode, int64_t part, int64_t parts, int64_t* step_rows,
+                     int64_t* step_prealloc, int64_t** out_rows, int64_t* out_n) {
   g_msg[0] = 0;
   *out_rows = NULL;
   *out_n = 0;
@@ -358,6 +373,13 @@ int orc_execute(const orc_pred* preds, int32_t max_pid, const orc_pattern* pats,
   Table cur;
   int rc = scan(&pats[0], MAT(&pats[0]), &cur);
   if (rc) return rc;
+  if (parts > 1) {
+    int64_t lo = (int64_t)((__int128)cur.n * part / parts);
+    int64_t hi = (int64_t)((__int128)cur.n * (part + 1) / parts);
+    if (lo > 0 && cur.arity > 0)
+      memmove(cur.rows, cur.rows + lo * cur.arity, sizeof(int64_t) * (size_t)(hi - lo) * cur.arity);
+    cur.n = hi - lo;
+  }
   if (step_rows) step_rows[0] = cur.n;
   if (step_prealloc) step_prealloc[0] = 0;
   for (int32_t s = 1; s < n; s++) {

@@ -65,6 +65,14 @@ def lib():
                 C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                 C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.c_int64),
             ]
+            L.orc_execute_part.restype = C.c_int
+            L.orc_execute_part.argtypes = [
+                C.POINTER(OrcPred), C.c_int32, C.POINTER(OrcPattern), C.c_int32,
+                C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int64, C.c_int32,
+                C.c_int64, C.c_int64,
+                C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.c_int64),
+            ]
             L.orc_last_error.restype = C.c_char_p
             L.orc_free.argtypes = [C.c_void_p]
             _lib = L
@@ -93,8 +101,12 @@ class PreparedStore:
             self.preds[pid] = OrcPred(so.shape[0], so.ctypes.data, os_.ctypes.data)
 
 
-def run(store, patterns, projection, distinct=False, budget=(1 << 62), mode="sequential"):
-    """Returns (rows: list[tuple], step_rows: list[int], step_prealloc: list[int])."""
+def run(store, patterns, projection, distinct=False, budget=(1 << 62), mode="sequential",
+        partition=(0, 1)):
+    """Returns (rows: list[tuple], step_rows: list[int], step_prealloc: list[int]).
+
+    ``partition=(i, k)`` keeps only the i-th of k contiguous slices of the
+    first step's rows (the executor's multi-GPU row partitioning)."""
     if not isinstance(store, PreparedStore):
         store = PreparedStore(store)
     n = len(patterns)
@@ -119,9 +131,10 @@ def run(store, patterns, projection, distinct=False, budget=(1 << 62), mode="seq
     out = C.POINTER(C.c_int64)()
     nout = C.c_int64(0)
     L = lib()
-    rc = L.orc_execute(store.preds, store.max_pid, arr, n, proj_arr, len(proj), 1 if distinct else 0,
-                       int(budget), 1 if mode == "parallel" else 0, srows, spre, C.byref(out),
-                       C.byref(nout))
+    rc = L.orc_execute_part(store.preds, store.max_pid, arr, n, proj_arr, len(proj),
+                            1 if distinct else 0, int(budget), 1 if mode == "parallel" else 0,
+                            int(partition[0]), int(partition[1]), srows, spre, C.byref(out),
+                            C.byref(nout))
     if rc == ORC_ERR_RESOURCE:
         raise OracleResourceError(L.orc_last_error().decode())
     if rc != ORC_OK:

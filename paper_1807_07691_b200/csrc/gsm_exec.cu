@@ -32,6 +32,7 @@ constexpr int TS_THREADS = 256;
 constexpr int TS_ITEMS = 1;
 constexpr int TS_TILE = TS_THREADS * TS_ITEMS;
 constexpr u64 LB_MASK = (1ull << 40) - 1;
+constexpr int WARP_ROW = 32;  // rows with >= this many candidates are written by a warp
 constexpr u32 EPOCH_MAX = (1u << 22) - 1;
 
 struct TileSync {
@@ -109,6 +110,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
   __shared__ i64 s_wsum[TS_THREADS / 32];
   __shared__ i64 s_base;
   __shared__ u32 s_tile;
+  __shared__ int s_long[TS_TILE];
+  __shared__ int s_nlong;
   __shared__ DTable s_in;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -122,7 +125,10 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
   }
   i64 e_acc = 0;
   for (;;) {
-    if (tid == 0) s_tile = atomicAdd(ts.counter, 1u);
+    if (tid == 0) {
+      s_tile = atomicAdd(ts.counter, 1u);
+      s_nlong = 0;
+    }
     __syncthreads();
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
@@ -167,13 +173,34 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
     }
     __syncthreads();
     const i64 gbase = s_base;
-    for (i64 k = tid; k < total; k += TS_THREADS) {
-      int lo = 0, hi = TS_TILE;  // s_pre[lo] <= k < s_pre[hi]
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_pre[mid] <= k) lo = mid; else hi = mid;
+    // Scatter (TS_ITEMS == 1: thread tid owns tile row tid).  Rows with fewer
+    // than WARP_ROW candidates are written by their own thread (consecutive
+    // rows are adjacent in the output, so a warp's stores stay dense); longer
+    // rows (hubs) are queued and written warp-cooperatively, 32 consecutive
+    // outputs per store instruction, unrolled for memory-level parallelism.
+    {
+      const i64 mine = s_pre[tid + 1] - s_pre[tid];
+      if (mine > 0 && mine < WARP_ROW) {
+        const i64 pos = gbase + s_pre[tid];
+        const u32 aux = s_aux[tid];
+        for (i64 j = 0; j < mine; j++) p.emit(s_in, base + tid, aux, j, pos + j);
+      } else if (mine >= WARP_ROW) {
+        s_long[atomicAdd(&s_nlong, 1)] = tid;
       }
-      p.emit(s_in, base + lo, s_aux[lo], k - s_pre[lo], gbase + k);
+    }
+    __syncthreads();
+    for (int q = warp; q < s_nlong; q += TS_THREADS / 32) {
+      const int r = s_long[q];
+      const i64 c = s_pre[r + 1] - s_pre[r];
+      const i64 pos = gbase + s_pre[r];
+      const u32 aux = s_aux[r];
+      for (i64 j = lane; j < c; j += 4 * 32) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const i64 jj = j + 32 * u;
+          if (jj < c) p.emit(s_in, base + r, aux, jj, pos + jj);
+        }
+      }
     }
     if ((i64)t == ntiles - 1 && tid == 0) p.finish(gbase + total);
     __syncthreads();
@@ -194,6 +221,23 @@ __device__ __forceinline__ void copy_desc(DTable& dst, const DTable* src, int nc
 // J1: one shared variable with a two-variable right pattern -> neighbour expand
 // (sm_join / parallel_sm_join without secondary variables, executor.py:168-194,
 // 218-280).  New column = the other endpoint, read from the CSR/CSC segment.
+// Fused final projection: when the join is the plan's last step and there is
+// no DISTINCT, emit() writes the projected row straight into the mapped
+// pinned staging buffer (row-major, fk columns) instead of the arena, and
+// finish() records the result count in the pack stat (pad = 1, or 3 when the
+// result outgrew the staging buffer and the host must re-run unfused).
+struct FusedOut {
+  u32* stage = nullptr;  // device alias of the pinned staging buffer; null = not fused
+  i64 cap = 0;           // rows that fit
+  int k = 0;
+  int pj[GSM_MAX_VARS];
+  StepStat* pst = nullptr;
+  __device__ void finish(i64 total) const {
+    pst->rows = total;
+    pst->pad = total <= cap ? 1 : 3;
+  }
+};
+
 struct ExpandP {
   static constexpr bool kAccumE = false;
   const DTable* L;
@@ -203,6 +247,7 @@ struct ExpandP {
   i64 cap;
   DTable* O;
   StepStat* st;
+  FusedOut fz;
   __device__ void prepare(DTable& s) const { copy_desc(s, L, a); }
   __device__ i64 rows(const DTable& s) const { return s.n; }
   __device__ u32 count(const DTable& s, i64 r, u32& aux, i64&) const {
@@ -211,16 +256,27 @@ struct ExpandP {
     return sg.y;
   }
   __device__ void emit(const DTable& s, i64 r, u32 aux, i64 j, i64 g) const {
+    const u32 nv = __ldg(R.dst + aux + j);
+    if (fz.stage) {
+      if (g >= fz.cap) return;
+      u32* o = fz.stage + g * fz.k;
+      for (int x = 0; x < fz.k; x++) {
+        const int c = fz.pj[x];
+        o[x] = c < a ? __ldg(s.col[c] + r) : nv;
+      }
+      return;
+    }
     if (g >= cap) return;
 #pragma unroll 4
     for (int c = 0; c < a; c++) out[(i64)c * cap + g] = __ldg(s.col[c] + r);
-    out[(i64)a * cap + g] = __ldg(R.dst + aux + j);
+    out[(i64)a * cap + g] = nv;
   }
   __device__ void finish(i64 total) const {
     O->n = total < cap ? total : cap;
     st->e = total;
     st->rows = total;
-    st->overflow = total > cap;
+    st->overflow = !fz.stage && total > cap;
+    if (fz.stage) fz.finish(total);
   }
 };
 
@@ -239,6 +295,7 @@ struct FilterP {
   i64 cap;
   DTable* O;
   StepStat* st;
+  FusedOut fz;
   __device__ void prepare(DTable& s) const { copy_desc(s, L, a); }
   __device__ i64 rows(const DTable& s) const { return s.n; }
   __device__ u32 count(const DTable& s, i64 r, u32& aux, i64& e) const {
@@ -251,6 +308,12 @@ struct FilterP {
     return keep;
   }
   __device__ void emit(const DTable& s, i64 r, u32, i64, i64 g) const {
+    if (fz.stage) {
+      if (g >= fz.cap) return;
+      u32* o = fz.stage + g * fz.k;
+      for (int x = 0; x < fz.k; x++) o[x] = __ldg(s.col[fz.pj[x]] + r);
+      return;
+    }
     if (g >= cap) return;
 #pragma unroll 4
     for (int c = 0; c < a; c++) out[(i64)c * cap + g] = __ldg(s.col[c] + r);
@@ -258,7 +321,8 @@ struct FilterP {
   __device__ void finish(i64 total) const {
     O->n = total < cap ? total : cap;
     st->rows = total;
-    st->overflow = total > cap;
+    st->overflow = !fz.stage && total > cap;
+    if (fz.stage) fz.finish(total);
   }
 };
 
@@ -540,6 +604,7 @@ struct Exec {
   std::vector<StepPlan> plan;
   std::vector<Home> home;  // per table
   std::vector<int> arity;  // per table
+  std::vector<i64> ub;     // per table: host-side upper bound on rows (grid sizing)
   int ntables = 0;
   ResolveArgs res{};
   size_t half;
@@ -554,6 +619,7 @@ struct Exec {
     int t = ntables++;
     home.push_back(h);
     arity.push_back(a);
+    ub.push_back((i64)1 << 62);
     DTable& d = hb->tables[t];
     d.n = 0;
     for (int i = 0; i < GSM_MAX_VARS; i++) d.col[i] = nullptr;
@@ -575,6 +641,7 @@ struct Exec {
     DTable& d = hb->tables[t];
     if (!m) {  // R6: empty flag or no matrix -> zero rows, schema kept
       d.n = 0;
+      ub[t] = 0;
       if (stat >= 0) hb->stats[stat].rows = 0;
       return t;
     }
@@ -588,26 +655,40 @@ struct Exec {
       d.n = m->ndiag;
       d.col[0] = const_cast<u32*>(m->diag);
       if (stat >= 0) hb->stats[stat].rows = d.n;
-    } else {
+    } else if (sv || ov) {
+      // R2 (?s p C): pairs_for_object(C) -> the s values of C's os run;
+      // R3 (C p ?o): pairs_for_subject(C) -> the o values of C's so run.
+      // Resolved on the host from the aux arrays: a zero-copy descriptor.
+      const HostAux& ha = sv ? c->store->aux_os[p.pid] : c->store->aux_so[p.pid];
+      const Orient& R = sv ? m->os : m->so;
+      u32 b = 0, len = 0;
+      ha.find(sv ? p.o_const : p.s_const, b, len);
+      d.n = len;
+      d.col[0] = const_cast<u32*>(R.dst) + b;
+      if (stat >= 0) hb->stats[stat].rows = d.n;
+    } else {  // R5 (C p C'): membership, resolved on the device
       ResolveJob& j = res.job[res.njobs++];
       j.table = t;
       j.stat = stat;
-      if (sv) {  // R2 (?s p C): pairs_for_object(C) -> s values (os segment)
-        j.kind = J_SEG;
-        j.R = m->os;
-        j.k1 = p.o_const;
-      } else if (ov) {  // R3 (C p ?o): pairs_for_subject(C) -> o values
-        j.kind = J_SEG;
-        j.R = m->so;
-        j.k1 = p.s_const;
-      } else {  // R5 (C p C'): contains
-        j.kind = J_CONTAINS;
-        j.R = m->so;
-        j.k1 = p.s_const;
-        j.k2 = p.o_const;
-      }
+      j.kind = J_CONTAINS;
+      j.R = m->so;
+      j.k1 = p.s_const;
+      j.k2 = p.o_const;
+      d.n = 1;  // upper bound until k_resolve writes the real value
     }
+    ub[t] = d.n;
     return t;
+  }
+  // Persistent-grid size for a kernel whose input has at most `rows` rows.
+  int grid_for_rows(i64 rows, int per_block) const {
+    i64 g = (rows + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    return (int)std::min<i64>(g, c->grid_ts);
+  }
+  static i64 sat_mul(i64 x, i64 y) {
+    if (x <= 0 || y <= 0) return 0;
+    __int128 z = (__int128)x * y;
+    return z > ((__int128)1 << 62) ? ((i64)1 << 62) : (i64)z;
   }
 };
 
@@ -675,8 +756,8 @@ gsm_status gsm_context_free(gsm_context* c) {
 
 static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
                            int32_t n_proj, int64_t budget, int64_t part, int64_t parts,
-                           bool timing, bool distinct, Exec& ex, int& pack_stat, i64& pack_cap,
-                           u32*& pack_out, bool& overflow, int& kernels, i64& h2d) {
+                           bool timing, bool distinct, bool allow_fuse, Exec& ex, int& pack_stat,
+                           i64& pack_cap, u32*& pack_out, bool& overflow, int& kernels, i64& h2d) {
   kernels = 0;
   QueryBlock* hb = c->h_block;
   ex.c = c;
@@ -706,6 +787,7 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
     ExpandP ep;
     FilterP fp;
     int a, b;
+    int grid;
   };
   std::vector<Launch> launches;
   for (int s = 1; s < n; s++) {
@@ -792,6 +874,22 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
         }
       }
     }
+    // host-side row bounds -> grid sizes (any grid is correct: blocks are persistent)
+    const i64 lub = ex.ub[cur];
+    switch (L.kind) {
+      case S_EMPTY: ex.ub[L.out] = 0; break;
+      case S_FILTER: ex.ub[L.out] = lub; break;
+      case S_GATE: ex.ub[L.out] = lub; break;
+      case S_CROSS: ex.ub[L.out] = Exec::sat_mul(lub, ex.ub[L.right]); break;
+      case S_EXPAND: {
+        const bool on_s = jv[0] == p.s_var;
+        const HostAux& ha = on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid];
+        ex.ub[L.out] = Exec::sat_mul(lub, (i64)ha.max_run);
+        break;
+      }
+      default: break;
+    }
+    L.grid = L.kind == S_CROSS ? ex.grid_for_rows(ex.ub[L.out], 256) : ex.grid_for_rows(lub, TS_TILE);
     ex.plan[s].kind = L.kind;
     ex.plan[s].schema = out_schema;
     ex.plan[s].out_table = L.out;
@@ -811,6 +909,22 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
   pack_out = reinterpret_cast<u32*>(ex.buf(ph));
   pack_cap = n_proj ? (i64)(ex.half / (4 * (size_t)n_proj)) : ((i64)1 << 62);
   pack_stat = n;
+  const i64 stage_cap = n_proj ? (i64)(c->stage_bytes / (4 * (size_t)n_proj)) : ((i64)1 << 62);
+  // Fuse the projection into the last join when it is an expand/filter and
+  // the result goes to the host staging buffer (no DISTINCT).
+  bool fused = false;
+  if (allow_fuse && !distinct && !launches.empty() &&
+      (launches.back().kind == S_EXPAND || launches.back().kind == S_FILTER)) {
+    FusedOut fz;
+    fz.stage = c->d_stage;
+    fz.cap = stage_cap;
+    fz.k = n_proj;
+    for (int j = 0; j < n_proj; j++) fz.pj[j] = pj_idx[j];
+    fz.pst = dS + pack_stat;
+    if (launches.back().kind == S_EXPAND) launches.back().ep.fz = fz;
+    else launches.back().fp.fz = fz;
+    fused = true;
+  }
 
   // ---- upload the query block (stats, counters, used descriptors) ----
   size_t used = offsetof(QueryBlock, tables) + sizeof(DTable) * (size_t)ex.ntables;
@@ -839,21 +953,21 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
         break;  // descriptor n = 0 and zero stats were uploaded
       case S_EXPAND: {
         TileSync ts{c->d_status, dC + counter++, next_epoch(c)};
-        k_tilescan<ExpandP><<<c->grid_ts, TS_THREADS, 0, st>>>(L.ep, ts);
+        k_tilescan<ExpandP><<<L.grid, TS_THREADS, 0, st>>>(L.ep, ts);
         count_launch();
         kernels++;
         break;
       }
       case S_FILTER: {
         TileSync ts{c->d_status, dC + counter++, next_epoch(c)};
-        k_tilescan<FilterP><<<c->grid_ts, TS_THREADS, 0, st>>>(L.fp, ts);
+        k_tilescan<FilterP><<<L.grid, TS_THREADS, 0, st>>>(L.fp, ts);
         count_launch();
         kernels++;
         break;
       }
       case S_CROSS: {
         Home oh = ex.home[L.out];
-        k_cross<<<c->grid_ts, 256, 0, st>>>(dT + L.left, dT + L.right, L.a, L.b,
+        k_cross<<<L.grid, 256, 0, st>>>(dT + L.left, dT + L.right, L.a, L.b,
                                              reinterpret_cast<u32*>(ex.buf(oh)),
                                              ex.cap_for(L.a + L.b), budget, dT + L.out, dS + L.step);
         count_launch();
@@ -874,12 +988,14 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
   for (int j = 0; j < n_proj; j++) pa.col[j] = pj_idx[j];
   // DISTINCT reads the packed rows on the device, so only plain projections
   // are packed straight into the pinned staging buffer.
-  u32* host_dst = distinct ? nullptr : c->d_stage;
-  const i64 host_cap = n_proj ? (i64)(c->stage_bytes / (4 * (size_t)n_proj)) : ((i64)1 << 62);
-  k_pack<<<c->grid_ts, 256, 0, st>>>(dT + cur, pa, n_proj, pack_out, pack_cap, host_dst, host_cap,
-                                     dS + pack_stat);
-  count_launch();
-  kernels++;
+  if (!fused) {
+    u32* host_dst = distinct ? nullptr : c->d_stage;
+    k_pack<<<ex.grid_for_rows(ex.ub[cur], 256), 256, 0, st>>>(dT + cur, pa, n_proj, pack_out,
+                                                              pack_cap, host_dst, stage_cap,
+                                                              dS + pack_stat);
+    count_launch();
+    kernels++;
+  }
   if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
   GSM_CUDA(cudaGetLastError());
   GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(StepStat) * (size_t)(n + 1), cudaMemcpyDeviceToHost, st));
@@ -889,6 +1005,7 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
   for (int s = 1; s < n; s++)
     if (hb->stats[s].overflow) overflow = true;
   if (hb->stats[pack_stat].overflow) overflow = true;
+  if (fused && hb->stats[pack_stat].pad == 3) overflow = true;  // staging too small
   return GSM_OK;
 }
 
@@ -918,11 +1035,12 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
   bool overflow = false;
   int kernels = 0;
   i64 h2d = 0;
+  bool allow_fuse = true;
   for (int attempt = 0;; attempt++) {
     ex = Exec{};
     c->gen++;
     gsm_status stt = run_once(c, steps, n, proj, n_proj, budget, part, parts, timing, distinct != 0,
-                              ex, pack_stat, pack_cap, pack_out, overflow, kernels, h2d);
+                              allow_fuse, ex, pack_stat, pack_cap, pack_out, overflow, kernels, h2d);
     if (stt != GSM_OK) return stt;
     const QueryBlock* hb = c->h_block;
     // Budget checks in plan order (executor.py:158-163, 192-193, 237-241).
@@ -963,6 +1081,14 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
       ovf = true;
       need_rows = hb->stats[pack_stat].rows;
       need_arity = n_proj;
+    }
+    if (!ovf && hb->stats[pack_stat].pad == 3) {
+      // The fused projection outgrew the pinned staging buffer: re-run with a
+      // device-side pack, and grow staging (<= 1 GiB) for the next query.
+      size_t want = (size_t)hb->stats[pack_stat].rows * 4 * (size_t)std::max(n_proj, 1);
+      if (want <= ((size_t)1 << 30)) ctx_set_stage(c, want + want / 4);
+      allow_fuse = false;
+      continue;
     }
     if (!ovf) break;
     // Intermediate table larger than the arena half: grow and re-run.

@@ -4,11 +4,22 @@
 
 #include "gsm_common.cuh"
 
+// Host copy of one orientation's aux array (storage.py:38-53): distinct keys
+// and their run offsets.  Lets the host resolve constant-endpoint scans
+// (R2/R3) without a device round trip.
+struct HostAux {
+  std::vector<u32> key;  // ascending distinct keys
+  std::vector<u32> off;  // off[i]..off[i+1] = run of key[i]; size key.size()+1
+  u32 max_run = 0;       // longest run (max degree in this orientation)
+  bool find(u32 k, u32& begin, u32& len) const;
+};
+
 struct gsm_store {
   int device = 0;
   i64 node_count = 0;
   int max_pid = 0;
   std::vector<gsm::PredDev> preds;  // indexed by pid (0 unused)
+  std::vector<HostAux> aux_so, aux_os;  // indexed by pid
   std::vector<void*> allocations;
   i64 bytes = 0;
   u32 max_nnz = 0;

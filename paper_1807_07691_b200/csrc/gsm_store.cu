@@ -13,6 +13,34 @@
 
 #include "gsm_internal.cuh"
 
+bool HostAux::find(u32 k, u32& begin, u32& len) const {
+  auto it = std::lower_bound(key.begin(), key.end(), k);
+  if (it == key.end() || *it != k) {
+    begin = 0;
+    len = 0;
+    return false;
+  }
+  size_t i = (size_t)(it - key.begin());
+  begin = off[i];
+  len = off[i + 1] - off[i];
+  return true;
+}
+
+static void build_host_aux(const uint64_t* pairs, i64 nnz, HostAux& a) {
+  a.key.clear();
+  a.off.clear();
+  for (i64 i = 0; i < nnz; i++) {
+    u32 k = (u32)pairs[2 * i];
+    if (i == 0 || k != (u32)pairs[2 * i - 2]) {
+      a.key.push_back(k);
+      a.off.push_back((u32)i);
+    }
+  }
+  a.off.push_back((u32)nnz);
+  a.max_run = 0;
+  for (size_t i = 0; i + 1 < a.off.size(); i++) a.max_run = std::max(a.max_run, a.off[i + 1] - a.off[i]);
+}
+
 namespace gsm {
 
 cudaError_t store_alloc(gsm_store* s, void** p, size_t bytes) {
@@ -202,6 +230,8 @@ gsm_status gsm_store_create(int32_t device, int64_t node_count, int32_t max_pid,
   s->node_count = node_count;
   s->max_pid = max_pid;
   s->preds.resize((size_t)max_pid + 1);
+  s->aux_so.resize((size_t)max_pid + 1);
+  s->aux_os.resize((size_t)max_pid + 1);
   cudaError_t e = cudaMalloc(&s->d_flag, 16);
   if (e != cudaSuccess) {
     delete s;
@@ -269,6 +299,8 @@ gsm_status gsm_store_put_predicate(gsm_store* s, int32_t pid, const uint64_t* so
     }
   }
   if (stage) cudaFree(stage);
+  build_host_aux(so_pairs, nnz, s->aux_so[pid]);
+  build_host_aux(os_pairs, nnz, s->aux_os[pid]);
   s->max_nnz = std::max<u32>(s->max_nnz, (u32)nnz);
   GSM_CUDA(cudaGetLastError());
   return GSM_OK;
