@@ -150,9 +150,9 @@ gsm_status gsm_result_shape(const gsm_result* res, int64_t* n_rows, int32_t* n_c
 
 /* Copies the result rows, row-major uint32 ids, into host memory
  * (n_rows * n_cols * 4 bytes).  Results up to the context's staging size are
- * already in pinned host memory when gsm_execute returns (the projection
- * kernel writes them through a mapped buffer); such a result must be copied
- * before the next gsm_execute on the same context (else GSM_ERR_VALUE). */
+ * already in pinned host memory when gsm_execute returns (copied inside the
+ * query's launch sequence); such a result must be copied before the next
+ * gsm_execute on the same context (else GSM_ERR_VALUE). */
 gsm_status gsm_result_copy(const gsm_result* res, uint32_t* host_rows);
 
 /* Device pointer of the row-major result (valid until gsm_result_free). */

@@ -69,11 +69,10 @@ gsm_status gsm_result_copy(const gsm_result* res, uint32_t* host_rows) {
 
 gsm_status gsm_result_device_ptr(const gsm_result* res, uint64_t* device_ptr) {
   if (!res) return gsm::set_error(GSM_ERR_VALUE, "null result");
-  if (res->staged) {  // mapped pinned memory: a device-visible alias of the host rows
-    void* d = nullptr;
-    cudaError_t e = cudaHostGetDevicePointer(&d, const_cast<u32*>(res->staged), 0);
-    if (e != cudaSuccess) return gsm::cuda_error(e, "cudaHostGetDevicePointer");
-    *device_ptr = (uint64_t)(uintptr_t)d;
+  if (res->staged) {  // the device copy of staged rows lives in the context's result buffer
+    if (gsm::context_generation(res->ctx) != res->gen)
+      return gsm::set_error(GSM_ERR_VALUE, "result invalidated by a later gsm_execute on its context");
+    *device_ptr = (uint64_t)(uintptr_t)gsm::context_device_rows(res->ctx);
     return GSM_OK;
   }
   *device_ptr = (uint64_t)(uintptr_t)res->rows;

@@ -20,8 +20,10 @@
 // power-law tail are spread over all 256 threads of the tile.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "gsm_internal.cuh"
@@ -36,9 +38,11 @@ constexpr int WARP_ROW = 32;  // rows with >= this many candidates are written b
 constexpr u32 EPOCH_MAX = (1u << 22) - 1;
 
 struct TileSync {
-  u64* status;   // one word per tile: epoch:22 | flag:2 | value:40
-  u32* counter;  // dynamic tile counter (zeroed per query)
-  u32 epoch;
+  u64* status;            // one word per tile: epoch:22 | flag:2 | value:40
+  u32* counter;           // dynamic tile counter (zeroed per query)
+  const u32* epoch_ptr;   // this launch's epoch, in the query block (so a captured
+                          // CUDA graph replays with fresh epochs and no param change)
+  u32 epoch;              // loaded from epoch_ptr at kernel start
 };
 
 __device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
@@ -105,6 +109,7 @@ __device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
 // ---------------------------------------------------------------------------
 template <class P>
 __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
+  ts.epoch = *ts.epoch_ptr;
   __shared__ i64 s_pre[TS_TILE + 1];
   __shared__ u32 s_aux[TS_TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
@@ -222,10 +227,10 @@ __device__ __forceinline__ void copy_desc(DTable& dst, const DTable* src, int nc
 // (sm_join / parallel_sm_join without secondary variables, executor.py:168-194,
 // 218-280).  New column = the other endpoint, read from the CSR/CSC segment.
 // Fused final projection: when the join is the plan's last step and there is
-// no DISTINCT, emit() writes the projected row straight into the mapped
-// pinned staging buffer (row-major, fk columns) instead of the arena, and
+// no DISTINCT, emit() writes the projected row straight into the context's
+// result buffer (row-major, fz.k columns) instead of the arena, and
 // finish() records the result count in the pack stat (pad = 1, or 3 when the
-// result outgrew the staging buffer and the host must re-run unfused).
+// result outgrew the result buffer and the host must re-run unfused).
 struct FusedOut {
   u32* stage = nullptr;  // device alias of the pinned staging buffer; null = not fused
   i64 cap = 0;           // rows that fit
@@ -460,9 +465,10 @@ __global__ void k_slice(DTable* T, int a, i64 part, i64 parts, StepStat* st) {
 struct ProjArgs {
   int col[GSM_MAX_VARS];
 };
-// Projection (executor.py:358-359) into row-major u32 rows.  Small results go
-// straight into mapped pinned host memory (one sync per query, no device
-// result buffer); larger ones into the arena.  st->pad = 1 when staged.
+// Projection (executor.py:358-359) into row-major u32 rows.  Results that fit
+// go to the context's result buffer, whose head the launch sequence copies to
+// pinned host memory before its single sync; larger ones go to the arena and
+// become a device-resident result.  st->pad = 1 when staged.
 __global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* dev_out, i64 dev_cap,
                        u32* host_out, i64 host_cap, StepStat* st) {
   i64 n = T->n;
@@ -496,6 +502,7 @@ constexpr int MAX_TABLES = 2 * GSM_MAX_STEPS + 2;
 struct QueryBlock {
   StepStat stats[GSM_MAX_STEPS + 2];
   u32 counters[GSM_MAX_STEPS + 4];
+  u32 epochs[GSM_MAX_STEPS + 4];
   DTable tables[MAX_TABLES];
 };
 
@@ -527,19 +534,36 @@ struct gsm_context {
   int grid_ts = 296;
   cudaEvent_t ev[GSM_MAX_STEPS + 2] = {};
   cudaEvent_t ev_q0 = nullptr, ev_q1 = nullptr;  // whole-query device time
-  u32* h_stage = nullptr;  // mapped pinned result staging (host address)
-  u32* d_stage = nullptr;  // its device alias
+  u32* h_stage = nullptr;  // pinned host result staging
+  u32* d_stage = nullptr;  // device result buffer (projected rows, row-major)
   size_t stage_bytes = 0;
+  size_t guess = 0;        // bytes of the result D2H copied inside the launch sequence
+  std::unordered_map<std::string, size_t> last_bytes;  // per plan: last result size
   u64 gen = 0;             // bumped by every gsm_execute (staged results expire)
+  bool use_graphs = true;  // replay each distinct query's launch sequence as a CUDA graph
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    int kernels;
+  };
+  std::unordered_map<std::string, GraphEntry> graphs;
 };
 
 namespace gsm {
 u64 context_generation(const gsm_context* c) { return c ? c->gen : ~0ull; }
+const u32* context_device_rows(const gsm_context* c) { return c ? c->d_stage : nullptr; }
 }
 
 namespace {
 
+// Captured graphs embed arena / staging / status pointers: drop them whenever
+// one of those buffers is reallocated.
+void ctx_clear_graphs(gsm_context* c) {
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+  c->graphs.clear();
+}
+
 gsm_status ctx_set_arena(gsm_context* c, size_t bytes) {
+  ctx_clear_graphs(c);
   if (c->arena) {
     cudaFree(c->arena);
     c->arena = nullptr;
@@ -561,14 +585,16 @@ gsm_status ctx_set_arena(gsm_context* c, size_t bytes) {
 }
 
 gsm_status ctx_set_stage(gsm_context* c, size_t bytes) {
+  ctx_clear_graphs(c);
   if (c->h_stage) {
     cudaFreeHost(c->h_stage);
+    cudaFree(c->d_stage);
     c->h_stage = c->d_stage = nullptr;
     c->stage_bytes = 0;
   }
   bytes = (bytes + 4095) & ~(size_t)4095;
-  GSM_CUDA(cudaHostAlloc(&c->h_stage, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
-  GSM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_stage), c->h_stage, 0));
+  GSM_CUDA(cudaMallocHost(&c->h_stage, bytes));
+  GSM_CUDA(cudaMalloc(&c->d_stage, bytes));
   c->stage_bytes = bytes;
   return GSM_OK;
 }
@@ -703,6 +729,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   gsm_context* c = new gsm_context();
   c->store = store;
   c->device = store->device;
+  if (const char* ng = getenv("GSM_NO_GRAPHS")) c->use_graphs = !(ng[0] == '1');
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
     return st;
@@ -739,12 +766,14 @@ gsm_status gsm_context_free(gsm_context* c) {
   if (!c) return GSM_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  ctx_clear_graphs(c);
   if (c->arena) cudaFree(c->arena);
   if (c->d_status) cudaFree(c->d_status);
   if (c->d_block) cudaFree(c->d_block);
   if (c->h_block) cudaFreeHost(c->h_block);
   if (c->d_slots) cudaFree(c->d_slots);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->d_stage) cudaFree(c->d_stage);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->ev_q0) cudaEventDestroy(c->ev_q0);
@@ -757,7 +786,8 @@ gsm_status gsm_context_free(gsm_context* c) {
 static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
                            int32_t n_proj, int64_t budget, int64_t part, int64_t parts,
                            bool timing, bool distinct, bool allow_fuse, Exec& ex, int& pack_stat,
-                           i64& pack_cap, u32*& pack_out, bool& overflow, int& kernels, i64& h2d) {
+                           i64& pack_cap, u32*& pack_out, bool& overflow, int& kernels, i64& h2d,
+                           std::string& last_key) {
   kernels = 0;
   QueryBlock* hb = c->h_block;
   ex.c = c;
@@ -926,79 +956,144 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
     fused = true;
   }
 
-  // ---- upload the query block (stats, counters, used descriptors) ----
-  size_t used = offsetof(QueryBlock, tables) + sizeof(DTable) * (size_t)ex.ntables;
-  cudaStream_t st = c->stream;
-  if (timing) GSM_CUDA(cudaEventRecord(c->ev_q0, st));
-  GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
-  h2d = (i64)used;
-
-  if (timing) GSM_CUDA(cudaEventRecord(c->ev[0], st));
-  if (ex.res.njobs > 0) {
-    k_resolve<<<1, 64, 0, st>>>(ex.res, dT, dS);
-    count_launch();
-        kernels++;
-  }
-  if (parts > 1) {
-    k_slice<<<1, 64, 0, st>>>(dT + ex.plan[0].out_table, (int)ex.plan[0].schema.size(), part, parts,
-                              dS + 0);
-    count_launch();
-        kernels++;
-  }
-  if (timing) GSM_CUDA(cudaEventRecord(c->ev[1], st));
-  int counter = 0;
-  for (auto& L : launches) {
-    switch (L.kind) {
-      case S_EMPTY:
-        break;  // descriptor n = 0 and zero stats were uploaded
-      case S_EXPAND: {
-        TileSync ts{c->d_status, dC + counter++, next_epoch(c)};
-        k_tilescan<ExpandP><<<L.grid, TS_THREADS, 0, st>>>(L.ep, ts);
-        count_launch();
-        kernels++;
-        break;
-      }
-      case S_FILTER: {
-        TileSync ts{c->d_status, dC + counter++, next_epoch(c)};
-        k_tilescan<FilterP><<<L.grid, TS_THREADS, 0, st>>>(L.fp, ts);
-        count_launch();
-        kernels++;
-        break;
-      }
-      case S_CROSS: {
-        Home oh = ex.home[L.out];
-        k_cross<<<L.grid, 256, 0, st>>>(dT + L.left, dT + L.right, L.a, L.b,
-                                             reinterpret_cast<u32*>(ex.buf(oh)),
-                                             ex.cap_for(L.a + L.b), budget, dT + L.out, dS + L.step);
-        count_launch();
-        kernels++;
-        break;
-      }
-      case S_GATE:
-        k_gate<<<1, 64, 0, st>>>(dT + L.left, dT + L.right, ex.arity[L.left], dT + L.out, dS + L.step);
-        count_launch();
-        kernels++;
-        break;
-      default:
-        break;
-    }
-    if (timing) GSM_CUDA(cudaEventRecord(c->ev[L.step + 1], st));
+  // ---- per-launch epochs: data in the query block, so a captured graph
+  //      replays with fresh epochs and unchanged kernel parameters ----
+  {
+    int slot = 0;
+    for (auto& L : launches)
+      if (L.kind == S_EXPAND || L.kind == S_FILTER) hb->epochs[slot++] = next_epoch(c);
   }
   ProjArgs pa{};
   for (int j = 0; j < n_proj; j++) pa.col[j] = pj_idx[j];
-  // DISTINCT reads the packed rows on the device, so only plain projections
-  // are packed straight into the pinned staging buffer.
-  if (!fused) {
-    u32* host_dst = distinct ? nullptr : c->d_stage;
-    k_pack<<<ex.grid_for_rows(ex.ub[cur], 256), 256, 0, st>>>(dT + cur, pa, n_proj, pack_out,
-                                                              pack_cap, host_dst, stage_cap,
-                                                              dS + pack_stat);
-    count_launch();
-    kernels++;
+  const size_t used = offsetof(QueryBlock, tables) + sizeof(DTable) * (size_t)ex.ntables;
+  h2d = (i64)used;
+  cudaStream_t st = c->stream;
+
+  // The whole query as one stream-ordered sequence: H2D of the query block,
+  // the kernels, D2H of the step counters.  Nothing here writes host memory.
+  auto issue = [&]() -> gsm_status {
+    int nk = 0;
+    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q0, st));
+    GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
+    if (timing) GSM_CUDA(cudaEventRecord(c->ev[0], st));
+    if (ex.res.njobs > 0) {
+      k_resolve<<<1, 64, 0, st>>>(ex.res, dT, dS);
+      nk++;
+    }
+    if (parts > 1) {
+      k_slice<<<1, 64, 0, st>>>(dT + ex.plan[0].out_table, (int)ex.plan[0].schema.size(), part,
+                                parts, dS + 0);
+      nk++;
+    }
+    if (timing) GSM_CUDA(cudaEventRecord(c->ev[1], st));
+    int slot = 0;
+    for (auto& L : launches) {
+      switch (L.kind) {
+        case S_EMPTY:
+          break;  // descriptor n = 0 and zero stats were uploaded
+        case S_EXPAND: {
+          TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
+          slot++;
+          k_tilescan<ExpandP><<<L.grid, TS_THREADS, 0, st>>>(L.ep, ts);
+          nk++;
+          break;
+        }
+        case S_FILTER: {
+          TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
+          slot++;
+          k_tilescan<FilterP><<<L.grid, TS_THREADS, 0, st>>>(L.fp, ts);
+          nk++;
+          break;
+        }
+        case S_CROSS: {
+          Home oh = ex.home[L.out];
+          k_cross<<<L.grid, 256, 0, st>>>(dT + L.left, dT + L.right, L.a, L.b,
+                                          reinterpret_cast<u32*>(ex.buf(oh)),
+                                          ex.cap_for(L.a + L.b), budget, dT + L.out, dS + L.step);
+          nk++;
+          break;
+        }
+        case S_GATE:
+          k_gate<<<1, 64, 0, st>>>(dT + L.left, dT + L.right, ex.arity[L.left], dT + L.out,
+                                   dS + L.step);
+          nk++;
+          break;
+        default:
+          break;
+      }
+      if (timing) GSM_CUDA(cudaEventRecord(c->ev[L.step + 1], st));
+    }
+    if (!fused) {
+      // DISTINCT reads the packed rows on the device, so only plain
+      // projections are packed straight into the pinned staging buffer.
+      u32* host_dst = distinct ? nullptr : c->d_stage;
+      k_pack<<<ex.grid_for_rows(ex.ub[cur], 256), 256, 0, st>>>(dT + cur, pa, n_proj, pack_out,
+                                                                pack_cap, host_dst, stage_cap,
+                                                                dS + pack_stat);
+      nk++;
+    }
+    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
+    GSM_CUDA(cudaGetLastError());
+    GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(StepStat) * (size_t)(n + 1),
+                             cudaMemcpyDeviceToHost, st));
+    // The result rows, up to this plan's expected size; the host fetches any
+    // remainder after the sync (rare: only when the result grew).
+    if (!distinct && c->guess)
+      GSM_CUDA(cudaMemcpyAsync(c->h_stage, c->d_stage, c->guess, cudaMemcpyDeviceToHost, st));
+    kernels = nk;
+    return GSM_OK;
+  };
+
+  // Plan key: everything the launch sequence's parameters derive from.
+  std::string key;
+  {
+    auto put = [&key](const void* p, size_t b) { key.append(reinterpret_cast<const char*>(p), b); };
+    put(steps, sizeof(gsm_pattern) * (size_t)n);
+    put(proj, sizeof(int32_t) * (size_t)n_proj);
+    const i64 scal[] = {n, n_proj, distinct, allow_fuse, timing, budget, part, parts};
+    put(scal, sizeof scal);
   }
-  if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
-  GSM_CUDA(cudaGetLastError());
-  GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(StepStat) * (size_t)(n + 1), cudaMemcpyDeviceToHost, st));
+  {
+    // D2H size guess: the last result size of this plan rounded up to a power
+    // of two (>= 4 KiB), else 64 KiB; never more than the staging buffer.
+    auto lb = c->last_bytes.find(key);
+    size_t g = 65536;
+    if (lb != c->last_bytes.end()) {
+      g = 4096;
+      while (g < lb->second) g <<= 1;
+    }
+    c->guess = std::min(g, c->stage_bytes);
+  }
+  last_key = key;
+  if (c->use_graphs) {
+    key.append(reinterpret_cast<const char*>(&c->guess), sizeof c->guess);
+    cudaGraphExec_t ge = nullptr;
+    auto it = c->graphs.find(key);
+    if (it != c->graphs.end()) {
+      ge = it->second.exec;
+      kernels = it->second.kernels;
+    } else {
+      if (c->graphs.size() >= 1024) ctx_clear_graphs(c);
+      GSM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      gsm_status is = issue();
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(st, &g);
+      if (is != GSM_OK) {
+        if (g) cudaGraphDestroy(g);
+        return is;
+      }
+      if (ce != cudaSuccess) return cuda_error(ce, "cudaStreamEndCapture");
+      ce = cudaGraphInstantiate(&ge, g, 0);
+      cudaGraphDestroy(g);
+      if (ce != cudaSuccess) return cuda_error(ce, "cudaGraphInstantiate");
+      c->graphs.emplace(key, gsm_context::GraphEntry{ge, kernels});
+    }
+    GSM_CUDA(cudaGraphLaunch(ge, st));
+  } else {
+    gsm_status is = issue();
+    if (is != GSM_OK) return is;
+  }
+  count_launch(kernels);
   GSM_CUDA(cudaStreamSynchronize(st));
 
   overflow = false;
@@ -1036,11 +1131,13 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
   int kernels = 0;
   i64 h2d = 0;
   bool allow_fuse = true;
+  std::string plan_key;
   for (int attempt = 0;; attempt++) {
     ex = Exec{};
     c->gen++;
     gsm_status stt = run_once(c, steps, n, proj, n_proj, budget, part, parts, timing, distinct != 0,
-                              allow_fuse, ex, pack_stat, pack_cap, pack_out, overflow, kernels, h2d);
+                              allow_fuse, ex, pack_stat, pack_cap, pack_out, overflow, kernels, h2d,
+                              plan_key);
     if (stt != GSM_OK) return stt;
     const QueryBlock* hb = c->h_block;
     // Budget checks in plan order (executor.py:158-163, 192-193, 237-241).
@@ -1176,7 +1273,11 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
     dp.cap_out = nrows;
     dp.st = c->d_block->stats + pack_stat + 1;
     GSM_CUDA(cudaMemsetAsync(c->d_block->counters + GSM_MAX_STEPS + 2, 0, 4, st));
-    TileSync ts{c->d_status, c->d_block->counters + GSM_MAX_STEPS + 2, next_epoch(c)};
+    c->h_block->epochs[GSM_MAX_STEPS + 2] = next_epoch(c);
+    GSM_CUDA(cudaMemcpyAsync(c->d_block->epochs + GSM_MAX_STEPS + 2,
+                             c->h_block->epochs + GSM_MAX_STEPS + 2, 4, cudaMemcpyHostToDevice, st));
+    TileSync ts{c->d_status, c->d_block->counters + GSM_MAX_STEPS + 2,
+                c->d_block->epochs + GSM_MAX_STEPS + 2, 0};
     k_tilescan<DistinctP><<<c->grid_ts, TS_THREADS, 0, st>>>(dp, ts);
     count_launch();
     kernels++;
@@ -1186,10 +1287,21 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
     GSM_CUDA(cudaStreamSynchronize(st));
     d2h_extra = sizeof(StepStat);
     r->n = c->h_block->stats[pack_stat + 1].rows;
-    if (to_host) r->staged = c->h_stage;
+    if (to_host) {
+      if (r->n * (i64)row_bytes > 0)
+        GSM_CUDA(cudaMemcpy(c->h_stage, c->d_stage, (size_t)r->n * row_bytes, cudaMemcpyDeviceToHost));
+      r->staged = c->h_stage;
+    }
   } else if (staged) {
     r->n = nrows;
     r->staged = c->h_stage;
+    const size_t bytes = (size_t)nrows * row_bytes;
+    if (bytes > c->guess)
+      GSM_CUDA(cudaMemcpy(reinterpret_cast<char*>(c->h_stage) + c->guess,
+                          reinterpret_cast<char*>(c->d_stage) + c->guess, bytes - c->guess,
+                          cudaMemcpyDeviceToHost));
+    c->last_bytes[plan_key] = bytes;
+    if (c->last_bytes.size() > 4096) c->last_bytes.clear();
   } else {
     // Result larger than the staging buffer: keep it on the device, and grow
     // the staging buffer (up to 1 GiB) for the next query.
@@ -1207,8 +1319,8 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
   if (rep) {
     rep->kernels = kernels;
     rep->h2d_bytes = h2d;
-    // stats read-back + the result rows (written through the mapped staging
-    // buffer, or copied by gsm_result_copy for device-resident results)
+    // stats read-back + the result rows (copied into the pinned staging
+    // buffer, or by gsm_result_copy for device-resident results)
     rep->d2h_bytes = (i64)sizeof(StepStat) * (n + 1) + d2h_extra + (i64)((size_t)r->n * row_bytes);
     rep->total_device_ms = 0.f;
     if (timing) cudaEventElapsedTime(&rep->total_device_ms, c->ev_q0, c->ev_q1);

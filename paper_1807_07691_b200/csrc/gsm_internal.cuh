@@ -41,6 +41,7 @@ struct gsm_result {
 
 namespace gsm {
 u64 context_generation(const gsm_context* c);
+const u32* context_device_rows(const gsm_context* c);
 }
 
 namespace gsm {

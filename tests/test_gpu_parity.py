@@ -182,3 +182,37 @@ def test_reference_objects_drop_in():
     assert _bag(got.rows) == _bag(ref.rows)
     with pytest.raises(gsmat.errors.ResourceLimitError):
         g.execute(q, plan, st, row_budget=0)
+
+
+def test_graph_replay_matches_fresh_launches(store_factory, tmp_path):
+    """Each query is captured once as a CUDA graph and replayed afterwards;
+    replays and the graph-free launch path (GSM_NO_GRAPHS=1) agree."""
+    import json
+    import subprocess
+    import sys
+
+    d = store_factory("lubm", univ=2, seed=4)
+    store = g.load(d)
+    fps = {}
+    for name, text in lubm_queries():
+        q, plan = _plan(store, text)
+        runs = [orc.fingerprint_array(g.execute(q, plan, store).array) for _ in range(3)]
+        assert runs[0] == runs[1] == runs[2], name
+        fps[name] = [str(v) for v in runs[0]]
+    script = (
+        "import json, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_1807_07691_b200 as g\n"
+        "from oracle import oracle as orc\n"
+        "from conftest import lubm_queries\n"
+        "st = g.load(%r)\n"
+        "out = {}\n"
+        "for name, text in lubm_queries():\n"
+        "    q = g.bind_constants(g.parse_query(text), st.dictionary)\n"
+        "    p = g.make_plan(q, st.stats)\n"
+        "    out[name] = [str(v) for v in orc.fingerprint_array(g.execute(q, p, st).array)]\n"
+        "print(json.dumps(out))\n" % (str(GOLDEN.parents[1]), str(GOLDEN.parent), str(d))
+    )
+    env = dict(__import__("os").environ, GSM_NO_GRAPHS="1")
+    out = subprocess.run([sys.executable, "-c", script], env=env, check=True, capture_output=True,
+                         text=True).stdout
+    assert json.loads(out.strip().splitlines()[-1]) == fps
