@@ -534,6 +534,7 @@ struct gsm_context {
   int grid_ts = 296;
   cudaEvent_t ev[GSM_MAX_STEPS + 2] = {};
   cudaEvent_t ev_q0 = nullptr, ev_q1 = nullptr;  // whole-query device time
+  cudaEvent_t ev_q2 = nullptr;  // end of the (un-captured) DISTINCT tail
   u32* h_stage = nullptr;  // pinned host result staging
   u32* d_stage = nullptr;  // device result buffer (projected rows, row-major)
   size_t stage_bytes = 0;
@@ -743,7 +744,8 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
     return fail(cuda_error(e, "cudaMallocHost(query block)"));
   for (auto& ev : c->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(cuda_error(e, "cudaEventCreate"));
-  if ((e = cudaEventCreate(&c->ev_q0)) != cudaSuccess || (e = cudaEventCreate(&c->ev_q1)) != cudaSuccess)
+  if ((e = cudaEventCreate(&c->ev_q0)) != cudaSuccess || (e = cudaEventCreate(&c->ev_q1)) != cudaSuccess ||
+      (e = cudaEventCreate(&c->ev_q2)) != cudaSuccess)
     return fail(cuda_error(e, "cudaEventCreate"));
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -778,6 +780,7 @@ gsm_status gsm_context_free(gsm_context* c) {
     if (ev) cudaEventDestroy(ev);
   if (c->ev_q0) cudaEventDestroy(c->ev_q0);
   if (c->ev_q1) cudaEventDestroy(c->ev_q1);
+  if (c->ev_q2) cudaEventDestroy(c->ev_q2);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GSM_OK;
@@ -973,9 +976,9 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
   // the kernels, D2H of the step counters.  Nothing here writes host memory.
   auto issue = [&]() -> gsm_status {
     int nk = 0;
-    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q0, st));
+    if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev_q0, st, cudaEventRecordExternal));
     GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
-    if (timing) GSM_CUDA(cudaEventRecord(c->ev[0], st));
+    if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev[0], st, cudaEventRecordExternal));
     if (ex.res.njobs > 0) {
       k_resolve<<<1, 64, 0, st>>>(ex.res, dT, dS);
       nk++;
@@ -985,7 +988,7 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
                                 parts, dS + 0);
       nk++;
     }
-    if (timing) GSM_CUDA(cudaEventRecord(c->ev[1], st));
+    if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev[1], st, cudaEventRecordExternal));
     int slot = 0;
     for (auto& L : launches) {
       switch (L.kind) {
@@ -1021,7 +1024,7 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
         default:
           break;
       }
-      if (timing) GSM_CUDA(cudaEventRecord(c->ev[L.step + 1], st));
+      if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev[L.step + 1], st, cudaEventRecordExternal));
     }
     if (!fused) {
       // DISTINCT reads the packed rows on the device, so only plain
@@ -1032,7 +1035,7 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
                                                                 dS + pack_stat);
       nk++;
     }
-    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
+    if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev_q1, st, cudaEventRecordExternal));
     GSM_CUDA(cudaGetLastError());
     GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(StepStat) * (size_t)(n + 1),
                              cudaMemcpyDeviceToHost, st));
@@ -1132,6 +1135,7 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
   i64 h2d = 0;
   bool allow_fuse = true;
   std::string plan_key;
+  bool tail_event = false;  // DISTINCT ran after the captured sequence
   for (int attempt = 0;; attempt++) {
     ex = Exec{};
     c->gen++;
@@ -1217,7 +1221,10 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
         rep->prealloc_total[s] = (k == S_EXPAND || k == S_FILTER) ? hb->stats[s].e : 0;
       if (rep->device_ms) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->ev[s], c->ev[s + 1]);
+        if (cudaEventElapsedTime(&ms, c->ev[s], c->ev[s + 1]) != cudaSuccess) {
+          ms = -1.f;
+          cudaGetLastError();  // do not leave the failure pending for a later check
+        }
         rep->device_ms[s] = ms;
       }
     }
@@ -1281,7 +1288,8 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
     k_tilescan<DistinctP><<<c->grid_ts, TS_THREADS, 0, st>>>(dp, ts);
     count_launch();
     kernels++;
-    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q1, st));
+    if (timing) GSM_CUDA(cudaEventRecord(c->ev_q2, st));
+    tail_event = true;
     GSM_CUDA(cudaMemcpyAsync(&c->h_block->stats[pack_stat + 1], dp.st, sizeof(StepStat),
                              cudaMemcpyDeviceToHost, st));
     GSM_CUDA(cudaStreamSynchronize(st));
@@ -1323,7 +1331,11 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
     // buffer, or by gsm_result_copy for device-resident results)
     rep->d2h_bytes = (i64)sizeof(StepStat) * (n + 1) + d2h_extra + (i64)((size_t)r->n * row_bytes);
     rep->total_device_ms = 0.f;
-    if (timing) cudaEventElapsedTime(&rep->total_device_ms, c->ev_q0, c->ev_q1);
+    if (timing && cudaEventElapsedTime(&rep->total_device_ms, c->ev_q0,
+                                       tail_event ? c->ev_q2 : c->ev_q1) != cudaSuccess) {
+      rep->total_device_ms = -1.f;
+      cudaGetLastError();
+    }
   }
   *out = r;
   return GSM_OK;
