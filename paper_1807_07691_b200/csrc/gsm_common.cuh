@@ -87,8 +87,17 @@ __device__ __forceinline__ uint2 seg_lookup(const Orient& R, u32 key) {
   return make_uint2(0, 0);
 }
 
-// Membership of `v` in the ascending run a[0..len).
+// Membership of `v` in the ascending run a[0..len).  Short runs (the common
+// case: most keys have a handful of neighbours) are scanned with independent
+// loads — one memory round trip instead of log2(len) dependent ones.
 __device__ __forceinline__ bool sorted_contains(const u32* a, u32 len, u32 v) {
+  if (len <= 8) {
+    bool hit = false;
+#pragma unroll
+    for (u32 i = 0; i < 8; i++)
+      if (i < len) hit |= __ldg(a + i) == v;
+    return hit;
+  }
   u32 lo = 0, hi = len;
   while (lo < hi) {
     u32 mid = (lo + hi) >> 1;
@@ -99,6 +108,12 @@ __device__ __forceinline__ bool sorted_contains(const u32* a, u32 len, u32 v) {
   }
   return false;
 }
+
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; it must wait before touching the predecessor's output.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 }  // namespace gsm
 

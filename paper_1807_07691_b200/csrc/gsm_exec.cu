@@ -19,6 +19,7 @@
 // load-balanced output-slot -> row binary search, so hub rows of the
 // power-law tail are spread over all 256 threads of the tile.
 #include <algorithm>
+#include <utility>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -109,7 +110,6 @@ __device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
 // ---------------------------------------------------------------------------
 template <class P>
 __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
-  ts.epoch = *ts.epoch_ptr;
   __shared__ i64 s_pre[TS_TILE + 1];
   __shared__ u32 s_aux[TS_TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
@@ -120,6 +120,14 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
   __shared__ DTable s_in;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  pdl_wait();  // everything below reads the previous kernel's output
+  pdl_trigger();
+  ts.epoch = *ts.epoch_ptr;
+  // The first tile grab overlaps the descriptor load.
+  if (tid == 0) {
+    s_tile = atomicAdd(ts.counter, 1u);
+    s_nlong = 0;
+  }
   p.prepare(s_in);
   __syncthreads();
   const i64 n = p.rows(s_in);
@@ -129,12 +137,14 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
     return;
   }
   i64 e_acc = 0;
-  for (;;) {
-    if (tid == 0) {
-      s_tile = atomicAdd(ts.counter, 1u);
-      s_nlong = 0;
+  for (bool first = true;; first = false) {
+    if (!first) {
+      if (tid == 0) {
+        s_tile = atomicAdd(ts.counter, 1u);
+        s_nlong = 0;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
     const i64 base = (i64)t * TS_TILE;
@@ -383,6 +393,8 @@ struct DistinctP {
 // stat: e = |L|, pad = |R| (for the budget message); rows = |L|*|R|.
 __global__ void k_cross(const DTable* L, const DTable* R, int a, int b, u32* out, i64 cap,
                         i64 budget, DTable* O, StepStat* st) {
+  pdl_wait();
+  pdl_trigger();
   const i64 nl = L->n, nr = R->n;
   // |L|*|R| saturated at 2^62 (nl, nr < 2^40 in practice)
   const __int128 t128 = (__int128)nl * (__int128)nr;
@@ -407,6 +419,8 @@ __global__ void k_cross(const DTable* L, const DTable* R, int a, int b, u32* out
 // J0 against a zero-arity right table (a constant-constant pattern, R5):
 // the result is the left table itself or nothing -> descriptor aliasing.
 __global__ void k_gate(const DTable* L, const DTable* R, int a, DTable* O, StepStat* st) {
+  pdl_wait();
+  pdl_trigger();
   const int tid = threadIdx.x;
   const i64 nl = L->n, nr = R->n;
   if (tid < a) O->col[tid] = L->col[tid];
@@ -434,6 +448,8 @@ struct ResolveArgs {
   int njobs;
 };
 __global__ void k_resolve(ResolveArgs args, DTable* tables, StepStat* stats) {
+  pdl_wait();
+  pdl_trigger();
   const int i = threadIdx.x;
   if (i >= args.njobs) return;
   const ResolveJob& jb = args.job[i];
@@ -451,6 +467,8 @@ __global__ void k_resolve(ResolveArgs args, DTable* tables, StepStat* stats) {
 
 // Multi-GPU row partitioning of the first table: keep rows [n*i/k, n*(i+1)/k).
 __global__ void k_slice(DTable* T, int a, i64 part, i64 parts, StepStat* st) {
+  pdl_wait();
+  pdl_trigger();
   const i64 n = T->n;
   const i64 lo = (i64)((__int128)n * part / parts), hi = (i64)((__int128)n * (part + 1) / parts);
   __syncthreads();
@@ -471,6 +489,8 @@ struct ProjArgs {
 // become a device-resident result.  st->pad = 1 when staged.
 __global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* dev_out, i64 dev_cap,
                        u32* host_out, i64 host_cap, StepStat* st) {
+  pdl_wait();
+  pdl_trigger();
   i64 n = T->n;
   const bool to_host = host_out != nullptr && n <= host_cap;
   u32* out = to_host ? host_out : dev_out;
@@ -492,6 +512,29 @@ __global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* dev_out, i64 de
 // Host orchestration
 // ===========================================================================
 using namespace gsm;
+
+namespace {
+// Launch with Programmatic Dependent Launch allowed: the kernel's blocks may
+// be scheduled while the previous kernel in the stream drains (they block in
+// griddepcontrol.wait until its results are visible), hiding launch latency
+// between the dependent steps of a plan.  Captured into graphs as
+// programmatic edges.
+template <typename... KArgs, typename... Args>
+cudaError_t launch(bool pdl, void (*kern)(KArgs...), int grid, int block, cudaStream_t st,
+                   Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+}  // namespace
 
 namespace {
 
@@ -542,6 +585,7 @@ struct gsm_context {
   std::unordered_map<std::string, size_t> last_bytes;  // per plan: last result size
   u64 gen = 0;             // bumped by every gsm_execute (staged results expire)
   bool use_graphs = true;  // replay each distinct query's launch sequence as a CUDA graph
+  bool use_pdl = true;     // programmatic dependent launch between plan steps
   struct GraphEntry {
     cudaGraphExec_t exec;
     int kernels;
@@ -731,6 +775,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   c->store = store;
   c->device = store->device;
   if (const char* ng = getenv("GSM_NO_GRAPHS")) c->use_graphs = !(ng[0] == '1');
+  if (const char* np = getenv("GSM_NO_PDL")) c->use_pdl = !(np[0] == '1');
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
     return st;
@@ -980,12 +1025,12 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
     GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
     if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev[0], st, cudaEventRecordExternal));
     if (ex.res.njobs > 0) {
-      k_resolve<<<1, 64, 0, st>>>(ex.res, dT, dS);
+      GSM_CUDA(launch(c->use_pdl, k_resolve, 1, 64, st, ex.res, dT, dS));
       nk++;
     }
     if (parts > 1) {
-      k_slice<<<1, 64, 0, st>>>(dT + ex.plan[0].out_table, (int)ex.plan[0].schema.size(), part,
-                                parts, dS + 0);
+      GSM_CUDA(launch(c->use_pdl, k_slice, 1, 64, st, dT + ex.plan[0].out_table,
+                      (int)ex.plan[0].schema.size(), part, parts, dS + 0));
       nk++;
     }
     if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev[1], st, cudaEventRecordExternal));
@@ -997,28 +1042,29 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
         case S_EXPAND: {
           TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
           slot++;
-          k_tilescan<ExpandP><<<L.grid, TS_THREADS, 0, st>>>(L.ep, ts);
+          GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP>, L.grid, TS_THREADS, st, L.ep, ts));
           nk++;
           break;
         }
         case S_FILTER: {
           TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
           slot++;
-          k_tilescan<FilterP><<<L.grid, TS_THREADS, 0, st>>>(L.fp, ts);
+          GSM_CUDA(launch(c->use_pdl, k_tilescan<FilterP>, L.grid, TS_THREADS, st, L.fp, ts));
           nk++;
           break;
         }
         case S_CROSS: {
           Home oh = ex.home[L.out];
-          k_cross<<<L.grid, 256, 0, st>>>(dT + L.left, dT + L.right, L.a, L.b,
-                                          reinterpret_cast<u32*>(ex.buf(oh)),
-                                          ex.cap_for(L.a + L.b), budget, dT + L.out, dS + L.step);
+          GSM_CUDA(launch(c->use_pdl, k_cross, L.grid, 256, st, (const DTable*)(dT + L.left),
+                          (const DTable*)(dT + L.right), L.a, L.b,
+                          reinterpret_cast<u32*>(ex.buf(oh)), ex.cap_for(L.a + L.b), (i64)budget,
+                          dT + L.out, dS + L.step));
           nk++;
           break;
         }
         case S_GATE:
-          k_gate<<<1, 64, 0, st>>>(dT + L.left, dT + L.right, ex.arity[L.left], dT + L.out,
-                                   dS + L.step);
+          GSM_CUDA(launch(c->use_pdl, k_gate, 1, 64, st, (const DTable*)(dT + L.left),
+                          (const DTable*)(dT + L.right), ex.arity[L.left], dT + L.out, dS + L.step));
           nk++;
           break;
         default:
@@ -1030,9 +1076,9 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
       // DISTINCT reads the packed rows on the device, so only plain
       // projections are packed straight into the pinned staging buffer.
       u32* host_dst = distinct ? nullptr : c->d_stage;
-      k_pack<<<ex.grid_for_rows(ex.ub[cur], 256), 256, 0, st>>>(dT + cur, pa, n_proj, pack_out,
-                                                                pack_cap, host_dst, stage_cap,
-                                                                dS + pack_stat);
+      GSM_CUDA(launch(c->use_pdl, k_pack, ex.grid_for_rows(ex.ub[cur], 256), 256, st,
+                      (const DTable*)(dT + cur), pa, n_proj, pack_out, pack_cap, host_dst,
+                      stage_cap, dS + pack_stat));
       nk++;
     }
     if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev_q1, st, cudaEventRecordExternal));
