@@ -143,6 +143,32 @@ gsm_status gsm_execute(gsm_context* ctx, const gsm_pattern* steps, int32_t n_ste
                        int64_t row_budget, int32_t budget_mode, int64_t part_index,
                        int64_t part_count, gsm_report* report, gsm_result** out);
 
+/* One query of a batch: the arguments of gsm_execute. */
+typedef struct {
+  const gsm_pattern* steps;
+  int32_t n_steps;
+  const int32_t* proj;
+  int32_t n_proj;
+  int32_t distinct;
+  int64_t row_budget;
+  int32_t budget_mode;
+  int64_t part_index;
+  int64_t part_count;
+  gsm_report* report; /* may be NULL */
+} gsm_query;
+
+/* Evaluates n_queries independent queries concurrently: query i runs on
+ * ctxs[i] (distinct contexts = distinct streams and arenas of the same
+ * store), all launch sequences are enqueued before any is awaited, so their
+ * latency-bound join kernels overlap on the GPU (the serving counterpart of
+ * calling execute() in a loop).  statuses[i] (may be NULL) and outs[i]
+ * receive each query's outcome; the return value is the first failure in
+ * query order (GSM_OK if none), with its message in gsm_last_error().
+ * device_ms (may be NULL) receives the device time from the first launch to
+ * the end of the last query's launch sequence (CUDA events). */
+gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
+                             gsm_status* statuses, gsm_result** outs, float* device_ms);
+
 /* ---- results ---------------------------------------------------------- */
 
 /* Shape of the projected result: n_rows x n_cols (BindingTable.rows). */

@@ -15,7 +15,14 @@ from .errors import (
     UnknownPredicateError,
     UnsupportedFeatureError,
 )
-from .executor import DEFAULT_ROW_BUDGET, BindingTable, ExecutionReport, StepReport, execute
+from .executor import (
+    DEFAULT_ROW_BUDGET,
+    BindingTable,
+    ExecutionReport,
+    StepReport,
+    execute,
+    execute_batch,
+)
 from .frontend import Plan, QueryGraph, TriplePattern, bind_constants, make_plan, parse_query
 from .storage import DeviceStore, StatEntry, from_store, load
 
@@ -38,6 +45,7 @@ __all__ = [
     "UnsupportedFeatureError",
     "bind_constants",
     "execute",
+    "execute_batch",
     "from_store",
     "load",
     "make_plan",

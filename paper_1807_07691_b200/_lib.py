@@ -39,6 +39,7 @@ EXPORTS = (
     "gsm_context_create",
     "gsm_context_free",
     "gsm_execute",
+    "gsm_execute_batch",
     "gsm_result_shape",
     "gsm_result_copy",
     "gsm_result_device_ptr",
@@ -77,6 +78,23 @@ class Report(C.Structure):
     ]
 
 
+class Query(C.Structure):
+    """gsm_query"""
+
+    _fields_ = [
+        ("steps", C.POINTER(Pattern)),
+        ("n_steps", C.c_int32),
+        ("proj", C.POINTER(C.c_int32)),
+        ("n_proj", C.c_int32),
+        ("distinct", C.c_int32),
+        ("row_budget", C.c_int64),
+        ("budget_mode", C.c_int32),
+        ("part_index", C.c_int64),
+        ("part_count", C.c_int64),
+        ("report", C.POINTER(Report)),
+    ]
+
+
 _lock = threading.Lock()
 _lib: C.CDLL | None = None
 
@@ -112,6 +130,7 @@ def lib() -> C.CDLL:
                 i32,
                 [vp, P(Pattern), i32, P(i32), i32, i32, i64, i32, i64, i64, P(Report), P(vp)],
             ),
+            "gsm_execute_batch": (i32, [P(vp), i32, P(Query), P(i32), P(vp), P(C.c_float)]),
             "gsm_result_shape": (i32, [vp, P(i64), P(i32)]),
             "gsm_result_copy": (i32, [vp, vp]),
             "gsm_result_device_ptr": (i32, [vp, P(C.c_uint64)]),
@@ -136,7 +155,10 @@ def check(status: int) -> None:
     """Map a gsm_status to the reference's exception classes."""
     if status == GSM_OK:
         return
-    msg = last_error()
+    raise_status(status, last_error())
+
+
+def raise_status(status: int, msg: str) -> None:
     if status == GSM_ERR_RESOURCE:
         raise errors.ResourceLimitError(msg)
     if status == GSM_ERR_STORE_FORMAT:

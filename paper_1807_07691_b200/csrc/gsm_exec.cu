@@ -578,6 +578,7 @@ struct gsm_context {
   cudaEvent_t ev[GSM_MAX_STEPS + 2] = {};
   cudaEvent_t ev_q0 = nullptr, ev_q1 = nullptr;  // whole-query device time
   cudaEvent_t ev_q2 = nullptr;  // end of the (un-captured) DISTINCT tail
+  cudaEvent_t ev_b0 = nullptr, ev_b1 = nullptr, ev_done = nullptr;  // batch timing
   u32* h_stage = nullptr;  // pinned host result staging
   u32* d_stage = nullptr;  // device result buffer (projected rows, row-major)
   size_t stage_bytes = 0;
@@ -790,7 +791,8 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   for (auto& ev : c->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(cuda_error(e, "cudaEventCreate"));
   if ((e = cudaEventCreate(&c->ev_q0)) != cudaSuccess || (e = cudaEventCreate(&c->ev_q1)) != cudaSuccess ||
-      (e = cudaEventCreate(&c->ev_q2)) != cudaSuccess)
+      (e = cudaEventCreate(&c->ev_q2)) != cudaSuccess || (e = cudaEventCreate(&c->ev_b0)) != cudaSuccess ||
+      (e = cudaEventCreate(&c->ev_b1)) != cudaSuccess || (e = cudaEventCreate(&c->ev_done)) != cudaSuccess)
     return fail(cuda_error(e, "cudaEventCreate"));
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -826,16 +828,58 @@ gsm_status gsm_context_free(gsm_context* c) {
   if (c->ev_q0) cudaEventDestroy(c->ev_q0);
   if (c->ev_q1) cudaEventDestroy(c->ev_q1);
   if (c->ev_q2) cudaEventDestroy(c->ev_q2);
+  for (cudaEvent_t ev : {c->ev_b0, c->ev_b1, c->ev_done})
+    if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GSM_OK;
 }
 
-static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
-                           int32_t n_proj, int64_t budget, int64_t part, int64_t parts,
-                           bool timing, bool distinct, bool allow_fuse, Exec& ex, int& pack_stat,
-                           i64& pack_cap, u32*& pack_out, bool& overflow, int& kernels, i64& h2d,
-                           std::string& last_key) {
+struct QueryArgs {
+  const gsm_pattern* steps;
+  int32_t n;
+  const int32_t* proj;
+  int32_t n_proj;
+  int32_t distinct;
+  int64_t budget;
+  int32_t budget_mode;
+  int64_t part, parts;
+  gsm_report* rep;
+};
+
+// Per-query host state between launch and completion.
+struct ExecState {
+  Exec ex;
+  int pack_stat = 0;
+  i64 pack_cap = 0;
+  u32* pack_out = nullptr;
+  bool fused = false;
+  int kernels = 0;
+  i64 h2d = 0;
+  bool allow_fuse = true;
+  bool timing = false;
+  std::string plan_key;
+};
+
+// Plan the query and enqueue its whole launch sequence (as a CUDA graph
+// replay when possible) on the context's stream.  Does not synchronize.
+static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S) {
+  const gsm_pattern* steps = qa.steps;
+  const int32_t n = qa.n;
+  const int32_t* proj = qa.proj;
+  const int32_t n_proj = qa.n_proj;
+  const int64_t budget = qa.budget;
+  const int64_t part = qa.part, parts = qa.parts;
+  const bool timing = S.timing, distinct = qa.distinct != 0, allow_fuse = S.allow_fuse;
+  S.ex = Exec{};
+  c->gen++;
+  Exec& ex = S.ex;
+  int& pack_stat = S.pack_stat;
+  i64& pack_cap = S.pack_cap;
+  u32*& pack_out = S.pack_out;
+  int& kernels = S.kernels;
+  i64& h2d = S.h2d;
+  std::string& last_key = S.plan_key;
   kernels = 0;
   QueryBlock* hb = c->h_block;
   ex.c = c;
@@ -1003,6 +1047,7 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
     else launches.back().fp.fz = fz;
     fused = true;
   }
+  S.fused = fused;
 
   // ---- per-launch epochs: data in the query block, so a captured graph
   //      replays with fresh epochs and unchanged kernel parameters ----
@@ -1143,52 +1188,57 @@ static gsm_status run_once(gsm_context* c, const gsm_pattern* steps, int32_t n, 
     if (is != GSM_OK) return is;
   }
   count_launch(kernels);
-  GSM_CUDA(cudaStreamSynchronize(st));
-
-  overflow = false;
-  for (int s = 1; s < n; s++)
-    if (hb->stats[s].overflow) overflow = true;
-  if (hb->stats[pack_stat].overflow) overflow = true;
-  if (fused && hb->stats[pack_stat].pad == 3) overflow = true;  // staging too small
   return GSM_OK;
 }
 
-gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
-                       int32_t n_proj, int32_t distinct, int64_t budget, int32_t budget_mode,
-                       int64_t part, int64_t parts, gsm_report* rep, gsm_result** out) {
-  *out = nullptr;
+static gsm_status validate_query(const gsm_context* c, const QueryArgs& q) {
   if (!c) return set_error(GSM_ERR_VALUE, "null context");
-  if (n <= 0) return set_error(GSM_ERR_VALUE, "cannot execute an empty plan");
-  if (n > GSM_MAX_STEPS) return set_error(GSM_ERR_VALUE, "plan has more than 64 steps");
-  if (n_proj < 0 || (n_proj > 0 && !proj)) return set_error(GSM_ERR_VALUE, "bad projection");
-  if (parts < 1 || part < 0 || part >= parts) return set_error(GSM_ERR_VALUE, "bad partition");
-  if (budget_mode != GSM_BUDGET_SEQUENTIAL && budget_mode != GSM_BUDGET_PARALLEL)
+  if (q.n <= 0) return set_error(GSM_ERR_VALUE, "cannot execute an empty plan");
+  if (q.n > GSM_MAX_STEPS) return set_error(GSM_ERR_VALUE, "plan has more than 64 steps");
+  if (!q.steps) return set_error(GSM_ERR_VALUE, "null plan");
+  if (q.n_proj < 0 || (q.n_proj > 0 && !q.proj)) return set_error(GSM_ERR_VALUE, "bad projection");
+  if (q.parts < 1 || q.part < 0 || q.part >= q.parts) return set_error(GSM_ERR_VALUE, "bad partition");
+  if (q.budget_mode != GSM_BUDGET_SEQUENTIAL && q.budget_mode != GSM_BUDGET_PARALLEL)
     return set_error(GSM_ERR_VALUE, "bad budget mode");
-  for (int s = 0; s < n; s++) {
-    const gsm_pattern& p = steps[s];
+  for (int s = 0; s < q.n; s++) {
+    const gsm_pattern& p = q.steps[s];
     if (p.s_var >= GSM_MAX_VARS || p.o_var >= GSM_MAX_VARS || p.s_var < -1 || p.o_var < -1)
       return set_error(GSM_ERR_VALUE, "variable index out of range");
   }
-  GSM_CUDA(cudaSetDevice(c->device));
-  const bool timing = rep && rep->device_ms;
+  return GSM_OK;
+}
 
-  Exec ex{};
-  int pack_stat = 0;
-  i64 pack_cap = 0;
-  u32* pack_out = nullptr;
-  bool overflow = false;
-  int kernels = 0;
-  i64 h2d = 0;
-  bool allow_fuse = true;
-  std::string plan_key;
+static gsm_status begin_query(gsm_context* c, const QueryArgs& q, ExecState& S) {
+  gsm_status v = validate_query(c, q);
+  if (v != GSM_OK) return v;
+  GSM_CUDA(cudaSetDevice(c->device));
+  S.timing = q.rep && q.rep->device_ms;
+  return launch_query(c, q, S);
+}
+
+// Wait for a launched query, apply the budget rules, re-run on arena /
+// staging overflow, and hand the result over.
+static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState& S,
+                                 gsm_result** out) {
+  *out = nullptr;
+  const int32_t n = qa.n, n_proj = qa.n_proj, budget_mode = qa.budget_mode;
+  const int64_t budget = qa.budget;
+  const bool distinct = qa.distinct != 0, timing = S.timing;
+  gsm_report* rep = qa.rep;
+  Exec& ex = S.ex;
+  int& pack_stat = S.pack_stat;
+  i64& pack_cap = S.pack_cap;
+  u32*& pack_out = S.pack_out;
+  int& kernels = S.kernels;
+  i64& h2d = S.h2d;
+  std::string& plan_key = S.plan_key;
   bool tail_event = false;  // DISTINCT ran after the captured sequence
   for (int attempt = 0;; attempt++) {
-    ex = Exec{};
-    c->gen++;
-    gsm_status stt = run_once(c, steps, n, proj, n_proj, budget, part, parts, timing, distinct != 0,
-                              allow_fuse, ex, pack_stat, pack_cap, pack_out, overflow, kernels, h2d,
-                              plan_key);
-    if (stt != GSM_OK) return stt;
+    if (attempt > 0) {
+      gsm_status stt = launch_query(c, qa, S);
+      if (stt != GSM_OK) return stt;
+    }
+    GSM_CUDA(cudaStreamSynchronize(c->stream));
     const QueryBlock* hb = c->h_block;
     // Budget checks in plan order (executor.py:158-163, 192-193, 237-241).
     // A step's counters are exact as long as no earlier step overflowed.
@@ -1234,7 +1284,7 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
       // device-side pack, and grow staging (<= 1 GiB) for the next query.
       size_t want = (size_t)hb->stats[pack_stat].rows * 4 * (size_t)std::max(n_proj, 1);
       if (want <= ((size_t)1 << 30)) ctx_set_stage(c, want + want / 4);
-      allow_fuse = false;
+      S.allow_fuse = false;
       continue;
     }
     if (!ovf) break;
@@ -1385,6 +1435,74 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
   }
   *out = r;
   return GSM_OK;
+}
+
+gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
+                       int32_t n_proj, int32_t distinct, int64_t budget, int32_t budget_mode,
+                       int64_t part, int64_t parts, gsm_report* rep, gsm_result** out) {
+  *out = nullptr;
+  QueryArgs qa{steps, n, proj, n_proj, distinct, budget, budget_mode, part, parts, rep};
+  ExecState S;
+  gsm_status st = begin_query(c, qa, S);
+  if (st != GSM_OK) return st;
+  return complete_query(c, qa, S, out);
+}
+
+gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
+                             gsm_status* statuses, gsm_result** outs, float* device_ms) {
+  if (n_queries < 0 || (n_queries > 0 && (!ctxs || !queries || !outs)))
+    return set_error(GSM_ERR_VALUE, "bad batch arguments");
+  for (int i = 0; i < n_queries; i++) {
+    outs[i] = nullptr;
+    for (int j = 0; j < i; j++)
+      if (ctxs[j] == ctxs[i]) return set_error(GSM_ERR_VALUE, "batch contexts must be distinct");
+  }
+  std::vector<ExecState> S((size_t)n_queries);
+  std::vector<QueryArgs> qa((size_t)n_queries);
+  std::vector<gsm_status> st((size_t)n_queries, GSM_OK);
+  std::vector<std::string> msg((size_t)n_queries);
+  const bool timed = device_ms && n_queries > 0;
+  if (device_ms) *device_ms = 0.f;
+  if (timed) {  // all streams start after ev_b0 ...
+    GSM_CUDA(cudaSetDevice(ctxs[0]->device));
+    GSM_CUDA(cudaEventRecord(ctxs[0]->ev_b0, ctxs[0]->stream));
+    for (int i = 1; i < n_queries; i++) GSM_CUDA(cudaStreamWaitEvent(ctxs[i]->stream, ctxs[0]->ev_b0, 0));
+  }
+  // Phase 1: enqueue every query on its own context's stream (they overlap).
+  for (int i = 0; i < n_queries; i++) {
+    const gsm_query& q = queries[i];
+    qa[i] = QueryArgs{q.steps, q.n_steps, q.proj, q.n_proj, q.distinct, q.row_budget,
+                      q.budget_mode, q.part_index, q.part_count, q.report};
+    st[i] = begin_query(ctxs[i], qa[i], S[i]);
+    if (st[i] != GSM_OK) msg[i] = gsm_last_error();
+  }
+  if (timed) {  // ... and ev_b1 on stream 0 follows all of them
+    for (int i = 1; i < n_queries; i++) {
+      GSM_CUDA(cudaEventRecord(ctxs[i]->ev_done, ctxs[i]->stream));
+      GSM_CUDA(cudaStreamWaitEvent(ctxs[0]->stream, ctxs[i]->ev_done, 0));
+    }
+    GSM_CUDA(cudaEventRecord(ctxs[0]->ev_b1, ctxs[0]->stream));
+  }
+  // Phase 2: complete in order (budget checks, retries, result hand-off).
+  gsm_status first = GSM_OK;
+  std::string first_msg;
+  for (int i = 0; i < n_queries; i++) {
+    if (st[i] == GSM_OK) {
+      st[i] = complete_query(ctxs[i], qa[i], S[i], &outs[i]);
+      if (st[i] != GSM_OK) msg[i] = gsm_last_error();
+    }
+    if (statuses) statuses[i] = st[i];
+    if (st[i] != GSM_OK && first == GSM_OK) {
+      first = st[i];
+      first_msg = msg[i];
+    }
+  }
+  if (timed && cudaEventElapsedTime(device_ms, ctxs[0]->ev_b0, ctxs[0]->ev_b1) != cudaSuccess) {
+    *device_ms = -1.f;
+    cudaGetLastError();
+  }
+  if (first != GSM_OK) set_error(first, first_msg);
+  return first;
 }
 
 }  // extern "C"

@@ -204,12 +204,7 @@ def execute(
     rep_struct = None
     rows_buf = pre_buf = ms_buf = kind_buf = ar_buf = None
     if report is not None:
-        rows_buf = (C.c_int64 * n)()
-        pre_buf = (C.c_int64 * n)()
-        ms_buf = (C.c_float * n)()
-        kind_buf = (C.c_int32 * n)()
-        ar_buf = (C.c_int32 * n)()
-        rep_struct = _lib.Report(rows_buf, pre_buf, ms_buf, kind_buf, ar_buf)
+        rep_struct, (rows_buf, pre_buf, ms_buf, kind_buf, ar_buf) = _new_report(n)
 
     L = _lib.lib()
     res = C.c_void_p()
@@ -220,6 +215,14 @@ def execute(
         C.byref(res),
     )
     _lib.check(st)
+    out = _fetch(L, res)
+    if report is not None:
+        _fill_report(report, steps, rep_struct, rows_buf, pre_buf, ms_buf, kind_buf, ar_buf)
+    return BindingTable(tuple(query.projection), array=out)
+
+
+def _fetch(L, res) -> np.ndarray:
+    """Copy a gsm_result's rows into a new (n, k) uint32 array and free it."""
     try:
         nrows = C.c_int64(0)
         ncols = C.c_int32(0)
@@ -229,23 +232,93 @@ def execute(
             _lib.check(L.gsm_result_copy(res, out.ctypes.data))
     finally:
         L.gsm_result_free(res)
+    return out
 
-    if report is not None:
-        # matrix_of(): one preparation per distinct pid, one use per step (executor.py:315-325)
-        seen: set[int] = set()
-        for pat in steps:
-            if pat.p not in seen:
-                seen.add(pat.p)
-                report.preparations += 1
-            report.uses += 1
-        for i, pat in enumerate(steps):
-            report.steps.append(
-                StepReport(_pattern_text(pat), int(rows_buf[i]), int(pre_buf[i]), float(ms_buf[i]) / 1e3)
-            )
-            report.kinds.append(_lib.STEP_KINDS[kind_buf[i]])
-            report.arities.append(int(ar_buf[i]))
-        report.device_seconds += rep_struct.total_device_ms / 1e3
-        report.h2d_bytes += int(rep_struct.h2d_bytes)
-        report.d2h_bytes += int(rep_struct.d2h_bytes)
-        report.kernels += int(rep_struct.kernels)
-    return BindingTable(tuple(query.projection), array=out)
+
+def _new_report(n: int):
+    bufs = ((C.c_int64 * n)(), (C.c_int64 * n)(), (C.c_float * n)(), (C.c_int32 * n)(),
+            (C.c_int32 * n)())
+    return _lib.Report(*bufs), bufs
+
+
+def _fill_report(report, steps, rep_struct, rows_buf, pre_buf, ms_buf, kind_buf, ar_buf) -> None:
+    # matrix_of(): one preparation per distinct pid, one use per step (executor.py:315-325)
+    seen: set[int] = set()
+    for pat in steps:
+        if pat.p not in seen:
+            seen.add(pat.p)
+            report.preparations += 1
+        report.uses += 1
+    for i, pat in enumerate(steps):
+        report.steps.append(
+            StepReport(_pattern_text(pat), int(rows_buf[i]), int(pre_buf[i]), float(ms_buf[i]) / 1e3)
+        )
+        report.kinds.append(_lib.STEP_KINDS[kind_buf[i]])
+        report.arities.append(int(ar_buf[i]))
+    report.device_seconds += rep_struct.total_device_ms / 1e3
+    report.h2d_bytes += int(rep_struct.h2d_bytes)
+    report.d2h_bytes += int(rep_struct.d2h_bytes)
+    report.kernels += int(rep_struct.kernels)
+
+
+def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW_BUDGET,
+                  reports: list | None = None, batch_timing: list | None = None) -> list[BindingTable]:
+    """Evaluate independent queries concurrently (``gsm_execute_batch``).
+
+    ``items`` is a sequence of ``(query, plan)``; query i runs on its own
+    context/stream, and all launch sequences are enqueued before any is
+    awaited.  Same results and errors as calling :func:`execute` on each in
+    order (the first failing query's exception is raised).  When
+    ``batch_timing`` is a list, the batch's device time in seconds is appended.
+    """
+    if mode not in _MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    items = list(items)
+    if not items:
+        return []
+    dstore = store if isinstance(store, DeviceStore) else from_store(store)
+    n = len(items)
+    budget_mode = _lib.GSM_BUDGET_SEQUENTIAL if mode == "sequential" else _lib.GSM_BUDGET_PARALLEL
+    budget = min(int(row_budget), (1 << 63) - 1)
+    ctxs = dstore.context_pool(n)
+    ctx_arr = (C.c_void_p * n)(*[c.value for c in ctxs])
+    qarr = (_lib.Query * n)()
+    prepared = []  # keeps every ctypes buffer alive until the call returns
+    for i, (query, plan) in enumerate(items):
+        if not plan.steps:
+            raise ValueError("cannot execute an empty plan")
+        steps, arr, proj_arr, nproj = compile_plan(query, plan)
+        rep_struct, bufs = _new_report(len(steps)) if reports is not None else (None, None)
+        prepared.append((steps, arr, proj_arr, rep_struct, bufs))
+        q = qarr[i]
+        q.steps = arr
+        q.n_steps = len(steps)
+        q.proj = proj_arr
+        q.n_proj = nproj
+        q.distinct = 1 if query.distinct else 0
+        q.row_budget = budget
+        q.budget_mode = budget_mode
+        q.part_index, q.part_count = 0, 1
+        q.report = C.pointer(rep_struct) if rep_struct is not None else None
+    outs = (C.c_void_p * n)()
+    statuses = (C.c_int32 * n)()
+    ms = C.c_float(0.0)
+    L = _lib.lib()
+    st = L.gsm_execute_batch(ctx_arr, n, qarr, statuses, outs,
+                             C.byref(ms) if batch_timing is not None else None)
+    if st != _lib.GSM_OK:
+        msg = _lib.last_error()
+        for i in range(n):
+            if outs[i]:
+                L.gsm_result_free(outs[i])
+        _lib.raise_status(st, msg)
+    results = []
+    for i, (query, plan) in enumerate(items):
+        out = _fetch(L, C.c_void_p(outs[i]))
+        steps, _, _, rep_struct, bufs = prepared[i]
+        if reports is not None:
+            _fill_report(reports[i], steps, rep_struct, *bufs)
+        results.append(BindingTable(tuple(query.projection), array=out))
+    if batch_timing is not None:
+        batch_timing.append(ms.value / 1e3)
+    return results

@@ -140,6 +140,21 @@ class DeviceStore:
             self._ctx.handle = ctx
         return ctx
 
+    def context_pool(self, n: int, arena_bytes: int = 256 << 20) -> list[C.c_void_p]:
+        """n distinct contexts (streams + arenas) for concurrent batch execution.
+
+        Pool contexts start with a small arena (grown on demand by the
+        library), so a wide pool does not reserve n full-size arenas.
+        """
+        with self._ctx_lock:
+            pool = self.__dict__.setdefault("_pool", [])
+            while len(pool) < n:
+                ctx = C.c_void_p()
+                _lib.check(_lib.lib().gsm_context_create(self._handle, int(arena_bytes), C.byref(ctx)))
+                self._contexts.append(ctx)
+                pool.append(ctx)
+            return pool[:n]
+
     def close(self) -> None:
         self._finalizer()
 

@@ -216,3 +216,26 @@ def test_graph_replay_matches_fresh_launches(store_factory, tmp_path):
     out = subprocess.run([sys.executable, "-c", script], env=env, check=True, capture_output=True,
                          text=True).stdout
     assert json.loads(out.strip().splitlines()[-1]) == fps
+
+
+def test_execute_batch_matches_sequential(store_factory):
+    """gsm_execute_batch: the 14 LUBM queries concurrently on 14 streams give
+    the same bags and reports as one-by-one execution; errors propagate."""
+    store = g.load(store_factory("lubm", univ=3, seed=2))
+    items = [_plan(store, text) for _, text in lubm_queries()]
+    seq = [g.execute(q, p, store) for q, p in items]
+    for rep_round in range(3):  # first round captures graphs, later rounds replay
+        reps = [g.ExecutionReport() for _ in items]
+        timing = []
+        got = g.execute_batch(items, store, reports=reps, batch_timing=timing)
+        assert len(got) == len(seq)
+        for a, b, (q, p), r in zip(got, seq, items, reps):
+            assert orc.fingerprint_array(a.array) == orc.fingerprint_array(b.array)
+            assert a.schema == b.schema
+            assert len(r.steps) == len(p.steps)
+        assert timing and timing[0] > 0
+    # a budget violation in one query raises the reference's error
+    q9 = dict(lubm_queries())["q09"]
+    bad = items[:3] + [_plan(store, q9)]
+    with pytest.raises(g.ResourceLimitError, match="pre-allocated join region"):
+        g.execute_batch(bad, store, row_budget=5)
