@@ -216,11 +216,16 @@ def run_ours(args):
             print(json.dumps(run_probe(g, store, _peaks()[0], reps=2)))
             return
 
+        items = [(q, plan) for _, q, plan in queries]
+
         def one_step(collect):
-            """One step = the 14 queries, twice, each pass after an L2 flush:
-            (1) device pass with a report (CUDA-event device time + counters),
-            (2) end-to-end pass exactly as a user calls execute() (no report),
-                wall clock incl. H2D of the query block and D2H of the rows."""
+            """One step = the 14 queries, three passes, each after an L2 flush:
+            (A) one by one with a report: per-query device latency (CUDA
+                events inside the library), step counters, per-kernel times;
+            (B) one by one exactly as a user calls execute() (no report), wall
+                clock incl. H2D of the query block and D2H of the result rows;
+            (C) the same 14 queries as one execute_batch() call (concurrent
+                streams): device time (events) and wall clock."""
             flush.add_(1)
             torch.cuda.synchronize()
             per_q = []
@@ -233,8 +238,15 @@ def run_ours(args):
             t0 = time.perf_counter()
             for name, q, plan in queries:
                 g.execute(q, plan, store)
-            wall = time.perf_counter() - t0
-            return wall, per_q
+            wall_seq = time.perf_counter() - t0
+            flush.add_(1)
+            torch.cuda.synchronize()
+            bt = []
+            t0 = time.perf_counter()
+            g.execute_batch(items, store, batch_timing=bt)
+            wall_batch = time.perf_counter() - t0
+            return {"per_q": per_q, "wall_seq": wall_seq, "wall_batch": wall_batch,
+                    "dev_batch": bt[0]}
 
         clk = ClockSampler(local).__enter__()  # sampling starts before warm-up (nvidia-smi start-up)
         time.sleep(0.5)
@@ -257,41 +269,44 @@ def run_ours(args):
             torch.distributed.barrier()
         launches = _lib.kernel_launches() - launches0
 
-        dev_s = sum(rep.device_seconds for _, per_q in steps for _, rep, _ in per_q)
-        wall_s = sum(w for w, _ in steps)
-        rows = sum(_join_rows(rep.steps) for _, per_q in steps for _, rep, _ in per_q)
-        delta = sum(rep.intermediate_total for _, per_q in steps for _, rep, _ in per_q)
-        h2d = sum(rep.h2d_bytes for _, per_q in steps for _, rep, _ in per_q) / args.steps
-        d2h = sum(rep.d2h_bytes for _, per_q in steps for _, rep, _ in per_q) / args.steps
+        all_q = [x for st_ in steps for x in st_["per_q"]]
+        dev_seq = sum(rep.device_seconds for _, rep, _ in all_q)
+        dev_s = sum(st_["dev_batch"] for st_ in steps)
+        wall_seq = sum(st_["wall_seq"] for st_ in steps)
+        wall_s = sum(st_["wall_batch"] for st_ in steps)
+        rows = sum(_join_rows(rep.steps) for _, rep, _ in all_q)
+        delta = sum(rep.intermediate_total for _, rep, _ in all_q)
+        h2d = sum(rep.h2d_bytes for _, rep, _ in all_q) / args.steps
+        d2h = sum(rep.d2h_bytes for _, rep, _ in all_q) / args.steps
 
         # roofline per kernel class from the per-step device events
         cls: dict[str, list[float]] = {}
-        for _, per_q in steps:
-            for _, rep, _ in per_q:
-                for i in range(1, len(rep.steps)):
-                    k = rep.kinds[i]
-                    if k not in ("expand", "filter", "cross"):
-                        continue
-                    L = rep.steps[i - 1].rows
-                    a = rep.arities[i - 1]
-                    b = _step_bytes(k, L, a, rep.steps[i].prealloc_total, rep.steps[i].rows,
-                                    rep.arities[i])
-                    c = cls.setdefault(k, [0.0, 0.0, 0])
-                    c[0] += b
-                    c[1] += rep.steps[i].seconds
-                    c[2] += 1
+        for _, rep, _ in all_q:
+            for i in range(1, len(rep.steps)):
+                k = rep.kinds[i]
+                if k not in ("expand", "filter", "cross"):
+                    continue
+                L = rep.steps[i - 1].rows
+                a = rep.arities[i - 1]
+                b = _step_bytes(k, L, a, rep.steps[i].prealloc_total, rep.steps[i].rows,
+                                rep.arities[i])
+                c = cls.setdefault(k, [0.0, 0.0, 0])
+                c[0] += b
+                c[1] += rep.steps[i].seconds
+                c[2] += 1
 
         lat = {}
         for name, *_ in queries:
-            d = [rep.device_seconds for _, per_q in steps for n, rep, _ in per_q if n == name]
+            d = [rep.device_seconds for n, rep, _ in all_q if n == name]
             lat[name] = round(1e3 * statistics.median(d), 4)
 
         if world > 1:
-            t = torch.tensor([dev_s, wall_s], dtype=torch.float64, device=f"cuda:{local}")
+            t = torch.tensor([dev_s, wall_s, dev_seq, wall_seq], dtype=torch.float64,
+                             device=f"cuda:{local}")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             r = torch.tensor([rows], dtype=torch.float64, device=f"cuda:{local}")
             torch.distributed.all_reduce(r)
-            dev_s, wall_s = float(t[0]), float(t[1])
+            dev_s, wall_s, dev_seq, wall_seq = (float(x) for x in t)
             rows_all = float(r[0])
         else:
             rows_all = float(rows)
@@ -340,13 +355,20 @@ def run_ours(args):
             "dtype": "u32",
             "data": "synthetic (datagen/gsmgen lubm, seeded)",
             "config": {"workload": f"LUBM-style U={args.univ} ({triples} triples), Q1-Q14 "
-                                   "(datagen/queries/lubm), one step = 14 queries",
+                                   "(datagen/queries/lubm), one step = 14 queries "
+                                   "(executed concurrently via execute_batch)",
                        "univ": args.univ, "seed": args.seed, "triples": triples,
                        "l2": "flushed before every step (256 MB write)",
                        "parallelism": f"replica x{world}"},
             "e2e": {"value": round(rows_all / wall_s, 1) if wall_s > 0 else 0.0, "unit": "rows/s",
                     "ms_per_step": round(1e3 * wall_s / args.steps, 4),
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "sequential": {"value": round(rows_all / dev_seq, 1) if dev_seq > 0 else 0.0,
+                           "ms_per_step": round(1e3 * dev_seq / args.steps, 4),
+                           "e2e": round(rows_all / wall_seq, 1) if wall_seq > 0 else 0.0,
+                           "e2e_ms_per_step": round(1e3 * wall_seq / args.steps, 4),
+                           "note": "queries one at a time (value/e2e above: the step's 14 "
+                                   "queries as one execute_batch call on 14 streams)"},
             "latency_ms": lat,
             "join_rows_per_step": rows // args.steps,
             "intermediate_rows_per_step": delta // args.steps,
@@ -432,6 +454,12 @@ def run_reference(args):
             "config": {"workload": f"LUBM-style U={args.univ} ({store.triple_count} triples), "
                                    "Q1-Q14, one step = 14 queries",
                        "univ": args.univ, "seed": args.seed},
+            "sequential": {"value": round(rows_all / dev_seq, 1) if dev_seq > 0 else 0.0,
+                           "ms_per_step": round(1e3 * dev_seq / args.steps, 4),
+                           "e2e": round(rows_all / wall_seq, 1) if wall_seq > 0 else 0.0,
+                           "e2e_ms_per_step": round(1e3 * wall_seq / args.steps, 4),
+                           "note": "queries one at a time (value/e2e above: the step's 14 "
+                                   "queries as one execute_batch call on 14 streams)"},
             "latency_ms": lat,
             "cpu_baseline": {"value": round(value, 1), "unit": "rows/s", "cores": cores,
                              "kind": "reference",
