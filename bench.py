@@ -68,11 +68,13 @@ def _args():
 # Kernel-at-scale probe on the same store: self-joins whose expand step writes
 # tens of millions of rows, so the join kernel's HBM roofline is measured
 # where bandwidth (not launch latency) decides.  Not part of `value`.
+# SELECT * keeps the written bytes equal to the expand's full output (a+1
+# columns) whether or not the projection is fused into the kernel.
 PROBES = [
     ("memberOf_coworkers", "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
-     "SELECT ?d WHERE { ?x ub:memberOf ?d . ?y ub:memberOf ?d . }"),
+     "SELECT * WHERE { ?x ub:memberOf ?d . ?y ub:memberOf ?d . }"),
     ("takesCourse_classmates", "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
-     "SELECT ?c WHERE { ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }"),
+     "SELECT * WHERE { ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }"),
 ]
 
 

@@ -7,14 +7,14 @@
 set -u
 out=gpurun_out
 mkdir -p $out
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
+: ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe > $out/ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:FilterP -s 30 -c 3 \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:FilterP -s 30 -c 3 \
     -o $out/prof_filter python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe \
     > $out/ncu_filter.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:ExpandP -s 15 -c 3 \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:ExpandP -s 15 -c 3 \
     -o $out/prof_expand_lubm python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe \
     > $out/ncu_expand_lubm.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:ExpandP -c 1 \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:ExpandP -c 1 \
     -o $out/prof_expand_probe python bench.py --only-probe > $out/ncu_probe.log 2>&1
 echo done

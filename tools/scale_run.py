@@ -1,0 +1,117 @@
+#!/usr/bin/env python
+"""Scale run (BASELINE.json configs[2]: LUBM-style U=1000, ~130M triples,
+complex cyclic / snowflake queries on 1 B200) with parity and a CPU baseline.
+
+For every query of datagen/queries/lubm and datagen/queries/lubm_complex:
+  * GPU: warm-up, then median device latency (CUDA events) over --reps runs,
+    result rows, join rows, per-step report;
+  * parity: the C oracle (oracle/gsm_oracle.c, the reference executor
+    restated, 1 core) on the same store — multiset fingerprint (count, sum,
+    xor of splitmix64 row hashes) and, when the result has at most
+    --exact-rows rows, an exact lexicographic comparison;
+  * the oracle's wall time is the CPU baseline at this scale (the Python
+    reference needs ~550 MB RAM and ~13 s per million triples to build, so
+    it is not run here; SURVEY.md §7 "Oracle at scale").
+Row budget is 2^62 in both engines.  One JSON line per query,
+then a summary line.  Usage:
+    python tools/scale_run.py --univ 1000 [--reps 5] [--skip-oracle-above 400000000]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(REPO))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--univ", type=int, default=1000)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--exact-rows", type=int, default=20_000_000)
+    ap.add_argument("--skip-oracle-above", type=int, default=400_000_000,
+                    help="skip the oracle when a step's E exceeds this (host RAM guard)")
+    ap.add_argument("--store", default=None, help="reuse an existing store directory")
+    args = ap.parse_args()
+
+    import numpy as np
+
+    import paper_1807_07691_b200 as g
+    from oracle import oracle as orc
+
+    subprocess.run(["make", "-s", "-C", str(REPO / "oracle")], check=True)
+    tmp = tempfile.mkdtemp(prefix="gsm_scale_")
+    store_dir = args.store or f"{tmp}/lubm{args.univ}"
+    t0 = time.perf_counter()
+    if not args.store:
+        subprocess.run([str(REPO / "oracle/_build/gsmgen"), "lubm", "--univ", str(args.univ),
+                        "--seed", str(args.seed), "--out", store_dir], check=True,
+                       stdout=subprocess.DEVNULL)
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    store = g.load(store_dir)
+    t_load = time.perf_counter() - t0
+    print(json.dumps({"store": store_dir, "triples": store.triple_count,
+                      "nodes": store.node_count, "gen_s": round(t_gen, 1),
+                      "load_s": round(t_load, 2), "device_bytes": store.device_bytes()}),
+          flush=True)
+    prep = orc.PreparedStore(store.matrices)
+    qfiles = sorted((REPO / "datagen/queries/lubm").glob("*.rq")) + \
+        sorted((REPO / "datagen/queries/lubm_complex").glob("*.rq"))
+    summary = {"gpu_ms": 0.0, "cpu_s": 0.0, "join_rows": 0, "parity_ok": 0, "parity_checked": 0}
+    for qf in qfiles:
+        q = g.bind_constants(g.parse_query(qf.read_text()), store.dictionary)
+        plan = g.make_plan(q, store.stats)
+        budget = 1 << 62
+        res = g.execute(q, plan, store, row_budget=budget)
+        dev = []
+        rep = None
+        for _ in range(args.reps):
+            rep = g.ExecutionReport()
+            g.execute(q, plan, store, row_budget=budget, report=rep)
+            dev.append(rep.device_seconds)
+        rec = {"query": qf.stem, "rows": len(res), "step_rows": [s.rows for s in rep.steps],
+               "step_prealloc": [s.prealloc_total for s in rep.steps], "kinds": rep.kinds,
+               "gpu_ms": round(1e3 * statistics.median(dev), 3),
+               "join_rows": sum(s.rows for s in rep.steps[1:])}
+        rec["join_rows_per_s"] = round(rec["join_rows"] / statistics.median(dev), 1)
+        if max(rec["step_prealloc"] + [0]) <= args.skip_oracle_above and \
+                max(rec["step_rows"]) <= args.skip_oracle_above:
+            t0 = time.perf_counter()
+            rows, srows, spre = orc.run(prep, [s.pattern for s in plan.steps], q.projection,
+                                        q.distinct, budget=budget)
+            rec["cpu_oracle_s"] = round(time.perf_counter() - t0, 3)
+            exp = np.asarray(rows, dtype=np.uint32).reshape(len(rows), len(q.projection))
+            del rows
+            ok = orc.fingerprint_array(exp) == orc.fingerprint_array(res.array)
+            ok = ok and srows == rec["step_rows"] and spre == rec["step_prealloc"]
+            if ok and len(res) <= args.exact_rows and exp.shape[1]:
+                a = res.array[np.lexsort(res.array.T[::-1])]
+                b = exp[np.lexsort(exp.T[::-1])]
+                ok = bool(np.array_equal(a, b))
+                rec["exact_compare"] = True
+            rec["parity"] = bool(ok)
+            summary["parity_checked"] += 1
+            summary["parity_ok"] += int(ok)
+            summary["cpu_s"] += rec["cpu_oracle_s"]
+        else:
+            rec["parity"] = "skipped (host RAM guard)"
+        summary["gpu_ms"] += rec["gpu_ms"]
+        summary["join_rows"] += rec["join_rows"]
+        print(json.dumps(rec), flush=True)
+    print(json.dumps({"summary": summary}), flush=True)
+    if not args.store:
+        subprocess.run(["rm", "-rf", tmp])
+
+
+if __name__ == "__main__":
+    main()
