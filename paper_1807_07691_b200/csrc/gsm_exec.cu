@@ -341,6 +341,240 @@ struct FilterP {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Fused step group: [filters on the left row] [expand] [filters on each
+// candidate] as ONE kernel.  The intermediate tables of the fused steps are
+// never materialised, but every fused step still produces its exact
+// StepReport counters (rows, prealloc_total E) for the report and the budget
+// rules: they are accumulated per block in shared memory and added to the
+// step's stats slot at the end.  Rows whose candidate list is long (hubs) are
+// counted and emitted warp-cooperatively (ballot compaction keeps the output
+// positions of surviving candidates dense and ordered).
+// ---------------------------------------------------------------------------
+constexpr int MAXF = 8;              // filters on each side of the expand
+constexpr int MAXGS = 2 * MAXF + 1;  // steps in a group
+
+struct FSpec {
+  Orient R;   // orientation searched
+  int mode;   // F_PAIR / F_CONST / F_SELF
+  int kc;     // virtual-row column of the lookup key (a = the expanded column)
+  int tc;     // F_PAIR: virtual-row column of the target
+  u32 cval;   // F_CONST target
+  int slot;   // counter slot (step) of this filter
+};
+
+struct GroupP {
+  const DTable* L;
+  int a;             // left arity
+  int npre, npost;   // f[0, npre) gate left rows, f[npre, npre+npost) test candidates
+  FSpec f[2 * MAXF];
+  int has_x;         // an expand step is fused
+  Orient X;
+  int xk, xslot;
+  int nslots;
+  int last_slot;     // slot of the group's final step
+  StepStat* st[MAXGS];
+  u32* out;          // columnar output (when not fused into the result)
+  i64 cap;
+  DTable* O;
+  FusedOut fz;
+};
+
+__device__ __forceinline__ u32 vcol(const DTable& s, int a, int c, i64 r, u32 cand) {
+  return c < a ? __ldg(s.col[c] + r) : cand;
+}
+
+// Evaluate filter f on virtual row (r, cand); accumulate E / rows when acc.
+__device__ __forceinline__ bool gfilter(const FSpec& f, const DTable& s, int a, i64 r, u32 cand,
+                                        unsigned long long* acc) {
+  const u32 key = vcol(s, a, f.kc, r, cand);
+  const uint2 sg = seg_lookup(f.R, key);
+  const u32 target = f.mode == F_PAIR ? vcol(s, a, f.tc, r, cand) : f.mode == F_CONST ? f.cval : key;
+  const bool keep = sg.y && sorted_contains(f.R.dst + sg.x, sg.y, target);
+  if (acc) {
+    atomicAdd(acc + 2 * f.slot, (unsigned long long)(f.mode == F_PAIR ? sg.y : (u32)keep));
+    if (keep) atomicAdd(acc + 2 * f.slot + 1, 1ull);
+  }
+  return keep;
+}
+
+__device__ __forceinline__ bool gpost(const GroupP& p, const DTable& s, i64 r, u32 cand,
+                                      unsigned long long* acc) {
+  for (int i = p.npre; i < p.npre + p.npost; i++)
+    if (!gfilter(p.f[i], s, p.a, r, cand, acc)) return false;
+  return true;
+}
+
+__device__ __forceinline__ void gwrite(const GroupP& p, const DTable& s, i64 r, u32 cand, i64 g) {
+  if (p.fz.stage) {
+    if (g >= p.fz.cap) return;
+    u32* o = p.fz.stage + g * p.fz.k;
+    for (int x = 0; x < p.fz.k; x++) o[x] = vcol(s, p.a, p.fz.pj[x], r, cand);
+    return;
+  }
+  if (g >= p.cap) return;
+  for (int c = 0; c < p.a; c++) p.out[(i64)c * p.cap + g] = __ldg(s.col[c] + r);
+  if (p.has_x) p.out[(i64)p.a * p.cap + g] = cand;
+}
+
+__global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
+  __shared__ i64 s_pre[TS_TILE + 1];
+  __shared__ u32 s_aux[TS_TILE];
+  __shared__ u32 s_len[TS_TILE];
+  __shared__ i64 s_wsum[TS_THREADS / 32];
+  __shared__ i64 s_base;
+  __shared__ u32 s_tile;
+  __shared__ int s_long[TS_TILE];
+  __shared__ int s_nlong;
+  __shared__ unsigned long long s_acc[2 * MAXGS];
+  __shared__ DTable s_in;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  pdl_wait();
+  pdl_trigger();
+  ts.epoch = *ts.epoch_ptr;
+  if (tid == 0) {
+    s_tile = atomicAdd(ts.counter, 1u);
+    s_nlong = 0;
+  }
+  if (tid < 2 * MAXGS) s_acc[tid] = 0;
+  copy_desc(s_in, p.L, p.a);
+  __syncthreads();
+  const i64 n = s_in.n;
+  const i64 ntiles = (n + TS_TILE - 1) / TS_TILE;
+  if (ntiles == 0) {
+    if (blockIdx.x == 0 && tid == 0) {
+      p.O->n = 0;
+      if (p.fz.stage) p.fz.finish(0);
+    }
+    return;
+  }
+  for (bool first = true;; first = false) {
+    if (!first) {
+      if (tid == 0) {
+        s_tile = atomicAdd(ts.counter, 1u);
+        s_nlong = 0;
+      }
+      __syncthreads();
+    }
+    const u32 t = s_tile;
+    if ((i64)t >= ntiles) break;
+    const i64 base = (i64)t * TS_TILE;
+    const i64 r = base + tid;
+    // ---- count: pre-filters, expand, post-filters on short candidate lists
+    u32 cnt = 0, aux = 0, len = 0;
+    bool warp_row = false;
+    if (r < n) {
+      bool pass = true;
+      for (int i = 0; i < p.npre && pass; i++) pass = gfilter(p.f[i], s_in, p.a, r, 0u, s_acc);
+      if (pass) {
+        if (!p.has_x) {
+          len = 1;
+          cnt = 1;
+        } else {
+          const uint2 sg = seg_lookup(p.X, __ldg(s_in.col[p.xk] + r));
+          aux = sg.x;
+          len = sg.y;
+          if (len) {
+            atomicAdd(s_acc + 2 * p.xslot, (unsigned long long)len);
+            atomicAdd(s_acc + 2 * p.xslot + 1, (unsigned long long)len);
+          }
+          if (len >= WARP_ROW) {
+            warp_row = true;  // counted (if filtered) and emitted by a warp
+            cnt = p.npost ? 0u : len;
+          } else if (p.npost == 0) {
+            cnt = len;
+          } else {
+            for (u32 j = 0; j < len; j++) cnt += gpost(p, s_in, r, __ldg(p.X.dst + aux + j), s_acc);
+          }
+        }
+      }
+    }
+    s_aux[tid] = aux;
+    s_len[tid] = len;
+    s_pre[tid] = cnt;
+    if (warp_row) s_long[atomicAdd(&s_nlong, 1)] = tid;
+    __syncthreads();
+    if (p.npost) {  // warp-cooperative counting of long candidate lists
+      for (int q = warp; q < s_nlong; q += TS_THREADS / 32) {
+        const int rl = s_long[q];
+        const u32 L = s_len[rl], ax = s_aux[rl];
+        u32 c = 0;
+        for (u32 j = lane; j < L; j += 32) c += gpost(p, s_in, base + rl, __ldg(p.X.dst + ax + j), s_acc);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) s_pre[rl] = c;
+      }
+      __syncthreads();
+    }
+    // ---- block scan of the per-row survivor counts + look-back
+    const i64 mine_cnt = s_pre[tid];
+    i64 x = mine_cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const i64 y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    i64 run = x - mine_cnt;
+    for (int w = 0; w < warp; w++) run += s_wsum[w];
+    s_pre[tid] = run;
+    if (tid == TS_THREADS - 1) s_pre[TS_TILE] = run + mine_cnt;
+    __syncthreads();
+    const i64 total = s_pre[TS_TILE];
+    if (warp == 0) {
+      const i64 b = lookback_warp(ts, t, total);
+      if (lane == 0) s_base = b;
+    }
+    __syncthreads();
+    const i64 gbase = s_base;
+    // ---- emit: short rows by their thread, long rows by a warp
+    if (!warp_row && mine_cnt > 0) {
+      i64 pos = gbase + s_pre[tid];
+      if (!p.has_x) {
+        gwrite(p, s_in, r, 0u, pos);
+      } else {
+        for (u32 j = 0; j < len; j++) {
+          const u32 cand = __ldg(p.X.dst + aux + j);
+          if (p.npost == 0 || gpost(p, s_in, r, cand, nullptr)) gwrite(p, s_in, r, cand, pos++);
+        }
+      }
+    }
+    for (int q = warp; q < s_nlong; q += TS_THREADS / 32) {
+      const int rl = s_long[q];
+      const u32 L = s_len[rl], ax = s_aux[rl];
+      i64 pos = gbase + s_pre[rl];
+      for (u32 j0 = 0; j0 < L; j0 += 32) {
+        const u32 j = j0 + lane;
+        u32 cand = 0;
+        bool ok = false;
+        if (j < L) {
+          cand = __ldg(p.X.dst + ax + j);
+          ok = p.npost == 0 || gpost(p, s_in, base + rl, cand, nullptr);
+        }
+        const u32 m = __ballot_sync(0xffffffffu, ok);
+        if (ok) gwrite(p, s_in, base + rl, cand, pos + __popc(m & ((1u << lane) - 1u)));
+        pos += __popc(m);
+      }
+    }
+    if ((i64)t == ntiles - 1 && tid == 0) {
+      const i64 tot = gbase + total;
+      p.O->n = tot < p.cap ? tot : p.cap;
+      p.st[p.last_slot]->overflow = !p.fz.stage && tot > p.cap;
+      if (p.fz.stage) p.fz.finish(tot);
+    }
+    __syncthreads();
+  }
+  // ---- publish this block's step counters
+  __syncthreads();
+  if (tid < p.nslots) {
+    const unsigned long long e = s_acc[2 * tid], rw = s_acc[2 * tid + 1];
+    if (e) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st[tid]->e), e);
+    if (rw) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st[tid]->rows), rw);
+  }
+}
+
 // DISTINCT over packed row-major rows: a row survives iff it wins the CAS
 // into an open-addressing set keyed by the whole tuple (executor.py:360-367).
 struct DistinctP {
@@ -551,7 +785,7 @@ struct QueryBlock {
 
 enum Home { H_NONE = 0, H_STORE = 1, H_A = 2, H_B = 3 };
 
-enum StepKind { S_SCAN = 0, S_EMPTY, S_EXPAND, S_FILTER, S_CROSS, S_GATE };
+enum StepKind { S_SCAN = 0, S_EMPTY, S_EXPAND, S_FILTER, S_CROSS, S_GATE, S_GROUP };
 
 struct StepPlan {
   StepKind kind;
@@ -587,6 +821,7 @@ struct gsm_context {
   u64 gen = 0;             // bumped by every gsm_execute (staged results expire)
   bool use_graphs = true;  // replay each distinct query's launch sequence as a CUDA graph
   bool use_pdl = true;     // programmatic dependent launch between plan steps
+  bool use_fusion = true;  // fuse [filters][expand][filters] step groups into one kernel
   struct GraphEntry {
     cudaGraphExec_t exec;
     int kernels;
@@ -777,6 +1012,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   c->device = store->device;
   if (const char* ng = getenv("GSM_NO_GRAPHS")) c->use_graphs = !(ng[0] == '1');
   if (const char* np = getenv("GSM_NO_PDL")) c->use_pdl = !(np[0] == '1');
+  if (const char* nf = getenv("GSM_NO_FUSION")) c->use_fusion = !(nf[0] == '1');
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
     return st;
@@ -908,10 +1144,20 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     int step, left, right, out;
     ExpandP ep;
     FilterP fp;
+    GroupP gp;
     int a, b;
     int grid;
+    int last_step;  // S_GROUP: the last fused step
   };
   std::vector<Launch> launches;
+  // Step fusion state: a group is [filters][expand][filters] over one input
+  // table; every fused step writes (if at all) to the buffer opposite the
+  // group's input, so the group's final table never aliases its input.
+  bool g_open = false, g_has_x = false;
+  int g_npre = 0, g_npost = 0;
+  Home g_in_home = H_NONE;
+  std::vector<int> group_id(n, -1);
+  int n_groups = 0;
   for (int s = 1; s < n; s++) {
     const gsm_pattern& p = steps[s];
     std::vector<int> rs = pattern_schema(p);
@@ -932,6 +1178,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     if ((int)out_schema.size() > GSM_MAX_VARS)
       return set_error(GSM_ERR_VALUE, "query binds more than " + std::to_string(GSM_MAX_VARS) + " variables");
     const int a = (int)schema.size();
+    if (!m || jv.empty()) g_open = false;  // empty / cross / gate steps end a fusion group
     if (!m) {
       // R6 right side: the join (or cross product) is empty, E = 0.
       L.kind = S_EMPTY;
@@ -949,9 +1196,27 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
         L.b = (int)rs.size();
       }
     } else {
-      Home oh = Exec::other(ex.home[cur]);
       bool sv = p.s_var >= 0, ov = p.o_var >= 0;
-      if (sv && ov && p.s_var != p.o_var && jv.size() == 1) {
+      const bool is_expand = sv && ov && p.s_var != p.o_var && jv.size() == 1;
+      // join the open group when the [F*][E][F*] shape allows it
+      bool join = false;
+      if (c->use_fusion && g_open) {
+        if (is_expand) join = !g_has_x;
+        else join = g_has_x ? g_npost < MAXF : g_npre < MAXF;
+      }
+      if (!join) {
+        g_open = true;
+        g_has_x = false;
+        g_npre = g_npost = 0;
+        g_in_home = ex.home[cur];
+        n_groups++;
+      }
+      if (is_expand) g_has_x = true;
+      else if (g_has_x) g_npost++;
+      else g_npre++;
+      group_id[s] = n_groups - 1;
+      const Home oh = Exec::other(g_in_home);
+      if (is_expand) {
         L.kind = S_EXPAND;
         L.out = ex.new_table((int)out_schema.size(), oh);
         ExpandP& e = L.ep;
@@ -1020,6 +1285,60 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     cur = L.out;
   }
 
+  // ---- fuse each multi-step group into one k_group launch ----
+  if (c->use_fusion) {
+    std::vector<Launch> fl;
+    size_t i = 0;
+    while (i < launches.size()) {
+      const int gid = group_id[launches[i].step];
+      size_t j = i + 1;
+      if (gid >= 0)
+        while (j < launches.size() && group_id[launches[j].step] == gid) j++;
+      if (gid < 0 || j - i == 1) {
+        fl.push_back(launches[i]);
+        i = j;
+        continue;
+      }
+      Launch G{};
+      G.kind = S_GROUP;
+      G.step = launches[i].step;
+      G.last_step = launches[j - 1].step;
+      G.left = launches[i].left;
+      G.out = launches[j - 1].out;
+      G.grid = launches[i].grid;
+      GroupP& gp = G.gp;
+      gp.L = dT + G.left;
+      gp.a = ex.arity[G.left];
+      std::vector<FSpec> pre, post;
+      for (size_t k = i; k < j; k++) {
+        const Launch& L = launches[k];
+        const int slot = gp.nslots++;
+        gp.st[slot] = dS + L.step;
+        if (L.kind == S_EXPAND) {
+          gp.has_x = 1;
+          gp.X = L.ep.R;
+          gp.xk = L.ep.li;
+          gp.xslot = slot;
+        } else {
+          FSpec fs{L.fp.R, L.fp.mode, L.fp.li, L.fp.lj, L.fp.cval, slot};
+          (gp.has_x ? post : pre).push_back(fs);
+        }
+      }
+      gp.npre = (int)pre.size();
+      gp.npost = (int)post.size();
+      for (int q = 0; q < gp.npre; q++) gp.f[q] = pre[q];
+      for (int q = 0; q < gp.npost; q++) gp.f[gp.npre + q] = post[q];
+      gp.last_slot = gp.nslots - 1;
+      const Launch& last = launches[j - 1];
+      gp.out = last.kind == S_EXPAND ? last.ep.out : last.fp.out;
+      gp.cap = last.kind == S_EXPAND ? last.ep.cap : last.fp.cap;
+      gp.O = dT + G.out;
+      fl.push_back(G);
+      i = j;
+    }
+    launches.swap(fl);
+  }
+
   // ---- projection target ----
   int pj_idx[GSM_MAX_VARS];
   if (n_proj > GSM_MAX_VARS) return set_error(GSM_ERR_VALUE, "too many projected variables");
@@ -1036,7 +1355,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // the result goes to the host staging buffer (no DISTINCT).
   bool fused = false;
   if (allow_fuse && !distinct && !launches.empty() &&
-      (launches.back().kind == S_EXPAND || launches.back().kind == S_FILTER)) {
+      (launches.back().kind == S_EXPAND || launches.back().kind == S_FILTER ||
+       launches.back().kind == S_GROUP)) {
     FusedOut fz;
     fz.stage = c->d_stage;
     fz.cap = stage_cap;
@@ -1044,7 +1364,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     for (int j = 0; j < n_proj; j++) fz.pj[j] = pj_idx[j];
     fz.pst = dS + pack_stat;
     if (launches.back().kind == S_EXPAND) launches.back().ep.fz = fz;
-    else launches.back().fp.fz = fz;
+    else if (launches.back().kind == S_FILTER) launches.back().fp.fz = fz;
+    else launches.back().gp.fz = fz;
     fused = true;
   }
   S.fused = fused;
@@ -1054,7 +1375,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   {
     int slot = 0;
     for (auto& L : launches)
-      if (L.kind == S_EXPAND || L.kind == S_FILTER) hb->epochs[slot++] = next_epoch(c);
+      if (L.kind == S_EXPAND || L.kind == S_FILTER || L.kind == S_GROUP)
+        hb->epochs[slot++] = next_epoch(c);
   }
   ProjArgs pa{};
   for (int j = 0; j < n_proj; j++) pa.col[j] = pj_idx[j];
@@ -1098,6 +1420,13 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           nk++;
           break;
         }
+        case S_GROUP: {
+          TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
+          slot++;
+          GSM_CUDA(launch(c->use_pdl, k_group, L.grid, TS_THREADS, st, L.gp, ts));
+          nk++;
+          break;
+        }
         case S_CROSS: {
           Home oh = ex.home[L.out];
           GSM_CUDA(launch(c->use_pdl, k_cross, L.grid, 256, st, (const DTable*)(dT + L.left),
@@ -1115,7 +1444,11 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
         default:
           break;
       }
-      if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev[L.step + 1], st, cudaEventRecordExternal));
+      if (timing) {
+        const int last = L.kind == S_GROUP ? L.last_step : L.step;
+        for (int q = L.step; q <= last; q++)  // fused steps: the group's time is on its first step
+          GSM_CUDA(cudaEventRecordWithFlags(c->ev[q + 1], st, cudaEventRecordExternal));
+      }
     }
     if (!fused) {
       // DISTINCT reads the packed rows on the device, so only plain

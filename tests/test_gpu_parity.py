@@ -184,38 +184,55 @@ def test_reference_objects_drop_in():
         g.execute(q, plan, st, row_budget=0)
 
 
-def test_graph_replay_matches_fresh_launches(store_factory, tmp_path):
-    """Each query is captured once as a CUDA graph and replayed afterwards;
-    replays and the graph-free launch path (GSM_NO_GRAPHS=1) agree."""
+def test_execution_variants_agree(store_factory):
+    """Graph replay, programmatic dependent launch and step fusion are pure
+    optimisations: each query gives the same bag and the same per-step report
+    with every combination switched off (GSM_NO_GRAPHS / GSM_NO_PDL /
+    GSM_NO_FUSION), and repeated (replayed) executions agree."""
     import json
+    import os
     import subprocess
     import sys
 
     d = store_factory("lubm", univ=2, seed=4)
-    store = g.load(d)
-    fps = {}
-    for name, text in lubm_queries():
-        q, plan = _plan(store, text)
-        runs = [orc.fingerprint_array(g.execute(q, plan, store).array) for _ in range(3)]
-        assert runs[0] == runs[1] == runs[2], name
-        fps[name] = [str(v) for v in runs[0]]
+    texts = [t for _, t in lubm_queries()] + [
+        (GOLDEN.parents[1] / "datagen/queries/lubm_complex" / f).read_text()
+        for f in sorted(os.listdir(GOLDEN.parents[1] / "datagen/queries/lubm_complex"))]
     script = (
         "import json, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
         "import paper_1807_07691_b200 as g\n"
         "from oracle import oracle as orc\n"
-        "from conftest import lubm_queries\n"
         "st = g.load(%r)\n"
-        "out = {}\n"
-        "for name, text in lubm_queries():\n"
+        "out = []\n"
+        "for text in json.loads(sys.stdin.read()):\n"
         "    q = g.bind_constants(g.parse_query(text), st.dictionary)\n"
         "    p = g.make_plan(q, st.stats)\n"
-        "    out[name] = [str(v) for v in orc.fingerprint_array(g.execute(q, p, st).array)]\n"
+        "    runs = []\n"
+        "    for _ in range(2):\n"
+        "        rep = g.ExecutionReport()\n"
+        "        r = g.execute(q, p, st, report=rep, row_budget=1 << 62)\n"
+        "        runs.append([[str(v) for v in orc.fingerprint_array(r.array)],\n"
+        "                     [s.rows for s in rep.steps], [s.prealloc_total for s in rep.steps]])\n"
+        "    assert runs[0] == runs[1]\n"
+        "    out.append(runs[0])\n"
         "print(json.dumps(out))\n" % (str(GOLDEN.parents[1]), str(GOLDEN.parent), str(d))
     )
-    env = dict(__import__("os").environ, GSM_NO_GRAPHS="1")
-    out = subprocess.run([sys.executable, "-c", script], env=env, check=True, capture_output=True,
-                         text=True).stdout
-    assert json.loads(out.strip().splitlines()[-1]) == fps
+    results = {}
+    for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION",
+                    "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION"):
+        env = dict(os.environ)
+        for k in filter(None, variant.split(",")):
+            env[k] = "1"
+        out = subprocess.run([sys.executable, "-c", script], input=json.dumps(texts), env=env,
+                             check=True, capture_output=True, text=True).stdout
+        results[variant] = json.loads(out.strip().splitlines()[-1])
+    base = results[""]
+    for variant, res in results.items():
+        assert res == base, variant
+    # and the default path against the oracle
+    store = g.load(d)
+    for text in texts:
+        _oracle_compare(store, text, row_budget=1 << 62)
 
 
 def test_execute_batch_matches_sequential(store_factory):
