@@ -1,6 +1,8 @@
 #!/usr/bin/env python
-"""Scale run (BASELINE.json configs[2]: LUBM-style U=1000, ~130M triples,
-complex cyclic / snowflake queries on 1 B200) with parity and a CPU baseline.
+"""Scale runs with parity and a CPU baseline: BASELINE.json configs[2]
+(LUBM-style U=1000, ~130M triples, complex cyclic / snowflake queries on
+1 B200) and the configs[4] power-law model (generate.py, hub-heavy chain
+joins) at single-GPU scale (--kind powerlaw --triples N).
 
 For every query of datagen/queries/lubm and datagen/queries/lubm_complex:
   * GPU: warm-up, then median device latency (CUDA events) over --reps runs,
@@ -15,6 +17,7 @@ For every query of datagen/queries/lubm and datagen/queries/lubm_complex:
 Row budget is 2^62 in both engines.  One JSON line per query,
 then a summary line.  Usage:
     python tools/scale_run.py --univ 1000 [--reps 5] [--skip-oracle-above 400000000]
+    python tools/scale_run.py --kind powerlaw --triples 200000000 --predicates 40
 """
 from __future__ import annotations
 
@@ -34,12 +37,15 @@ sys.path.insert(0, str(REPO))
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--kind", choices=["lubm", "powerlaw"], default="lubm")
     ap.add_argument("--univ", type=int, default=1000)
+    ap.add_argument("--triples", type=int, default=100_000_000)
+    ap.add_argument("--predicates", type=int, default=40)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--exact-rows", type=int, default=20_000_000)
     ap.add_argument("--skip-oracle-above", type=int, default=400_000_000,
-                    help="skip the oracle when a step's E exceeds this (host RAM guard)")
+                    help="skip the oracle when a step materialises more rows (host RAM guard)")
     ap.add_argument("--store", default=None, help="reuse an existing store directory")
     args = ap.parse_args()
 
@@ -50,12 +56,16 @@ def main():
 
     subprocess.run(["make", "-s", "-C", str(REPO / "oracle")], check=True)
     tmp = tempfile.mkdtemp(prefix="gsm_scale_")
-    store_dir = args.store or f"{tmp}/lubm{args.univ}"
+    store_dir = args.store or f"{tmp}/{args.kind}"
     t0 = time.perf_counter()
     if not args.store:
-        subprocess.run([str(REPO / "oracle/_build/gsmgen"), "lubm", "--univ", str(args.univ),
-                        "--seed", str(args.seed), "--out", store_dir], check=True,
-                       stdout=subprocess.DEVNULL)
+        gen = [str(REPO / "oracle/_build/gsmgen"), args.kind, "--seed", str(args.seed),
+               "--out", store_dir]
+        if args.kind == "lubm":
+            gen += ["--univ", str(args.univ)]
+        else:  # generate.py's model (Zipf predicates, i^-0.5 endpoints, nodes = triples/4)
+            gen += ["--triples", str(args.triples), "--predicates", str(args.predicates)]
+        subprocess.run(gen, check=True, stdout=subprocess.DEVNULL)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     store = g.load(store_dir)
@@ -65,8 +75,11 @@ def main():
                       "load_s": round(t_load, 2), "device_bytes": store.device_bytes()}),
           flush=True)
     prep = orc.PreparedStore(store.matrices)
-    qfiles = sorted((REPO / "datagen/queries/lubm").glob("*.rq")) + \
-        sorted((REPO / "datagen/queries/lubm_complex").glob("*.rq"))
+    if args.kind == "lubm":
+        qfiles = sorted((REPO / "datagen/queries/lubm").glob("*.rq")) + \
+            sorted((REPO / "datagen/queries/lubm_complex").glob("*.rq"))
+    else:
+        qfiles = sorted((REPO / "datagen/queries/powerlaw").glob("*.rq"))
     summary = {"gpu_ms": 0.0, "cpu_s": 0.0, "join_rows": 0, "parity_ok": 0, "parity_checked": 0}
     for qf in qfiles:
         q = g.bind_constants(g.parse_query(qf.read_text()), store.dictionary)
@@ -84,8 +97,7 @@ def main():
                "gpu_ms": round(1e3 * statistics.median(dev), 3),
                "join_rows": sum(s.rows for s in rep.steps[1:])}
         rec["join_rows_per_s"] = round(rec["join_rows"] / statistics.median(dev), 1)
-        if max(rec["step_prealloc"] + [0]) <= args.skip_oracle_above and \
-                max(rec["step_rows"]) <= args.skip_oracle_above:
+        if max(rec["step_rows"]) <= args.skip_oracle_above:
             t0 = time.perf_counter()
             rows, srows, spre = orc.run(prep, [s.pattern for s in plan.steps], q.projection,
                                         q.distinct, budget=budget)
