@@ -352,6 +352,7 @@ struct FilterP {
 // positions of surviving candidates dense and ordered).
 // ---------------------------------------------------------------------------
 constexpr int MAXF = 8;              // filters on each side of the expand
+constexpr u32 FUSE_MAX_FANOUT = 4;   // post-expand filters fuse only below this fan-out
 constexpr int MAXGS = 2 * MAXF + 1;  // steps in a group
 
 struct FSpec {
@@ -1155,6 +1156,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // group's input, so the group's final table never aliases its input.
   bool g_open = false, g_has_x = false;
   int g_npre = 0, g_npost = 0;
+  u32 g_x_fanout = 0;  // longest candidate list of the group's expand
   Home g_in_home = H_NONE;
   std::vector<int> group_id(n, -1);
   int n_groups = 0;
@@ -1199,10 +1201,14 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       bool sv = p.s_var >= 0, ov = p.o_var >= 0;
       const bool is_expand = sv && ov && p.s_var != p.o_var && jv.size() == 1;
       // join the open group when the [F*][E][F*] shape allows it
+      // Filters after the expand run per candidate inside the row's thread,
+      // so they are fused only when every candidate list is short (a large
+      // fan-out is better spread over blocks by materialising the expand).
       bool join = false;
       if (c->use_fusion && g_open) {
         if (is_expand) join = !g_has_x;
-        else join = g_has_x ? g_npost < MAXF : g_npre < MAXF;
+        else if (g_has_x) join = g_npost < MAXF && g_x_fanout <= FUSE_MAX_FANOUT;
+        else join = g_npre < MAXF;
       }
       if (!join) {
         g_open = true;
@@ -1211,8 +1217,11 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
         g_in_home = ex.home[cur];
         n_groups++;
       }
-      if (is_expand) g_has_x = true;
-      else if (g_has_x) g_npost++;
+      if (is_expand) {
+        g_has_x = true;
+        const bool on_s = jv[0] == p.s_var;
+        g_x_fanout = (on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid]).max_run;
+      } else if (g_has_x) g_npost++;
       else g_npre++;
       group_id[s] = n_groups - 1;
       const Home oh = Exec::other(g_in_home);

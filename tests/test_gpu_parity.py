@@ -223,9 +223,10 @@ def test_execution_variants_agree(store_factory):
         env = dict(os.environ)
         for k in filter(None, variant.split(",")):
             env[k] = "1"
-        out = subprocess.run([sys.executable, "-c", script], input=json.dumps(texts), env=env,
-                             check=True, capture_output=True, text=True).stdout
-        results[variant] = json.loads(out.strip().splitlines()[-1])
+        proc = subprocess.run([sys.executable, "-c", script], input=json.dumps(texts), env=env,
+                              capture_output=True, text=True)
+        assert proc.returncode == 0, (variant, proc.stderr[-3000:])
+        results[variant] = json.loads(proc.stdout.strip().splitlines()[-1])
     base = results[""]
     for variant, res in results.items():
         assert res == base, variant
