@@ -385,22 +385,23 @@ __device__ __forceinline__ u32 vcol(const DTable& s, int a, int c, i64 r, u32 ca
   return c < a ? __ldg(s.col[c] + r) : cand;
 }
 
-// Evaluate filter f on virtual row (r, cand); accumulate E / rows when acc.
+// Evaluate filter f on virtual row (r, cand); accumulate E / rows into the
+// calling thread's private counters when acc (reduced once per kernel).
 __device__ __forceinline__ bool gfilter(const FSpec& f, const DTable& s, int a, i64 r, u32 cand,
-                                        unsigned long long* acc) {
+                                        i64* acc) {
   const u32 key = vcol(s, a, f.kc, r, cand);
   const uint2 sg = seg_lookup(f.R, key);
   const u32 target = f.mode == F_PAIR ? vcol(s, a, f.tc, r, cand) : f.mode == F_CONST ? f.cval : key;
   const bool keep = sg.y && sorted_contains(f.R.dst + sg.x, sg.y, target);
   if (acc) {
-    atomicAdd(acc + 2 * f.slot, (unsigned long long)(f.mode == F_PAIR ? sg.y : (u32)keep));
-    if (keep) atomicAdd(acc + 2 * f.slot + 1, 1ull);
+    acc[2 * f.slot] += f.mode == F_PAIR ? (i64)sg.y : (i64)keep;
+    acc[2 * f.slot + 1] += keep;
   }
   return keep;
 }
 
 __device__ __forceinline__ bool gpost(const GroupP& p, const DTable& s, i64 r, u32 cand,
-                                      unsigned long long* acc) {
+                                      i64* acc) {
   for (int i = p.npre; i < p.npre + p.npost; i++)
     if (!gfilter(p.f[i], s, p.a, r, cand, acc)) return false;
   return true;
@@ -427,9 +428,11 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
   __shared__ u32 s_tile;
   __shared__ int s_long[TS_TILE];
   __shared__ int s_nlong;
-  __shared__ unsigned long long s_acc[2 * MAXGS];
   __shared__ DTable s_in;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  i64 acc[2 * MAXGS];  // this thread's (E, rows) contribution to each fused step
+  for (int k = 0; k < 2 * MAXGS; k++) acc[k] = 0;
+  i64* const s_acc = acc;
 
   pdl_wait();
   pdl_trigger();
@@ -438,7 +441,6 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
     s_tile = atomicAdd(ts.counter, 1u);
     s_nlong = 0;
   }
-  if (tid < 2 * MAXGS) s_acc[tid] = 0;
   copy_desc(s_in, p.L, p.a);
   __syncthreads();
   const i64 n = s_in.n;
@@ -476,10 +478,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
           const uint2 sg = seg_lookup(p.X, __ldg(s_in.col[p.xk] + r));
           aux = sg.x;
           len = sg.y;
-          if (len) {
-            atomicAdd(s_acc + 2 * p.xslot, (unsigned long long)len);
-            atomicAdd(s_acc + 2 * p.xslot + 1, (unsigned long long)len);
-          }
+          acc[2 * p.xslot] += len;
+          acc[2 * p.xslot + 1] += len;
           if (len >= WARP_ROW) {
             warp_row = true;  // counted (if filtered) and emitted by a warp
             cnt = p.npost ? 0u : len;
@@ -567,12 +567,18 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
     }
     __syncthreads();
   }
-  // ---- publish this block's step counters
-  __syncthreads();
-  if (tid < p.nslots) {
-    const unsigned long long e = s_acc[2 * tid], rw = s_acc[2 * tid + 1];
-    if (e) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st[tid]->e), e);
-    if (rw) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st[tid]->rows), rw);
+  // ---- publish the step counters: warp sums, one global atomic per warp
+  for (int k = 0; k < p.nslots; k++) {
+    i64 e = acc[2 * k], rw = acc[2 * k + 1];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      e += __shfl_xor_sync(0xffffffffu, e, o);
+      rw += __shfl_xor_sync(0xffffffffu, rw, o);
+    }
+    if (lane == 0) {
+      if (e) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st[k]->e), (unsigned long long)e);
+      if (rw) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st[k]->rows), (unsigned long long)rw);
+    }
   }
 }
 
@@ -1395,11 +1401,18 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
 
   // The whole query as one stream-ordered sequence: H2D of the query block,
   // the kernels, D2H of the step counters.  Nothing here writes host memory.
+  bool capturing = false;
+  // Under stream capture an event record must be an external node to be
+  // timeable; outside capture the flag is illegal.
+  auto record = [&](cudaEvent_t ev) -> cudaError_t {
+    return capturing ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                     : cudaEventRecord(ev, st);
+  };
   auto issue = [&]() -> gsm_status {
     int nk = 0;
-    if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev_q0, st, cudaEventRecordExternal));
+    if (timing) GSM_CUDA(record(c->ev_q0));
     GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
-    if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev[0], st, cudaEventRecordExternal));
+    if (timing) GSM_CUDA(record(c->ev[0]));
     if (ex.res.njobs > 0) {
       GSM_CUDA(launch(c->use_pdl, k_resolve, 1, 64, st, ex.res, dT, dS));
       nk++;
@@ -1409,7 +1422,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
                       (int)ex.plan[0].schema.size(), part, parts, dS + 0));
       nk++;
     }
-    if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev[1], st, cudaEventRecordExternal));
+    if (timing) GSM_CUDA(record(c->ev[1]));
     int slot = 0;
     for (auto& L : launches) {
       switch (L.kind) {
@@ -1456,7 +1469,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       if (timing) {
         const int last = L.kind == S_GROUP ? L.last_step : L.step;
         for (int q = L.step; q <= last; q++)  // fused steps: the group's time is on its first step
-          GSM_CUDA(cudaEventRecordWithFlags(c->ev[q + 1], st, cudaEventRecordExternal));
+          GSM_CUDA(record(c->ev[q + 1]));
       }
     }
     if (!fused) {
@@ -1468,7 +1481,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
                       stage_cap, dS + pack_stat));
       nk++;
     }
-    if (timing) GSM_CUDA(cudaEventRecordWithFlags(c->ev_q1, st, cudaEventRecordExternal));
+    if (timing) GSM_CUDA(record(c->ev_q1));
     GSM_CUDA(cudaGetLastError());
     GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(StepStat) * (size_t)(n + 1),
                              cudaMemcpyDeviceToHost, st));
@@ -1511,7 +1524,9 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     } else {
       if (c->graphs.size() >= 1024) ctx_clear_graphs(c);
       GSM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
       gsm_status is = issue();
+      capturing = false;
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(st, &g);
       if (is != GSM_OK) {
