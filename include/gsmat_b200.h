@@ -169,6 +169,25 @@ typedef struct {
 gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
                              gsm_status* statuses, gsm_result** outs, float* device_ms);
 
+/* Replaces executor.sm_join / parallel_sm_join / cross_product
+ * (executor.py:155-280) on arbitrary binding tables (not store-backed):
+ * `left` is n_left x a and `right` n_right x b row-major uint32 host arrays.
+ * join_left[i] / join_right[i] are the columns of the i-th shared variable
+ * in each table, in LEFT-schema order (executor.py:343); the first drives the
+ * match, the others are equality checks (executor.py:140-152, 186-191);
+ * n_join = 0 is the cross product.  Result rows: left row ++ the right
+ * columns not in join_right, in right order (executor.py:146-148), in the
+ * reference's sm_join order (left rows in order, candidates in right-table
+ * order).  prealloc_total (may be NULL) receives E, the first-variable match
+ * total (executor.py:197-215); row_counts (may be NULL, n_left entries)
+ * receives each left row's first-variable match count N.  Budget rules and
+ * messages as gsm_execute (cross product: |L|*|R|). */
+gsm_status gsm_table_join(gsm_context* ctx, const uint32_t* left, int64_t n_left, int32_t a,
+                          const uint32_t* right, int64_t n_right, int32_t b,
+                          const int32_t* join_left, const int32_t* join_right, int32_t n_join,
+                          int64_t row_budget, int32_t budget_mode, int64_t* prealloc_total,
+                          int64_t* row_counts, gsm_result** out);
+
 /* ---- results ---------------------------------------------------------- */
 
 /* Shape of the projected result: n_rows x n_cols (BindingTable.rows). */

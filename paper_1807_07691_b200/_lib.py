@@ -40,6 +40,7 @@ EXPORTS = (
     "gsm_context_free",
     "gsm_execute",
     "gsm_execute_batch",
+    "gsm_table_join",
     "gsm_result_shape",
     "gsm_result_copy",
     "gsm_result_device_ptr",
@@ -131,6 +132,10 @@ def lib() -> C.CDLL:
                 [vp, P(Pattern), i32, P(i32), i32, i32, i64, i32, i64, i64, P(Report), P(vp)],
             ),
             "gsm_execute_batch": (i32, [P(vp), i32, P(Query), P(i32), P(vp), P(C.c_float)]),
+            "gsm_table_join": (
+                i32,
+                [vp, vp, i64, i32, vp, i64, i32, P(i32), P(i32), i32, i64, i32, P(i64), vp, P(vp)],
+            ),
             "gsm_result_shape": (i32, [vp, P(i64), P(i32)]),
             "gsm_result_copy": (i32, [vp, vp]),
             "gsm_result_device_ptr": (i32, [vp, P(C.c_uint64)]),

@@ -34,6 +34,7 @@ struct Orient {
   u32 nnz = 0;
   u32 nrows = 0;
   u32 maxkey = 0;  // dense index covers keys 0..maxkey
+  u32 kbias = 0;   // hash keys are stored as key + kbias (1 for table joins, where 0 is a legal id)
 };
 
 struct PredDev {
@@ -76,6 +77,7 @@ __device__ __forceinline__ uint2 seg_lookup(const Orient& R, u32 key) {
     return make_uint2(b, e - b);
   }
   if (R.hs) {
+    key += R.kbias;
     u32 h = hash32(key) & R.hmask;
     for (;;) {
       uint4 s = __ldg(R.hs + h);

@@ -27,6 +27,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "gsm_internal.cuh"
 
 namespace gsm {
@@ -745,6 +747,112 @@ __global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* dev_out, i64 de
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride)
     for (int c = 0; c < k; c++) out[r * k + c] = __ldg(T->col[pj.col[c]] + r);
+}
+
+// ---------------------------------------------------------------------------
+// Table-level joins (gsm_table_join): sm_join / parallel_sm_join /
+// cross_product on arbitrary binding tables.
+// ---------------------------------------------------------------------------
+// Row-major host rows -> struct-of-arrays columns (column stride = n).
+__global__ void k_rows_to_cols(const u32* __restrict__ rm, i64 n, int a, u32* __restrict__ cols) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n * a; i += stride) {
+    const i64 r = i / a, c = i - r * a;
+    cols[c * n + r] = rm[i];
+  }
+}
+
+// Sort input of the right table's index: (key = first join column, row).
+__global__ void k_key_rows(const u32* __restrict__ R, i64 n, int b, int jc, u32* __restrict__ keys,
+                           u32* __restrict__ rows) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    keys[i] = R[i * b + jc];
+    rows[i] = (u32)i;
+  }
+}
+
+// Hash index over the runs of a sorted key array, keys stored as key + 1 so
+// that 0 stays the empty-slot marker (table ids may be 0).
+__global__ void k_hash_runs(const u32* __restrict__ keys, u32 n, u32* __restrict__ slots, u32 mask) {
+  const u32 stride = gridDim.x * blockDim.x;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 key = keys[i];
+    if (i != 0 && keys[i - 1] == key) continue;
+    u32 lo = i, hi = n;  // end of the run
+    while (lo < hi) {
+      const u32 mid = (lo + hi) >> 1;
+      if (keys[mid] <= key) lo = mid + 1; else hi = mid;
+    }
+    const u32 stored = key + 1u;
+    u32 h = hash32(stored) & mask;
+    for (;;) {
+      const u32 prev = atomicCAS(slots + 4 * h, 0u, stored);
+      if (prev == 0u) {
+        slots[4 * h + 1] = i;
+        slots[4 * h + 2] = lo - i;
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+// N_i of every left row (preallocate, executor.py:197-215) and E = sum N_i.
+__global__ void k_row_counts(const u32* __restrict__ Lk, i64 n, Orient X, i64* __restrict__ cnt,
+                             unsigned long long* __restrict__ total) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  unsigned long long acc = 0;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 c = seg_lookup(X, Lk[i]).y;
+    cnt[i] = c;
+    acc += c;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, acc);
+}
+
+// Secondary join variables + output gather of the expanded (left ++ right row
+// index) table: keep a candidate iff every further shared variable agrees
+// (executor.py:186-191); emit left ++ right[rcols] row-major.
+struct TFilterP {
+  static constexpr bool kAccumE = false;
+  const DTable* L;  // a left columns + the right row index at column a
+  int a;
+  const u32* R;     // right rows, row-major n_right x b
+  int b, nsec, nrc;
+  int jl[GSM_MAX_VARS], jr[GSM_MAX_VARS], rc[GSM_MAX_VARS];
+  u32* out;
+  StepStat* st;
+  __device__ void prepare(DTable& s) const { copy_desc(s, L, a + 1); }
+  __device__ i64 rows(const DTable& s) const { return s.n; }
+  __device__ u32 count(const DTable& s, i64 r, u32& aux, i64&) const {
+    const u32 ri = __ldg(s.col[a] + r);
+    aux = ri;
+    for (int i = 0; i < nsec; i++)
+      if (__ldg(s.col[jl[i]] + r) != __ldg(R + (i64)ri * b + jr[i])) return 0u;
+    return 1u;
+  }
+  __device__ void emit(const DTable& s, i64 r, u32 aux, i64, i64 g) const {
+    const int w = a + nrc;
+    u32* o = out + g * w;
+    for (int c = 0; c < a; c++) o[c] = __ldg(s.col[c] + r);
+    for (int k = 0; k < nrc; k++) o[a + k] = __ldg(R + (i64)aux * b + rc[k]);
+  }
+  __device__ void finish(i64 total) const { st->rows = total; }
+};
+
+// Row-major cross product: row g = L[g / nR] ++ R[g % nR] (executor.py:164).
+__global__ void k_cross_rows(const u32* __restrict__ L, i64 nl, int a, const u32* __restrict__ R,
+                             i64 nr, int b, u32* __restrict__ out) {
+  const i64 total = nl * nr, stride = (i64)gridDim.x * blockDim.x;
+  const int w = a + b;
+  for (i64 g = (i64)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += stride) {
+    const i64 i = g / nr, j = g - i * nr;
+    for (int c = 0; c < a; c++) out[g * w + c] = L[i * a + c];
+    for (int c = 0; c < b; c++) out[g * w + a + c] = R[j * b + c];
+  }
 }
 
 }  // namespace gsm
@@ -1860,6 +1968,237 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
   }
   if (first != GSM_OK) set_error(first, first_msg);
   return first;
+}
+
+
+// ---------------------------------------------------------------------------
+// gsm_table_join
+// ---------------------------------------------------------------------------
+namespace {
+struct TableJoinScratch {
+  DTable L, X;
+  StepStat st[2];
+  u32 counters[2];
+  u32 epochs[2];
+};
+}  // namespace
+
+gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, int32_t a,
+                          const uint32_t* right, int64_t n_right, int32_t b,
+                          const int32_t* join_left, const int32_t* join_right, int32_t n_join,
+                          int64_t budget, int32_t budget_mode, int64_t* prealloc_total,
+                          int64_t* row_counts, gsm_result** out) {
+  *out = nullptr;
+  if (!c) return set_error(GSM_ERR_VALUE, "null context");
+  if (n_left < 0 || n_right < 0 || a < 0 || b < 0 || n_join < 0 || n_join > a || n_join > b ||
+      a + b - n_join > GSM_MAX_VARS || a >= GSM_MAX_VARS)
+    return set_error(GSM_ERR_VALUE, "bad table shapes");
+  if ((n_left && a && !left) || (n_right && b && !right) || (n_join && (!join_left || !join_right)))
+    return set_error(GSM_ERR_VALUE, "null table or join columns");
+  if (n_right >= 0xFFFFFFF0LL) return set_error(GSM_ERR_VALUE, "right table must have < 2^32 rows");
+  for (int i = 0; i < n_join; i++)
+    if (join_left[i] < 0 || join_left[i] >= a || join_right[i] < 0 || join_right[i] >= b)
+      return set_error(GSM_ERR_VALUE, "join column out of range");
+  GSM_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  c->gen++;  // invalidates staged results of this context
+  std::vector<void*> tmp;
+  auto alloc = [&](void** p, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, st);
+    if (e == cudaSuccess) tmp.push_back(*p);
+    return e;
+  };
+  auto cleanup = [&]() {
+    for (void* p : tmp) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+    tmp.clear();
+  };
+#define TJ_CUDA(call)                              \
+  do {                                             \
+    cudaError_t _e = (call);                       \
+    if (_e != cudaSuccess) {                       \
+      cleanup();                                   \
+      return ::gsm::cuda_error(_e, #call);         \
+    }                                              \
+  } while (0)
+  const int w_out = a + b - n_join;
+  gsm_result* r = new gsm_result();
+  r->device = c->device;
+  r->k = w_out;
+  u32 *dL = nullptr, *dR = nullptr;
+  TJ_CUDA(alloc((void**)&dL, 4 * (size_t)n_left * a));
+  TJ_CUDA(alloc((void**)&dR, 4 * (size_t)n_right * b));
+  if (n_left * a) TJ_CUDA(cudaMemcpyAsync(dL, left, 4 * (size_t)n_left * a, cudaMemcpyHostToDevice, st));
+  if (n_right * b) TJ_CUDA(cudaMemcpyAsync(dR, right, 4 * (size_t)n_right * b, cudaMemcpyHostToDevice, st));
+  if (prealloc_total) *prealloc_total = 0;
+
+  if (n_join == 0) {  // cross product (executor.py:155-165)
+    i64 total = 0;
+    if (__builtin_mul_overflow((i64)n_left, (i64)n_right, &total) || total > budget) {
+      cleanup();
+      delete r;
+      char msg[256];
+      snprintf(msg, sizeof msg, "cross product of %lld x %lld rows exceeds budget %lld",
+               (long long)n_left, (long long)n_right, (long long)budget);
+      return set_error(GSM_ERR_RESOURCE, msg);
+    }
+    r->n = total;
+    if (total * w_out > 0) {
+      cudaError_t e = cudaMalloc(&r->rows, 4 * (size_t)total * w_out);
+      if (e != cudaSuccess) {
+        cleanup();
+        delete r;
+        return cuda_error(e, "cudaMalloc(result)");
+      }
+      k_cross_rows<<<c->grid_ts, 256, 0, st>>>(dL, n_left, a, dR, n_right, b, r->rows);
+      count_launch();
+    }
+    TJ_CUDA(cudaGetLastError());
+    cleanup();
+    *out = r;
+    return GSM_OK;
+  }
+
+  // ---- index the right table on its first join column: stable sort by key,
+  //      run heads -> hash {key, begin, len}  (the aux array of the right side)
+  u32 *keys_in, *rows_in, *keys, *rows, *slots;
+  TJ_CUDA(alloc((void**)&keys_in, 4 * (size_t)n_right));
+  TJ_CUDA(alloc((void**)&rows_in, 4 * (size_t)n_right));
+  TJ_CUDA(alloc((void**)&keys, 4 * (size_t)n_right));
+  TJ_CUDA(alloc((void**)&rows, 4 * (size_t)n_right));
+  size_t hcap = 16;
+  while (hcap < 2 * (size_t)n_right) hcap <<= 1;
+  TJ_CUDA(alloc((void**)&slots, 16 * hcap));
+  TJ_CUDA(cudaMemsetAsync(slots, 0, 16 * hcap, st));
+  if (n_right) {
+    k_key_rows<<<std::max(1, std::min(c->grid_ts, (int)((n_right + 255) / 256))), 256, 0, st>>>(
+        dR, n_right, b, join_right[0], keys_in, rows_in);
+    count_launch();
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in, keys, rows_in, rows, (int)n_right, 0, 32, st);
+    void* tsort;
+    TJ_CUDA(alloc(&tsort, tb));
+    TJ_CUDA(cub::DeviceRadixSort::SortPairs(tsort, tb, keys_in, keys, rows_in, rows, (int)n_right, 0, 32, st));
+    count_launch();
+  }
+  Orient X{};
+  X.src = keys;
+  X.dst = rows;
+  X.nnz = (u32)n_right;
+  X.hmask = (u32)(hcap - 1);
+  X.hs = reinterpret_cast<const uint4*>(slots);
+  X.kbias = 1;
+  if (n_right) {
+    k_hash_runs<<<std::max(1, std::min(c->grid_ts, (int)((n_right + 255) / 256))), 256, 0, st>>>(
+        keys, (u32)n_right, slots, (u32)(hcap - 1));
+    count_launch();
+  }
+
+  // ---- per-row first-variable counts N and E (preallocate)
+  u32* Lcols;
+  TJ_CUDA(alloc((void**)&Lcols, 4 * (size_t)n_left * a));
+  if (n_left * a) {
+    k_rows_to_cols<<<std::max(1, std::min(c->grid_ts, (int)((n_left * a + 255) / 256))), 256, 0, st>>>(
+        dL, n_left, a, Lcols);
+    count_launch();
+  }
+  i64* dcnt;
+  unsigned long long* dE;
+  TJ_CUDA(alloc((void**)&dcnt, 8 * (size_t)n_left));
+  TJ_CUDA(alloc((void**)&dE, 8));
+  TJ_CUDA(cudaMemsetAsync(dE, 0, 8, st));
+  if (n_left) {
+    k_row_counts<<<std::max(1, std::min(c->grid_ts, (int)((n_left + 255) / 256))), 256, 0, st>>>(
+        Lcols + (i64)join_left[0] * n_left, n_left, X, dcnt, dE);
+    count_launch();
+  }
+  unsigned long long E = 0;
+  TJ_CUDA(cudaMemcpyAsync(&E, dE, 8, cudaMemcpyDeviceToHost, st));
+  if (row_counts && n_left)
+    TJ_CUDA(cudaMemcpyAsync(row_counts, dcnt, 8 * (size_t)n_left, cudaMemcpyDeviceToHost, st));
+  TJ_CUDA(cudaStreamSynchronize(st));
+  if (prealloc_total) *prealloc_total = (i64)E;
+  if (budget_mode == GSM_BUDGET_PARALLEL && (i64)E > budget) {
+    cleanup();
+    delete r;
+    char msg[256];
+    snprintf(msg, sizeof msg, "pre-allocated join region of %lld rows exceeds budget %lld",
+             (long long)E, (long long)budget);
+    return set_error(GSM_ERR_RESOURCE, msg);
+  }
+
+  // ---- expand (left ++ right row index), then secondary checks + gather
+  const i64 ntile_max = (std::max<i64>(n_left, (i64)E) + TS_TILE - 1) / TS_TILE + 2;
+  u64* status;
+  TJ_CUDA(alloc((void**)&status, 8 * (size_t)ntile_max));
+  TJ_CUDA(cudaMemsetAsync(status, 0, 8 * (size_t)ntile_max, st));
+  u32* Xcols;
+  TJ_CUDA(alloc((void**)&Xcols, 4 * (size_t)std::max<u64>(E, 1) * (a + 1)));
+  TableJoinScratch h{};
+  h.L.n = n_left;
+  for (int i = 0; i < a; i++) h.L.col[i] = Lcols + (i64)i * n_left;
+  h.X.n = 0;
+  for (int i = 0; i <= a; i++) h.X.col[i] = Xcols + (i64)i * (i64)std::max<u64>(E, 1);
+  h.epochs[0] = 1;
+  h.epochs[1] = 2;
+  TableJoinScratch* d;
+  TJ_CUDA(alloc((void**)&d, sizeof(TableJoinScratch)));
+  TJ_CUDA(cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, st));
+  ExpandP ep{};
+  ep.L = &d->L;
+  ep.R = X;
+  ep.li = join_left[0];
+  ep.a = a;
+  ep.out = Xcols;
+  ep.cap = (i64)std::max<u64>(E, 1);
+  ep.O = &d->X;
+  ep.st = &d->st[0];
+  TileSync ts0{status, &d->counters[0], &d->epochs[0], 0};
+  k_tilescan<ExpandP><<<std::max(1, std::min(c->grid_ts, (int)((n_left + TS_TILE - 1) / TS_TILE))), TS_THREADS, 0, st>>>(ep, ts0);
+  count_launch();
+  TFilterP fp{};
+  fp.L = &d->X;
+  fp.a = a;
+  fp.R = dR;
+  fp.b = b;
+  fp.nsec = n_join - 1;
+  for (int i = 1; i < n_join; i++) {
+    fp.jl[i - 1] = join_left[i];
+    fp.jr[i - 1] = join_right[i];
+  }
+  fp.nrc = 0;
+  for (int k = 0; k < b; k++) {
+    bool joined = false;
+    for (int i = 0; i < n_join; i++) joined |= join_right[i] == k;
+    if (!joined) fp.rc[fp.nrc++] = k;
+  }
+  const i64 res_rows = (i64)std::max<u64>(E, 1);
+  cudaError_t e = cudaMalloc(&r->rows, 4 * (size_t)res_rows * std::max(w_out, 1));
+  if (e != cudaSuccess) {
+    cleanup();
+    delete r;
+    return cuda_error(e, "cudaMalloc(result)");
+  }
+  fp.out = r->rows;
+  fp.st = &d->st[1];
+  TileSync ts1{status, &d->counters[1], &d->epochs[1], 0};
+  k_tilescan<TFilterP><<<std::max(1, std::min(c->grid_ts, (int)(((i64)E + TS_TILE - 1) / TS_TILE))), TS_THREADS, 0, st>>>(fp, ts1);
+  count_launch();
+  TJ_CUDA(cudaGetLastError());
+  StepStat res{};
+  TJ_CUDA(cudaMemcpyAsync(&res, &d->st[1], sizeof res, cudaMemcpyDeviceToHost, st));
+  TJ_CUDA(cudaStreamSynchronize(st));
+  cleanup();
+#undef TJ_CUDA
+  r->n = res.rows;
+  if (budget_mode == GSM_BUDGET_SEQUENTIAL && r->n > budget) {
+    gsm_result_free(r);
+    char msg[256];
+    snprintf(msg, sizeof msg, "join output exceeds row budget %lld", (long long)budget);
+    return set_error(GSM_ERR_RESOURCE, msg);
+  }
+  *out = r;
+  return GSM_OK;
 }
 
 }  // extern "C"
