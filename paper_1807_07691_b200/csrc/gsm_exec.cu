@@ -48,6 +48,54 @@ struct TileSync {
   u32 epoch;              // loaded from epoch_ptr at kernel start
 };
 
+// Hub rows (>= DEFER_ROW candidates) of an expand are not written by their
+// tile's block: they are cut into CHUNK-output pieces and queued, and a
+// follow-up kernel (k_drain) spreads the pieces over every SM.
+constexpr int DEFER_ROW = 256;
+constexpr int CHUNK = 1024;
+struct Chunk {
+  i64 r;     // left row
+  i64 pos;   // output slot of candidate j0
+  u32 aux;   // run begin in dst
+  u32 j0;    // first candidate of the piece
+  u32 len;   // candidates in the piece
+  u32 pad;
+};
+struct ChunkQueue {
+  Chunk* items = nullptr;  // null: deferral disabled
+  u32* count = nullptr;    // pieces pushed (zeroed per query)
+  u32* head = nullptr;     // pieces taken by k_drain (zeroed per query)
+  u32 cap = 0;
+};
+
+// Push row r's candidates [0, c) starting at output pos as CHUNK pieces (one
+// warp).  Pieces that do not fit the queue are written by the warp itself.
+template <class P>
+__device__ void defer_row(const P& p, const DTable& s, const ChunkQueue& q, i64 r, u32 aux, i64 c,
+                          i64 pos) {
+  const int lane = threadIdx.x & 31;
+  const u32 pieces = (u32)((c + CHUNK - 1) / CHUNK);
+  u32 base = 0;
+  if (lane == 0) base = atomicAdd(q.count, pieces);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (u32 k = lane; k < pieces; k += 32) {
+    if (base + k < q.cap) {
+      Chunk ch;
+      ch.r = r;
+      ch.pos = pos + (i64)k * CHUNK;
+      ch.aux = aux;
+      ch.j0 = k * CHUNK;
+      ch.len = (u32)min((i64)CHUNK, c - (i64)k * CHUNK);
+      ch.pad = 0;
+      q.items[base + k] = ch;
+    }
+  }
+  for (u32 k = (base < q.cap ? q.cap - base : 0); k < pieces; k++) {  // overflow: write here
+    const i64 j0 = (i64)k * CHUNK, j1 = min((i64)(k + 1) * CHUNK, c);
+    for (i64 j = j0 + lane; j < j1; j += 32) p.emit(s, r, aux, j, pos + j);
+  }
+}
+
 __device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -211,6 +259,10 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
       const i64 c = s_pre[r + 1] - s_pre[r];
       const i64 pos = gbase + s_pre[r];
       const u32 aux = s_aux[r];
+      if (P::kDefer && c >= DEFER_ROW && p.dq.items) {
+        defer_row(p, s_in, p.dq, base + r, aux, c, pos);
+        continue;
+      }
       for (i64 j = lane; j < c; j += 4 * 32) {
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -257,6 +309,8 @@ struct FusedOut {
 
 struct ExpandP {
   static constexpr bool kAccumE = false;
+  static constexpr bool kDefer = true;
+  ChunkQueue dq;
   const DTable* L;
   Orient R;
   int li, a;
@@ -304,6 +358,8 @@ struct ExpandP {
 enum { F_PAIR = 0, F_CONST = 1, F_SELF = 2 };
 struct FilterP {
   static constexpr bool kAccumE = true;
+  static constexpr bool kDefer = false;
+  ChunkQueue dq;
   const DTable* L;
   Orient R;
   int li, lj, a, mode;
@@ -377,6 +433,7 @@ struct GroupP {
   int nslots;
   int last_slot;     // slot of the group's final step
   StepStat* st[MAXGS];
+  ChunkQueue dq;     // hub deferral (only when npost == 0)
   u32* out;          // columnar output (when not fused into the result)
   i64 cap;
   DTable* O;
@@ -420,6 +477,15 @@ __device__ __forceinline__ void gwrite(const GroupP& p, const DTable& s, i64 r, 
   for (int c = 0; c < p.a; c++) p.out[(i64)c * p.cap + g] = __ldg(s.col[c] + r);
   if (p.has_x) p.out[(i64)p.a * p.cap + g] = cand;
 }
+
+// Emit adaptor of a fused group for deferred hub pieces (no post filters).
+struct GroupEmit {
+  GroupP p;
+  __device__ void prepare(DTable& s) const { copy_desc(s, p.L, p.a); }
+  __device__ void emit(const DTable& s, i64 r, u32 aux, i64 j, i64 g) const {
+    gwrite(p, s, r, __ldg(p.X.dst + aux + j), g);
+  }
+};
 
 __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
   __shared__ i64 s_pre[TS_TILE + 1];
@@ -548,6 +614,10 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
       const int rl = s_long[q];
       const u32 L = s_len[rl], ax = s_aux[rl];
       i64 pos = gbase + s_pre[rl];
+      if (p.npost == 0 && L >= DEFER_ROW && p.dq.items) {
+        defer_row(GroupEmit{p}, s_in, p.dq, base + rl, ax, L, pos);
+        continue;
+      }
       for (u32 j0 = 0; j0 < L; j0 += 32) {
         const u32 j = j0 + lane;
         u32 cand = 0;
@@ -584,10 +654,35 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
   }
 }
 
+// Drain the hub pieces queued by the preceding expand: blocks grab pieces
+// (CHUNK consecutive outputs of one row) until the queue is empty.
+template <class E>
+__global__ void __launch_bounds__(TS_THREADS) k_drain(E e, ChunkQueue q) {
+  __shared__ DTable s_in;
+  __shared__ u32 s_idx;
+  pdl_wait();
+  pdl_trigger();
+  e.prepare(s_in);
+  __syncthreads();
+  const u32 n = min(*q.count, q.cap);
+  for (;;) {
+    if (threadIdx.x == 0) s_idx = atomicAdd(q.head, 1u);
+    __syncthreads();
+    const u32 idx = s_idx;
+    if (idx >= n) break;
+    const Chunk ch = q.items[idx];
+    for (u32 j = threadIdx.x; j < ch.len; j += TS_THREADS)
+      e.emit(s_in, ch.r, ch.aux, (i64)ch.j0 + j, ch.pos + j);
+    __syncthreads();
+  }
+}
+
 // DISTINCT over packed row-major rows: a row survives iff it wins the CAS
 // into an open-addressing set keyed by the whole tuple (executor.py:360-367).
 struct DistinctP {
   static constexpr bool kAccumE = false;
+  static constexpr bool kDefer = false;
+  ChunkQueue dq;
   const u32* in;
   const StepStat* nsrc;  // input row count = nsrc->rows (capped by cap_in)
   i64 cap_in;
@@ -818,6 +913,8 @@ __global__ void k_row_counts(const u32* __restrict__ Lk, i64 n, Orient X, i64* _
 // (executor.py:186-191); emit left ++ right[rcols] row-major.
 struct TFilterP {
   static constexpr bool kAccumE = false;
+  static constexpr bool kDefer = false;
+  ChunkQueue dq;
   const DTable* L;  // a left columns + the right row index at column a
   int a;
   const u32* R;     // right rows, row-major n_right x b
@@ -895,6 +992,8 @@ struct QueryBlock {
   StepStat stats[GSM_MAX_STEPS + 2];
   u32 counters[GSM_MAX_STEPS + 4];
   u32 epochs[GSM_MAX_STEPS + 4];
+  u32 qcount[GSM_MAX_STEPS + 4];  // hub-piece queue of each tile-scan launch
+  u32 qhead[GSM_MAX_STEPS + 4];
   DTable tables[MAX_TABLES];
 };
 
@@ -923,6 +1022,8 @@ struct gsm_context {
   u32 epoch = 0;
   u32* d_slots = nullptr;
   size_t n_slots = 0;
+  Chunk* d_chunks = nullptr;  // hub-piece queue storage (shared by a query's expands)
+  u32 chunk_cap = 0;
   int grid_ts = 296;
   cudaEvent_t ev[GSM_MAX_STEPS + 2] = {};
   cudaEvent_t ev_q0 = nullptr, ev_q1 = nullptr;  // whole-query device time
@@ -937,6 +1038,7 @@ struct gsm_context {
   bool use_graphs = true;  // replay each distinct query's launch sequence as a CUDA graph
   bool use_pdl = true;     // programmatic dependent launch between plan steps
   bool use_fusion = true;  // fuse [filters][expand][filters] step groups into one kernel
+  bool use_defer = true;   // spread hub rows over all SMs (k_drain)
   struct GraphEntry {
     cudaGraphExec_t exec;
     int kernels;
@@ -972,6 +1074,9 @@ gsm_status ctx_set_arena(gsm_context* c, size_t bytes) {
   GSM_CUDA(cudaMalloc(&c->arena, bytes));
   c->arena_bytes = bytes;
   size_t half = bytes / 2;
+  if (c->d_chunks) cudaFree(c->d_chunks);
+  c->chunk_cap = (u32)std::min<size_t>(std::max<size_t>(65536, half / 4 / 512), 1u << 28);
+  GSM_CUDA(cudaMalloc(&c->d_chunks, sizeof(Chunk) * (size_t)c->chunk_cap));
   size_t max_rows = std::max<size_t>(half / 4, c->store->max_nnz) + 1;
   c->n_status = max_rows / TS_TILE + 2;
   GSM_CUDA(cudaMalloc(&c->d_status, c->n_status * sizeof(u64)));
@@ -1128,6 +1233,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* ng = getenv("GSM_NO_GRAPHS")) c->use_graphs = !(ng[0] == '1');
   if (const char* np = getenv("GSM_NO_PDL")) c->use_pdl = !(np[0] == '1');
   if (const char* nf = getenv("GSM_NO_FUSION")) c->use_fusion = !(nf[0] == '1');
+  if (const char* nd = getenv("GSM_NO_DEFER")) c->use_defer = !(nd[0] == '1');
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
     return st;
@@ -1172,6 +1278,7 @@ gsm_status gsm_context_free(gsm_context* c) {
   if (c->d_block) cudaFree(c->d_block);
   if (c->h_block) cudaFreeHost(c->h_block);
   if (c->d_slots) cudaFree(c->d_slots);
+  if (c->d_chunks) cudaFree(c->d_chunks);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->d_stage) cudaFree(c->d_stage);
   for (auto& ev : c->ev)
@@ -1241,6 +1348,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   ex.plan.assign(n, StepPlan());
   memset(hb->stats, 0, sizeof(hb->stats));
   memset(hb->counters, 0, sizeof(hb->counters));
+  memset(hb->qcount, 0, sizeof(hb->qcount));
+  memset(hb->qhead, 0, sizeof(hb->qhead));
 
   DTable* dT = c->d_block->tables;
   StepStat* dS = c->d_block->stats;
@@ -1263,6 +1372,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     int a, b;
     int grid;
     int last_step;  // S_GROUP: the last fused step
+    u32 fanout;     // S_EXPAND: longest candidate run of the orientation
+    bool drain;     // hub pieces may be queued: launch k_drain after
   };
   std::vector<Launch> launches;
   // Step fusion state: a group is [filters][expand][filters] over one input
@@ -1352,6 +1463,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
         e.cap = ex.cap_for((int)out_schema.size());
         e.O = dT + L.out;
         e.st = dS + s;
+        L.fanout = (on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid]).max_run;
       } else {
         L.kind = S_FILTER;
         L.out = ex.new_table(a, oh);
@@ -1442,6 +1554,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           gp.X = L.ep.R;
           gp.xk = L.ep.li;
           gp.xslot = slot;
+          G.fanout = L.fanout;
         } else {
           FSpec fs{L.fp.R, L.fp.mode, L.fp.li, L.fp.lj, L.fp.cval, slot};
           (gp.has_x ? post : pre).push_back(fs);
@@ -1460,6 +1573,25 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       i = j;
     }
     launches.swap(fl);
+  }
+
+  // ---- hub deferral for expands whose orientation has long runs ----
+  {
+    int slot = 0;
+    for (auto& L : launches) {
+      if (L.kind != S_EXPAND && L.kind != S_FILTER && L.kind != S_GROUP) continue;
+      const bool hubby = c->use_defer && L.fanout >= (u32)DEFER_ROW;
+      if (hubby && L.kind == S_EXPAND) {
+        L.ep.dq = ChunkQueue{c->d_chunks, c->d_block->qcount + slot, c->d_block->qhead + slot,
+                             c->chunk_cap};
+        L.drain = true;
+      } else if (hubby && L.kind == S_GROUP && L.gp.has_x && L.gp.npost == 0) {
+        L.gp.dq = ChunkQueue{c->d_chunks, c->d_block->qcount + slot, c->d_block->qhead + slot,
+                             c->chunk_cap};
+        L.drain = true;
+      }
+      slot++;
+    }
   }
 
   // ---- projection target ----
@@ -1541,6 +1673,10 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           slot++;
           GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP>, L.grid, TS_THREADS, st, L.ep, ts));
           nk++;
+          if (L.drain) {
+            GSM_CUDA(launch(c->use_pdl, k_drain<ExpandP>, c->grid_ts, TS_THREADS, st, L.ep, L.ep.dq));
+            nk++;
+          }
           break;
         }
         case S_FILTER: {
@@ -1555,6 +1691,11 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           slot++;
           GSM_CUDA(launch(c->use_pdl, k_group, L.grid, TS_THREADS, st, L.gp, ts));
           nk++;
+          if (L.drain) {
+            GSM_CUDA(launch(c->use_pdl, k_drain<GroupEmit>, c->grid_ts, TS_THREADS, st,
+                            GroupEmit{L.gp}, L.gp.dq));
+            nk++;
+          }
           break;
         }
         case S_CROSS: {

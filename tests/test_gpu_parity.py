@@ -185,10 +185,10 @@ def test_reference_objects_drop_in():
 
 
 def test_execution_variants_agree(store_factory):
-    """Graph replay, programmatic dependent launch and step fusion are pure
-    optimisations: each query gives the same bag and the same per-step report
-    with every combination switched off (GSM_NO_GRAPHS / GSM_NO_PDL /
-    GSM_NO_FUSION), and repeated (replayed) executions agree."""
+    """Graph replay, programmatic dependent launch, step fusion and hub
+    deferral are pure optimisations: each query gives the same bag and the
+    same per-step report with them switched off (GSM_NO_GRAPHS / GSM_NO_PDL /
+    GSM_NO_FUSION / GSM_NO_DEFER), and repeated (replayed) executions agree."""
     import json
     import os
     import subprocess
@@ -218,8 +218,8 @@ def test_execution_variants_agree(store_factory):
         "print(json.dumps(out))\n" % (str(GOLDEN.parents[1]), str(GOLDEN.parent), str(d))
     )
     results = {}
-    for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION",
-                    "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION"):
+    for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION", "GSM_NO_DEFER",
+                    "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER"):
         env = dict(os.environ)
         for k in filter(None, variant.split(",")):
             env[k] = "1"
