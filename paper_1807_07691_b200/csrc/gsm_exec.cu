@@ -96,6 +96,33 @@ __device__ void defer_row(const P& p, const DTable& s, const ChunkQueue& q, i64 
   }
 }
 
+// The last kernel of a query copies the (then final) step counters to the
+// head of the result buffer, so the host reads counters and result rows with
+// ONE device->host copy.  "Last block" detection: every block bumps a counter
+// after its own counter updates; the block that sees gridDim.x - 1 copies.
+struct ExportArgs {
+  const StepStat* src = nullptr;
+  StepStat* dst = nullptr;  // null: this kernel is not the query's last
+  int n = 0;
+  u32* done = nullptr;
+};
+__device__ __forceinline__ void export_if_last(const ExportArgs& x) {
+  if (!x.dst) return;
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(x.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const volatile i64* src = reinterpret_cast<const volatile i64*>(x.src);
+    i64* dst = reinterpret_cast<i64*>(x.dst);
+    for (int i = threadIdx.x; i < x.n * 4; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
 __device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -159,7 +186,7 @@ __device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
 //   P::kAccumE                 accumulate e into st->e (filters)
 // ---------------------------------------------------------------------------
 template <class P>
-__global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
+__global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts, ExportArgs xa) {
   __shared__ i64 s_pre[TS_TILE + 1];
   __shared__ u32 s_aux[TS_TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
@@ -182,12 +209,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
   __syncthreads();
   const i64 n = p.rows(s_in);
   const i64 ntiles = (n + TS_TILE - 1) / TS_TILE;
-  if (ntiles == 0) {
-    if (blockIdx.x == 0 && tid == 0) p.finish(0);
-    return;
-  }
+  if (ntiles == 0 && blockIdx.x == 0 && tid == 0) p.finish(0);
   i64 e_acc = 0;
-  for (bool first = true;; first = false) {
+  for (bool first = true; ntiles > 0; first = false) {
     if (!first) {
       if (tid == 0) {
         s_tile = atomicAdd(ts.counter, 1u);
@@ -279,6 +303,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts) {
     for (int o = 16; o; o >>= 1) e_acc += __shfl_xor_sync(0xffffffffu, e_acc, o);
     if (lane == 0 && e_acc) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st->e), (unsigned long long)e_acc);
   }
+  export_if_last(xa);
 }
 
 __device__ __forceinline__ void copy_desc(DTable& dst, const DTable* src, int ncols) {
@@ -487,7 +512,7 @@ struct GroupEmit {
   }
 };
 
-__global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
+__global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts, ExportArgs xa) {
   __shared__ i64 s_pre[TS_TILE + 1];
   __shared__ u32 s_aux[TS_TILE];
   __shared__ u32 s_len[TS_TILE];
@@ -513,14 +538,11 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
   __syncthreads();
   const i64 n = s_in.n;
   const i64 ntiles = (n + TS_TILE - 1) / TS_TILE;
-  if (ntiles == 0) {
-    if (blockIdx.x == 0 && tid == 0) {
-      p.O->n = 0;
-      if (p.fz.stage) p.fz.finish(0);
-    }
-    return;
+  if (ntiles == 0 && blockIdx.x == 0 && tid == 0) {
+    p.O->n = 0;
+    if (p.fz.stage) p.fz.finish(0);
   }
-  for (bool first = true;; first = false) {
+  for (bool first = true; ntiles > 0; first = false) {
     if (!first) {
       if (tid == 0) {
         s_tile = atomicAdd(ts.counter, 1u);
@@ -652,12 +674,13 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts) {
       if (rw) atomicAdd(reinterpret_cast<unsigned long long*>(&p.st[k]->rows), (unsigned long long)rw);
     }
   }
+  export_if_last(xa);
 }
 
 // Drain the hub pieces queued by the preceding expand: blocks grab pieces
 // (CHUNK consecutive outputs of one row) until the queue is empty.
 template <class E>
-__global__ void __launch_bounds__(TS_THREADS) k_drain(E e, ChunkQueue q) {
+__global__ void __launch_bounds__(TS_THREADS) k_drain(E e, ChunkQueue q, ExportArgs xa) {
   __shared__ DTable s_in;
   __shared__ u32 s_idx;
   pdl_wait();
@@ -675,6 +698,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_drain(E e, ChunkQueue q) {
       e.emit(s_in, ch.r, ch.aux, (i64)ch.j0 + j, ch.pos + j);
     __syncthreads();
   }
+  export_if_last(xa);
 }
 
 // DISTINCT over packed row-major rows: a row survives iff it wins the CAS
@@ -730,7 +754,7 @@ struct DistinctP {
 // J0: cross product (executor.py:155-165).  Row g = L[g / |R|] ++ R[g % |R|].
 // stat: e = |L|, pad = |R| (for the budget message); rows = |L|*|R|.
 __global__ void k_cross(const DTable* L, const DTable* R, int a, int b, u32* out, i64 cap,
-                        i64 budget, DTable* O, StepStat* st) {
+                        i64 budget, DTable* O, StepStat* st, ExportArgs xa) {
   pdl_wait();
   pdl_trigger();
   const i64 nl = L->n, nr = R->n;
@@ -752,11 +776,13 @@ __global__ void k_cross(const DTable* L, const DTable* R, int a, int b, u32* out
     for (int c = 0; c < a; c++) out[(i64)c * cap + g] = __ldg(L->col[c] + i);
     for (int c = 0; c < b; c++) out[(i64)(a + c) * cap + g] = __ldg(R->col[c] + j);
   }
+  export_if_last(xa);
 }
 
 // J0 against a zero-arity right table (a constant-constant pattern, R5):
 // the result is the left table itself or nothing -> descriptor aliasing.
-__global__ void k_gate(const DTable* L, const DTable* R, int a, DTable* O, StepStat* st) {
+__global__ void k_gate(const DTable* L, const DTable* R, int a, DTable* O, StepStat* st,
+                       ExportArgs xa) {
   pdl_wait();
   pdl_trigger();
   const int tid = threadIdx.x;
@@ -769,6 +795,7 @@ __global__ void k_gate(const DTable* L, const DTable* R, int a, DTable* O, StepS
     st->pad = nr;
     st->rows = total;
   }
+  export_if_last(xa);
 }
 
 // Constant-endpoint scans (executor.py:115-126): one thread per job.
@@ -826,7 +853,7 @@ struct ProjArgs {
 // pinned host memory before its single sync; larger ones go to the arena and
 // become a device-resident result.  st->pad = 1 when staged.
 __global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* dev_out, i64 dev_cap,
-                       u32* host_out, i64 host_cap, StepStat* st) {
+                       u32* host_out, i64 host_cap, StepStat* st, ExportArgs xa) {
   pdl_wait();
   pdl_trigger();
   i64 n = T->n;
@@ -842,6 +869,7 @@ __global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* dev_out, i64 de
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride)
     for (int c = 0; c < k; c++) out[r * k + c] = __ldg(T->col[pj.col[c]] + r);
+  export_if_last(xa);
 }
 
 // ---------------------------------------------------------------------------
@@ -985,6 +1013,8 @@ cudaError_t launch(bool pdl, void (*kern)(KArgs...), int grid, int block, cudaSt
 namespace {
 
 constexpr int MAX_TABLES = 2 * GSM_MAX_STEPS + 2;
+constexpr size_t STAGE_HEAD = 4096;  // >= sizeof(StepStat) * (GSM_MAX_STEPS + 2)
+static_assert(sizeof(StepStat) * (GSM_MAX_STEPS + 2) <= STAGE_HEAD, "stage head too small");
 
 // Device query block: everything a query's kernels read/write besides the
 // store and the arena.  Uploaded in one H2D copy, read back in one D2H copy.
@@ -994,6 +1024,7 @@ struct QueryBlock {
   u32 epochs[GSM_MAX_STEPS + 4];
   u32 qcount[GSM_MAX_STEPS + 4];  // hub-piece queue of each tile-scan launch
   u32 qhead[GSM_MAX_STEPS + 4];
+  u32 done[4];  // blocks finished in the query's last kernel (export_if_last)
   DTable tables[MAX_TABLES];
 };
 
@@ -1029,9 +1060,12 @@ struct gsm_context {
   cudaEvent_t ev_q0 = nullptr, ev_q1 = nullptr;  // whole-query device time
   cudaEvent_t ev_q2 = nullptr;  // end of the (un-captured) DISTINCT tail
   cudaEvent_t ev_b0 = nullptr, ev_b1 = nullptr, ev_done = nullptr;  // batch timing
-  u32* h_stage = nullptr;  // pinned host result staging
-  u32* d_stage = nullptr;  // device result buffer (projected rows, row-major)
-  size_t stage_bytes = 0;
+  // Result staging: [step counters (STAGE_HEAD bytes) | projected rows].
+  u32* h_stage = nullptr;  // pinned host copy
+  u32* d_stage = nullptr;  // device buffer written by the query's last kernel(s)
+  u32* h_rows = nullptr;   // = h_stage + STAGE_HEAD
+  u32* d_rows = nullptr;   // = d_stage + STAGE_HEAD
+  size_t stage_bytes = 0;  // capacity for rows
   size_t guess = 0;        // bytes of the result D2H copied inside the launch sequence
   std::unordered_map<std::string, size_t> last_bytes;  // per plan: last result size
   u64 gen = 0;             // bumped by every gsm_execute (staged results expire)
@@ -1048,7 +1082,7 @@ struct gsm_context {
 
 namespace gsm {
 u64 context_generation(const gsm_context* c) { return c ? c->gen : ~0ull; }
-const u32* context_device_rows(const gsm_context* c) { return c ? c->d_stage : nullptr; }
+const u32* context_device_rows(const gsm_context* c) { return c ? c->d_rows : nullptr; }
 }
 
 namespace {
@@ -1090,12 +1124,14 @@ gsm_status ctx_set_stage(gsm_context* c, size_t bytes) {
   if (c->h_stage) {
     cudaFreeHost(c->h_stage);
     cudaFree(c->d_stage);
-    c->h_stage = c->d_stage = nullptr;
+    c->h_stage = c->d_stage = c->h_rows = c->d_rows = nullptr;
     c->stage_bytes = 0;
   }
   bytes = (bytes + 4095) & ~(size_t)4095;
-  GSM_CUDA(cudaMallocHost(&c->h_stage, bytes));
-  GSM_CUDA(cudaMalloc(&c->d_stage, bytes));
+  GSM_CUDA(cudaMallocHost(&c->h_stage, bytes + STAGE_HEAD));
+  GSM_CUDA(cudaMalloc(&c->d_stage, bytes + STAGE_HEAD));
+  c->h_rows = c->h_stage + STAGE_HEAD / 4;
+  c->d_rows = c->d_stage + STAGE_HEAD / 4;
   c->stage_bytes = bytes;
   return GSM_OK;
 }
@@ -1350,6 +1386,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   memset(hb->counters, 0, sizeof(hb->counters));
   memset(hb->qcount, 0, sizeof(hb->qcount));
   memset(hb->qhead, 0, sizeof(hb->qhead));
+  memset(hb->done, 0, sizeof(hb->done));
 
   DTable* dT = c->d_block->tables;
   StepStat* dS = c->d_block->stats;
@@ -1613,7 +1650,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       (launches.back().kind == S_EXPAND || launches.back().kind == S_FILTER ||
        launches.back().kind == S_GROUP)) {
     FusedOut fz;
-    fz.stage = c->d_stage;
+    fz.stage = c->d_rows;
     fz.cap = stage_cap;
     fz.k = n_proj;
     for (int j = 0; j < n_proj; j++) fz.pj[j] = pj_idx[j];
@@ -1663,18 +1700,30 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       nk++;
     }
     if (timing) GSM_CUDA(record(c->ev[1]));
+    // the query's last kernel exports the step counters to the stage head
+    const ExportArgs xlast{dS, reinterpret_cast<StepStat*>(c->d_stage), n + 1, c->d_block->done};
+    int last_launch = -1;
+    for (int i = (int)launches.size() - 1; i >= 0 && fused; i--)
+      if (launches[i].kind != S_EMPTY) {
+        last_launch = i;
+        break;
+      }
     int slot = 0;
-    for (auto& L : launches) {
+    for (int li = 0; li < (int)launches.size(); li++) {
+      auto& L = launches[li];
+      const bool is_last = li == last_launch;
+      const ExportArgs xm = is_last && !L.drain ? xlast : ExportArgs{};
+      const ExportArgs xd = is_last && L.drain ? xlast : ExportArgs{};
       switch (L.kind) {
         case S_EMPTY:
           break;  // descriptor n = 0 and zero stats were uploaded
         case S_EXPAND: {
           TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
           slot++;
-          GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP>, L.grid, TS_THREADS, st, L.ep, ts));
+          GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP>, L.grid, TS_THREADS, st, L.ep, ts, xm));
           nk++;
           if (L.drain) {
-            GSM_CUDA(launch(c->use_pdl, k_drain<ExpandP>, c->grid_ts, TS_THREADS, st, L.ep, L.ep.dq));
+            GSM_CUDA(launch(c->use_pdl, k_drain<ExpandP>, c->grid_ts, TS_THREADS, st, L.ep, L.ep.dq, xd));
             nk++;
           }
           break;
@@ -1682,18 +1731,18 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
         case S_FILTER: {
           TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
           slot++;
-          GSM_CUDA(launch(c->use_pdl, k_tilescan<FilterP>, L.grid, TS_THREADS, st, L.fp, ts));
+          GSM_CUDA(launch(c->use_pdl, k_tilescan<FilterP>, L.grid, TS_THREADS, st, L.fp, ts, xm));
           nk++;
           break;
         }
         case S_GROUP: {
           TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
           slot++;
-          GSM_CUDA(launch(c->use_pdl, k_group, L.grid, TS_THREADS, st, L.gp, ts));
+          GSM_CUDA(launch(c->use_pdl, k_group, L.grid, TS_THREADS, st, L.gp, ts, xm));
           nk++;
           if (L.drain) {
             GSM_CUDA(launch(c->use_pdl, k_drain<GroupEmit>, c->grid_ts, TS_THREADS, st,
-                            GroupEmit{L.gp}, L.gp.dq));
+                            GroupEmit{L.gp}, L.gp.dq, xd));
             nk++;
           }
           break;
@@ -1703,13 +1752,14 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           GSM_CUDA(launch(c->use_pdl, k_cross, L.grid, 256, st, (const DTable*)(dT + L.left),
                           (const DTable*)(dT + L.right), L.a, L.b,
                           reinterpret_cast<u32*>(ex.buf(oh)), ex.cap_for(L.a + L.b), (i64)budget,
-                          dT + L.out, dS + L.step));
+                          dT + L.out, dS + L.step, ExportArgs{}));
           nk++;
           break;
         }
         case S_GATE:
           GSM_CUDA(launch(c->use_pdl, k_gate, 1, 64, st, (const DTable*)(dT + L.left),
-                          (const DTable*)(dT + L.right), ex.arity[L.left], dT + L.out, dS + L.step));
+                          (const DTable*)(dT + L.right), ex.arity[L.left], dT + L.out, dS + L.step,
+                          ExportArgs{}));
           nk++;
           break;
         default:
@@ -1724,20 +1774,19 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     if (!fused) {
       // DISTINCT reads the packed rows on the device, so only plain
       // projections are packed straight into the pinned staging buffer.
-      u32* host_dst = distinct ? nullptr : c->d_stage;
+      u32* host_dst = distinct ? nullptr : c->d_rows;
       GSM_CUDA(launch(c->use_pdl, k_pack, ex.grid_for_rows(ex.ub[cur], 256), 256, st,
                       (const DTable*)(dT + cur), pa, n_proj, pack_out, pack_cap, host_dst,
-                      stage_cap, dS + pack_stat));
+                      stage_cap, dS + pack_stat, xlast));
       nk++;
     }
     if (timing) GSM_CUDA(record(c->ev_q1));
     GSM_CUDA(cudaGetLastError());
-    GSM_CUDA(cudaMemcpyAsync(hb->stats, dS, sizeof(StepStat) * (size_t)(n + 1),
-                             cudaMemcpyDeviceToHost, st));
-    // The result rows, up to this plan's expected size; the host fetches any
+    // ONE copy: the step counters (exported by the last kernel) and the
+    // result rows up to this plan's expected size; the host fetches any
     // remainder after the sync (rare: only when the result grew).
-    if (!distinct && c->guess)
-      GSM_CUDA(cudaMemcpyAsync(c->h_stage, c->d_stage, c->guess, cudaMemcpyDeviceToHost, st));
+    GSM_CUDA(cudaMemcpyAsync(c->h_stage, c->d_stage, STAGE_HEAD + (distinct ? 0 : c->guess),
+                             cudaMemcpyDeviceToHost, st));
     kernels = nk;
     return GSM_OK;
   };
@@ -1845,6 +1894,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
       if (stt != GSM_OK) return stt;
     }
     GSM_CUDA(cudaStreamSynchronize(c->stream));
+    memcpy(c->h_block->stats, c->h_stage, sizeof(StepStat) * (size_t)(n + 1));
     const QueryBlock* hb = c->h_block;
     // Budget checks in plan order (executor.py:158-163, 192-193, 237-241).
     // A step's counters are exact as long as no earlier step overflowed.
@@ -1961,7 +2011,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     const bool to_host = (size_t)nrows * row_bytes <= c->stage_bytes;
     u32* dst = nullptr;
     if (to_host) {
-      dst = c->d_stage;
+      dst = c->d_rows;
     } else {
       cudaError_t e = cudaMalloc(&r->rows, std::max<size_t>(4, (size_t)nrows * row_bytes));
       if (e != cudaSuccess) {
@@ -1987,7 +2037,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
                              c->h_block->epochs + GSM_MAX_STEPS + 2, 4, cudaMemcpyHostToDevice, st));
     TileSync ts{c->d_status, c->d_block->counters + GSM_MAX_STEPS + 2,
                 c->d_block->epochs + GSM_MAX_STEPS + 2, 0};
-    k_tilescan<DistinctP><<<c->grid_ts, TS_THREADS, 0, st>>>(dp, ts);
+    k_tilescan<DistinctP><<<c->grid_ts, TS_THREADS, 0, st>>>(dp, ts, ExportArgs{});
     count_launch();
     kernels++;
     if (timing) GSM_CUDA(cudaEventRecord(c->ev_q2, st));
@@ -1999,16 +2049,16 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     r->n = c->h_block->stats[pack_stat + 1].rows;
     if (to_host) {
       if (r->n * (i64)row_bytes > 0)
-        GSM_CUDA(cudaMemcpy(c->h_stage, c->d_stage, (size_t)r->n * row_bytes, cudaMemcpyDeviceToHost));
-      r->staged = c->h_stage;
+        GSM_CUDA(cudaMemcpy(c->h_rows, c->d_rows, (size_t)r->n * row_bytes, cudaMemcpyDeviceToHost));
+      r->staged = c->h_rows;
     }
   } else if (staged) {
     r->n = nrows;
-    r->staged = c->h_stage;
+    r->staged = c->h_rows;
     const size_t bytes = (size_t)nrows * row_bytes;
     if (bytes > c->guess)
-      GSM_CUDA(cudaMemcpy(reinterpret_cast<char*>(c->h_stage) + c->guess,
-                          reinterpret_cast<char*>(c->d_stage) + c->guess, bytes - c->guess,
+      GSM_CUDA(cudaMemcpy(reinterpret_cast<char*>(c->h_rows) + c->guess,
+                          reinterpret_cast<char*>(c->d_rows) + c->guess, bytes - c->guess,
                           cudaMemcpyDeviceToHost));
     c->last_bytes[plan_key] = bytes;
     if (c->last_bytes.size() > 4096) c->last_bytes.clear();
@@ -2295,7 +2345,7 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
   ep.O = &d->X;
   ep.st = &d->st[0];
   TileSync ts0{status, &d->counters[0], &d->epochs[0], 0};
-  k_tilescan<ExpandP><<<std::max(1, std::min(c->grid_ts, (int)((n_left + TS_TILE - 1) / TS_TILE))), TS_THREADS, 0, st>>>(ep, ts0);
+  k_tilescan<ExpandP><<<std::max(1, std::min(c->grid_ts, (int)((n_left + TS_TILE - 1) / TS_TILE))), TS_THREADS, 0, st>>>(ep, ts0, ExportArgs{});
   count_launch();
   TFilterP fp{};
   fp.L = &d->X;
@@ -2323,7 +2373,7 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
   fp.out = r->rows;
   fp.st = &d->st[1];
   TileSync ts1{status, &d->counters[1], &d->epochs[1], 0};
-  k_tilescan<TFilterP><<<std::max(1, std::min(c->grid_ts, (int)(((i64)E + TS_TILE - 1) / TS_TILE))), TS_THREADS, 0, st>>>(fp, ts1);
+  k_tilescan<TFilterP><<<std::max(1, std::min(c->grid_ts, (int)(((i64)E + TS_TILE - 1) / TS_TILE))), TS_THREADS, 0, st>>>(fp, ts1, ExportArgs{});
   count_launch();
   TJ_CUDA(cudaGetLastError());
   StepStat res{};
