@@ -1617,7 +1617,10 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     int slot = 0;
     for (auto& L : launches) {
       if (L.kind != S_EXPAND && L.kind != S_FILTER && L.kind != S_GROUP) continue;
-      const bool hubby = c->use_defer && L.fanout >= (u32)DEFER_ROW;
+      // Only when the left table is small: with many tiles the blocks already
+      // share the hubs, and the queue round trip would only add traffic.
+      const bool small_left = ex.ub[L.left] <= (i64)c->grid_ts * TS_TILE / 4;
+      const bool hubby = c->use_defer && small_left && L.fanout >= (u32)DEFER_ROW;
       if (hubby && L.kind == S_EXPAND) {
         L.ep.dq = ChunkQueue{c->d_chunks, c->d_block->qcount + slot, c->d_block->qhead + slot,
                              c->chunk_cap};
