@@ -287,11 +287,16 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts, Expor
         defer_row(p, s_in, p.dq, base + r, aux, c, pos);
         continue;
       }
-      for (i64 j = lane; j < c; j += 4 * 32) {
+      if constexpr (P::kWarpEmit) {
+#pragma unroll 4
+        for (i64 j0 = 0; j0 < c; j0 += 32) p.emit_warp(s_in, base + r, aux, j0, c, pos);
+      } else {
+        for (i64 j = lane; j < c; j += 4 * 32) {
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const i64 jj = j + 32 * u;
-          if (jj < c) p.emit(s_in, base + r, aux, jj, pos + jj);
+          for (int u = 0; u < 4; u++) {
+            const i64 jj = j + 32 * u;
+            if (jj < c) p.emit(s_in, base + r, aux, jj, pos + jj);
+          }
         }
       }
     }
@@ -335,6 +340,7 @@ struct FusedOut {
 struct ExpandP {
   static constexpr bool kAccumE = false;
   static constexpr bool kDefer = true;
+  static constexpr bool kWarpEmit = true;
   ChunkQueue dq;
   const DTable* L;
   Orient R;
@@ -367,6 +373,37 @@ struct ExpandP {
     for (int c = 0; c < a; c++) out[(i64)c * cap + g] = __ldg(s.col[c] + r);
     out[(i64)a * cap + g] = nv;
   }
+  // One warp writes candidates [j0, j0+32) of row r (output slots pos + j).
+  // Fused row-major output: the 32 rows x k words are contiguous, so lane l
+  // writes words l, l+32, ... of that block, fetching each value by shuffle
+  // (the left columns are the same for all 32 rows) -> 128-byte stores.
+  __device__ void emit_warp(const DTable& s, i64 r, u32 aux, i64 j0, i64 c, i64 pos) const {
+    const int lane = threadIdx.x & 31;
+    const i64 j = j0 + lane;
+    const u32 nv = j < c ? __ldg(R.dst + aux + j) : 0u;
+    if (fz.stage) {
+      const int k = fz.k;
+      const i64 rows = min((i64)32, c - j0);
+      const u32 lv = lane < a ? __ldg(s.col[lane] + r) : 0u;
+      const i64 base = pos + j0;  // output slot of candidate j0
+      const int words = (int)rows * k;
+      for (int w0 = 0; w0 < words; w0 += 32) {
+        const int w = w0 + lane;
+        const int rr = w < words ? w / k : 0;
+        const int src = w < words ? fz.pj[w - rr * k] : 0;
+        const u32 v_left = __shfl_sync(0xffffffffu, lv, src < a ? src : 0);
+        const u32 v_new = __shfl_sync(0xffffffffu, nv, rr);
+        if (w < words && base + rr < fz.cap) fz.stage[base * k + w] = src < a ? v_left : v_new;
+      }
+      return;
+    }
+    if (j < c && pos + j < cap) {
+      const i64 g = pos + j;
+#pragma unroll 4
+      for (int cc = 0; cc < a; cc++) out[(i64)cc * cap + g] = __ldg(s.col[cc] + r);
+      out[(i64)a * cap + g] = nv;
+    }
+  }
   __device__ void finish(i64 total) const {
     O->n = total < cap ? total : cap;
     st->e = total;
@@ -382,6 +419,7 @@ struct ExpandP {
 //   F_SELF  (?x p ?x):              (L[li], L[li]) in M       E = kept rows
 enum { F_PAIR = 0, F_CONST = 1, F_SELF = 2 };
 struct FilterP {
+  static constexpr bool kWarpEmit = false;
   static constexpr bool kAccumE = true;
   static constexpr bool kDefer = false;
   ChunkQueue dq;
@@ -505,6 +543,7 @@ __device__ __forceinline__ void gwrite(const GroupP& p, const DTable& s, i64 r, 
 
 // Emit adaptor of a fused group for deferred hub pieces (no post filters).
 struct GroupEmit {
+  static constexpr bool kWarpEmit = false;
   GroupP p;
   __device__ void prepare(DTable& s) const { copy_desc(s, p.L, p.a); }
   __device__ void emit(const DTable& s, i64 r, u32 aux, i64 j, i64 g) const {
@@ -694,8 +733,14 @@ __global__ void __launch_bounds__(TS_THREADS) k_drain(E e, ChunkQueue q, ExportA
     const u32 idx = s_idx;
     if (idx >= n) break;
     const Chunk ch = q.items[idx];
-    for (u32 j = threadIdx.x; j < ch.len; j += TS_THREADS)
-      e.emit(s_in, ch.r, ch.aux, (i64)ch.j0 + j, ch.pos + j);
+    if constexpr (E::kWarpEmit) {
+      const i64 c_end = (i64)ch.j0 + ch.len, pos0 = ch.pos - (i64)ch.j0;
+      for (u32 j = (threadIdx.x >> 5) * 32; j < ch.len; j += TS_THREADS)
+        e.emit_warp(s_in, ch.r, ch.aux, (i64)ch.j0 + j, c_end, pos0);
+    } else {
+      for (u32 j = threadIdx.x; j < ch.len; j += TS_THREADS)
+        e.emit(s_in, ch.r, ch.aux, (i64)ch.j0 + j, ch.pos + j);
+    }
     __syncthreads();
   }
   export_if_last(xa);
@@ -704,6 +749,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_drain(E e, ChunkQueue q, ExportA
 // DISTINCT over packed row-major rows: a row survives iff it wins the CAS
 // into an open-addressing set keyed by the whole tuple (executor.py:360-367).
 struct DistinctP {
+  static constexpr bool kWarpEmit = false;
   static constexpr bool kAccumE = false;
   static constexpr bool kDefer = false;
   ChunkQueue dq;
@@ -940,6 +986,7 @@ __global__ void k_row_counts(const u32* __restrict__ Lk, i64 n, Orient X, i64* _
 // index) table: keep a candidate iff every further shared variable agrees
 // (executor.py:186-191); emit left ++ right[rcols] row-major.
 struct TFilterP {
+  static constexpr bool kWarpEmit = false;
   static constexpr bool kAccumE = false;
   static constexpr bool kDefer = false;
   ChunkQueue dq;
