@@ -1120,6 +1120,7 @@ struct gsm_context {
   bool use_pdl = true;     // programmatic dependent launch between plan steps
   bool use_fusion = true;  // fuse [filters][expand][filters] step groups into one kernel
   bool use_defer = true;   // spread hub rows over all SMs (k_drain)
+  bool use_proj_fusion = true;  // write the projected result from the last join
   struct GraphEntry {
     cudaGraphExec_t exec;
     int kernels;
@@ -1317,6 +1318,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* np = getenv("GSM_NO_PDL")) c->use_pdl = !(np[0] == '1');
   if (const char* nf = getenv("GSM_NO_FUSION")) c->use_fusion = !(nf[0] == '1');
   if (const char* nd = getenv("GSM_NO_DEFER")) c->use_defer = !(nd[0] == '1');
+  if (const char* npf = getenv("GSM_NO_PROJ_FUSION")) c->use_proj_fusion = !(npf[0] == '1');
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
     return st;
@@ -1696,7 +1698,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // Fuse the projection into the last join when it is an expand/filter and
   // the result goes to the host staging buffer (no DISTINCT).
   bool fused = false;
-  if (allow_fuse && !distinct && !launches.empty() &&
+  if (allow_fuse && c->use_proj_fusion && !distinct && !launches.empty() &&
       (launches.back().kind == S_EXPAND || launches.back().kind == S_FILTER ||
        launches.back().kind == S_GROUP)) {
     FusedOut fz;
