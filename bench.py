@@ -215,7 +215,7 @@ def run_ours(args):
         triples = store.triple_count
         flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=f"cuda:{local}")  # 256 MB > L2
         if args.only_probe:
-            print(json.dumps(run_probe(g, store, _peaks()[0], reps=2)))
+            print(json.dumps(run_probe(g, store, _peaks()[0], reps=5)))
             return
 
         items = [(q, plan) for _, q, plan in queries]
@@ -344,7 +344,22 @@ def run_ours(args):
                     "classes": {k: {"bytes": int(v[0]), "steps": v[2], "ms": round(1e3 * v[1], 3)}
                                 for k, v in cls.items()}}
 
-        probe = None if args.no_probe else run_probe(g, store, peaks)
+        probe = None
+        if not args.no_probe:
+            # (a) as a user runs it: the projection is fused into the expand,
+            #     which writes the row-major result directly;
+            # (b) the expand kernel alone writing columnar binding tables (as
+            #     for every non-final step): a subprocess with projection
+            #     fusion off, timing only the expand step.
+            probe = {"fused_projection": run_probe(g, store, peaks)}
+            env = dict(os.environ, GSM_NO_PROJ_FUSION="1")
+            out = subprocess.run([sys.executable, str(REPO / "bench.py"), "--only-probe",
+                                  "--univ", str(args.univ), "--seed", str(args.seed)],
+                                 env=env, capture_output=True, text=True)
+            try:
+                probe["expand_kernel_columnar"] = json.loads(out.stdout.strip().splitlines()[-1])
+            except Exception:
+                probe["expand_kernel_columnar"] = {"error": out.stderr[-400:]}
         cpu = None
         if not args.no_cpu_baseline:
             cpu = cpu_baseline_port(store, queries, args.cpu_seconds)
