@@ -1121,9 +1121,19 @@ struct gsm_context {
   bool use_fusion = true;  // fuse [filters][expand][filters] step groups into one kernel
   bool use_defer = true;   // spread hub rows over all SMs (k_drain)
   bool use_proj_fusion = true;  // write the projected result from the last join
+  // A prepared plan: the captured launch sequence plus what the host needs
+  // to replay and complete it without re-planning.
   struct GraphEntry {
-    cudaGraphExec_t exec;
-    int kernels;
+    cudaGraphExec_t exec = nullptr;
+    int kernels = 0;
+    std::string image;  // query block bytes uploaded by the sequence's H2D
+    int n_epochs = 0;   // tile-scan launches (fresh epochs per replay)
+    int pack_stat = 0;
+    i64 pack_cap = 0;
+    u32* pack_out = nullptr;
+    bool fused = false;
+    i64 h2d = 0;
+    std::vector<int> kinds, arities;
   };
   std::unordered_map<std::string, GraphEntry> graphs;
 };
@@ -1402,6 +1412,7 @@ struct ExecState {
   bool allow_fuse = true;
   bool timing = false;
   std::string plan_key;
+  std::vector<int> kinds, arities;  // per step (report, budget checks)
 };
 
 // Plan the query and enqueue its whole launch sequence (as a CUDA graph
@@ -1425,6 +1436,52 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   std::string& last_key = S.plan_key;
   kernels = 0;
   QueryBlock* hb = c->h_block;
+  cudaStream_t st = c->stream;
+
+  // Plan key: everything the launch sequence's parameters derive from.
+  std::string key;
+  {
+    auto put = [&key](const void* p, size_t b) { key.append(reinterpret_cast<const char*>(p), b); };
+    put(steps, sizeof(gsm_pattern) * (size_t)n);
+    put(proj, sizeof(int32_t) * (size_t)n_proj);
+    const i64 scal[] = {n, n_proj, distinct, allow_fuse, timing, budget, part, parts};
+    put(scal, sizeof scal);
+  }
+  {
+    // D2H size guess: the last result size of this plan rounded up to a power
+    // of two (>= 4 KiB), else 64 KiB; never more than the staging buffer.
+    auto lb = c->last_bytes.find(key);
+    size_t g = 65536;
+    if (lb != c->last_bytes.end()) {
+      g = 4096;
+      while (g < lb->second) g <<= 1;
+    }
+    c->guess = std::min(g, c->stage_bytes);
+  }
+  last_key = key;
+  key.append(reinterpret_cast<const char*>(&c->guess), sizeof c->guess);
+
+  // Prepared plan: replay the captured launch sequence with the saved
+  // query-block image and fresh epochs — no re-planning on the host.
+  if (c->use_graphs) {
+    auto it = c->graphs.find(key);
+    if (it != c->graphs.end()) {
+      const auto& P = it->second;
+      memcpy(hb, P.image.data(), P.image.size());
+      for (int i = 0; i < P.n_epochs; i++) hb->epochs[i] = next_epoch(c);
+      pack_stat = P.pack_stat;
+      pack_cap = P.pack_cap;
+      pack_out = P.pack_out;
+      S.fused = P.fused;
+      kernels = P.kernels;
+      h2d = P.h2d;
+      S.kinds = P.kinds;
+      S.arities = P.arities;
+      GSM_CUDA(cudaGraphLaunch(P.exec, st));
+      count_launch(kernels);
+      return GSM_OK;
+    }
+  }
   ex.c = c;
   ex.steps = steps;
   ex.n = n;
@@ -1716,17 +1773,14 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
 
   // ---- per-launch epochs: data in the query block, so a captured graph
   //      replays with fresh epochs and unchanged kernel parameters ----
-  {
-    int slot = 0;
-    for (auto& L : launches)
-      if (L.kind == S_EXPAND || L.kind == S_FILTER || L.kind == S_GROUP)
-        hb->epochs[slot++] = next_epoch(c);
-  }
+  int n_epoch_slots = 0;
+  for (auto& L : launches)
+    if (L.kind == S_EXPAND || L.kind == S_FILTER || L.kind == S_GROUP)
+      hb->epochs[n_epoch_slots++] = next_epoch(c);
   ProjArgs pa{};
   for (int j = 0; j < n_proj; j++) pa.col[j] = pj_idx[j];
   const size_t used = offsetof(QueryBlock, tables) + sizeof(DTable) * (size_t)ex.ntables;
   h2d = (i64)used;
-  cudaStream_t st = c->stream;
 
   // The whole query as one stream-ordered sequence: H2D of the query block,
   // the kernels, D2H of the step counters.  Nothing here writes host memory.
@@ -1843,35 +1897,15 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     return GSM_OK;
   };
 
-  // Plan key: everything the launch sequence's parameters derive from.
-  std::string key;
-  {
-    auto put = [&key](const void* p, size_t b) { key.append(reinterpret_cast<const char*>(p), b); };
-    put(steps, sizeof(gsm_pattern) * (size_t)n);
-    put(proj, sizeof(int32_t) * (size_t)n_proj);
-    const i64 scal[] = {n, n_proj, distinct, allow_fuse, timing, budget, part, parts};
-    put(scal, sizeof scal);
+  S.kinds.resize(n);
+  S.arities.resize(n);
+  for (int q = 0; q < n; q++) {
+    S.kinds[q] = (int)ex.plan[q].kind;
+    S.arities[q] = (int)ex.plan[q].schema.size();
   }
-  {
-    // D2H size guess: the last result size of this plan rounded up to a power
-    // of two (>= 4 KiB), else 64 KiB; never more than the staging buffer.
-    auto lb = c->last_bytes.find(key);
-    size_t g = 65536;
-    if (lb != c->last_bytes.end()) {
-      g = 4096;
-      while (g < lb->second) g <<= 1;
-    }
-    c->guess = std::min(g, c->stage_bytes);
-  }
-  last_key = key;
   if (c->use_graphs) {
-    key.append(reinterpret_cast<const char*>(&c->guess), sizeof c->guess);
     cudaGraphExec_t ge = nullptr;
-    auto it = c->graphs.find(key);
-    if (it != c->graphs.end()) {
-      ge = it->second.exec;
-      kernels = it->second.kernels;
-    } else {
+    {
       if (c->graphs.size() >= 1024) ctx_clear_graphs(c);
       GSM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       capturing = true;
@@ -1887,7 +1921,19 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       ce = cudaGraphInstantiate(&ge, g, 0);
       cudaGraphDestroy(g);
       if (ce != cudaSuccess) return cuda_error(ce, "cudaGraphInstantiate");
-      c->graphs.emplace(key, gsm_context::GraphEntry{ge, kernels});
+      gsm_context::GraphEntry P;
+      P.exec = ge;
+      P.kernels = kernels;
+      P.image.assign(reinterpret_cast<const char*>(hb), reinterpret_cast<const char*>(hb) + used);
+      P.n_epochs = n_epoch_slots;
+      P.pack_stat = pack_stat;
+      P.pack_cap = pack_cap;
+      P.pack_out = pack_out;
+      P.fused = S.fused;
+      P.h2d = h2d;
+      P.kinds = S.kinds;
+      P.arities = S.arities;
+      c->graphs.emplace(key, std::move(P));
     }
     GSM_CUDA(cudaGraphLaunch(ge, st));
   } else {
@@ -1932,7 +1978,6 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
   const int64_t budget = qa.budget;
   const bool distinct = qa.distinct != 0, timing = S.timing;
   gsm_report* rep = qa.rep;
-  Exec& ex = S.ex;
   int& pack_stat = S.pack_stat;
   i64& pack_cap = S.pack_cap;
   u32*& pack_out = S.pack_out;
@@ -1955,7 +2000,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     bool ovf = false;
     for (int s = 1; s < n && !ovf; s++) {
       const StepStat& q = hb->stats[s];
-      StepKind k = ex.plan[s].kind;
+      StepKind k = (StepKind)S.kinds[s];
       char msg[256];
       if (k == S_CROSS || k == S_GATE) {
         i64 nl = q.e, nr = q.pad, tot = 0;
@@ -1979,7 +2024,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
       if (q.overflow) {
         ovf = true;
         need_rows = q.rows;
-        need_arity = (int)ex.plan[s].schema.size();
+        need_arity = S.arities[s];
       }
     }
     if (!ovf && hb->stats[pack_stat].overflow) {
@@ -2017,9 +2062,9 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
   const QueryBlock* hb = c->h_block;
   if (rep) {
     for (int s = 0; s < n; s++) {
-      StepKind k = ex.plan[s].kind;
+      StepKind k = (StepKind)S.kinds[s];
       if (rep->kind) rep->kind[s] = (int32_t)k;
-      if (rep->arity) rep->arity[s] = (int32_t)ex.plan[s].schema.size();
+      if (rep->arity) rep->arity[s] = (int32_t)S.arities[s];
       if (rep->rows) rep->rows[s] = hb->stats[s].rows;
       if (rep->prealloc_total)
         rep->prealloc_total[s] = (k == S_EXPAND || k == S_FILTER) ? hb->stats[s].e : 0;
