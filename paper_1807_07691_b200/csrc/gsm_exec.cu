@@ -186,7 +186,7 @@ __device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
 //   P::kAccumE                 accumulate e into st->e (filters)
 // ---------------------------------------------------------------------------
 template <class P>
-__global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts, ExportArgs xa) {
+__global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, ExportArgs xa) {
   __shared__ i64 s_pre[TS_TILE + 1];
   __shared__ u32 s_aux[TS_TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
@@ -288,8 +288,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tilescan(P p, TileSync ts, Expor
         continue;
       }
       if constexpr (P::kWarpEmit) {
-#pragma unroll 4
-        for (i64 j0 = 0; j0 < c; j0 += 32) p.emit_warp(s_in, base + r, aux, j0, c, pos);
+        p.emit_row_warp(s_in, base + r, aux, c, pos);
       } else {
         for (i64 j = lane; j < c; j += 4 * 32) {
 #pragma unroll
@@ -402,6 +401,53 @@ struct ExpandP {
 #pragma unroll 4
       for (int cc = 0; cc < a; cc++) out[(i64)cc * cap + g] = __ldg(s.col[cc] + r);
       out[(i64)a * cap + g] = nv;
+    }
+  }
+  // One warp writes the whole candidate run of a long row: U chunks of 32
+  // candidates are loaded before any of them is stored, so each warp keeps U
+  // coalesced loads in flight (memory-level parallelism for the hub rows).
+  __device__ void emit_row_warp(const DTable& s, i64 r, u32 aux, i64 c, i64 pos) const {
+    constexpr int U = 8;
+    const int lane = threadIdx.x & 31;
+    for (i64 j0 = 0; j0 < c; j0 += 32 * U) {
+      u32 v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const i64 j = j0 + 32 * u + lane;
+        v[u] = j < c ? __ldg(R.dst + aux + j) : 0u;
+      }
+      if (fz.stage) {
+#pragma unroll
+        for (int u = 0; u < U; u++)
+          if (j0 + 32 * u < c) emit_chunk_fused(s, r, v[u], j0 + 32 * u, c, pos);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const i64 j = j0 + 32 * u + lane;
+          if (j < c && pos + j < cap) {
+            const i64 g = pos + j;
+            for (int cc = 0; cc < a; cc++) out[(i64)cc * cap + g] = __ldg(s.col[cc] + r);
+            out[(i64)a * cap + g] = v[u];
+          }
+        }
+      }
+    }
+  }
+  // Fused row-major output of candidates [j0, j0+32) (value nv per lane).
+  __device__ void emit_chunk_fused(const DTable& s, i64 r, u32 nv, i64 j0, i64 c, i64 pos) const {
+    const int lane = threadIdx.x & 31;
+    const int k = fz.k;
+    const i64 rows = min((i64)32, c - j0);
+    const u32 lv = lane < a ? __ldg(s.col[lane] + r) : 0u;
+    const i64 base = pos + j0;
+    const int words = (int)rows * k;
+    for (int w0 = 0; w0 < words; w0 += 32) {
+      const int w = w0 + lane;
+      const int rr = w < words ? w / k : 0;
+      const int src = w < words ? fz.pj[w - rr * k] : 0;
+      const u32 v_left = __shfl_sync(0xffffffffu, lv, src < a ? src : 0);
+      const u32 v_new = __shfl_sync(0xffffffffu, nv, rr);
+      if (w < words && base + rr < fz.cap) fz.stage[base * k + w] = src < a ? v_left : v_new;
     }
   }
   __device__ void finish(i64 total) const {
@@ -551,7 +597,7 @@ struct GroupEmit {
   }
 };
 
-__global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts, ExportArgs xa) {
+__global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, ExportArgs xa) {
   __shared__ i64 s_pre[TS_TILE + 1];
   __shared__ u32 s_aux[TS_TILE];
   __shared__ u32 s_len[TS_TILE];
@@ -719,7 +765,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_group(GroupP p, TileSync ts, Exp
 // Drain the hub pieces queued by the preceding expand: blocks grab pieces
 // (CHUNK consecutive outputs of one row) until the queue is empty.
 template <class E>
-__global__ void __launch_bounds__(TS_THREADS) k_drain(E e, ChunkQueue q, ExportArgs xa) {
+__global__ void __launch_bounds__(TS_THREADS, 4) k_drain(E e, ChunkQueue q, ExportArgs xa) {
   __shared__ DTable s_in;
   __shared__ u32 s_idx;
   pdl_wait();
