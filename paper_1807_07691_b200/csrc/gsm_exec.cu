@@ -404,33 +404,100 @@ struct ExpandP {
     }
   }
   // One warp writes the whole candidate run of a long row: U chunks of 32
-  // candidates are loaded before any of them is stored, so each warp keeps U
-  // coalesced loads in flight (memory-level parallelism for the hub rows).
-  __device__ void emit_row_warp(const DTable& s, i64 r, u32 aux, i64 c, i64 pos) const {
+  // candidates are loaded before any of them is stored (U loads in flight
+  // per warp).  For small left arities the row's left values are hoisted into
+  // registers and the columns are streamed through precomputed pointers, so a
+  // chunk costs little more than its a+1 coalesced stores.
+  template <int A>
+  __device__ void row_warp_cols(const DTable& s, i64 r, u32 aux, i64 c, i64 pos) const {
     constexpr int U = 8;
     const int lane = threadIdx.x & 31;
+    u32 lv[A > 0 ? A : 1];
+#pragma unroll
+    for (int cc = 0; cc < A; cc++) lv[cc] = __ldg(s.col[cc] + r);
+    const u32* src = R.dst + aux;
+    u32* ob = out + pos;  // column cc of output slot pos + j is ob[cc * cap + j]
+    const i64 lim = min(c, cap - pos);
     for (i64 j0 = 0; j0 < c; j0 += 32 * U) {
       u32 v[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const i64 j = j0 + 32 * u + lane;
-        v[u] = j < c ? __ldg(R.dst + aux + j) : 0u;
+        v[u] = j < c ? __ldg(src + j) : 0u;
       }
-      if (fz.stage) {
 #pragma unroll
-        for (int u = 0; u < U; u++)
-          if (j0 + 32 * u < c) emit_chunk_fused(s, r, v[u], j0 + 32 * u, c, pos);
-      } else {
+      for (int u = 0; u < U; u++) {
+        const i64 j = j0 + 32 * u + lane;
+        if (j < lim) {
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-          const i64 j = j0 + 32 * u + lane;
-          if (j < c && pos + j < cap) {
-            const i64 g = pos + j;
-            for (int cc = 0; cc < a; cc++) out[(i64)cc * cap + g] = __ldg(s.col[cc] + r);
-            out[(i64)a * cap + g] = v[u];
-          }
+          for (int cc = 0; cc < A; cc++) ob[(i64)cc * cap + j] = lv[cc];
+          ob[(i64)A * cap + j] = v[u];
         }
       }
+    }
+  }
+  template <int K>
+  __device__ void row_warp_fused(const DTable& s, i64 r, u32 aux, i64 c, i64 pos) const {
+    // row-major, K words per row: lane l of a 32-row chunk writes words
+    // l, l+32, ..., (K-1)*32+l of the chunk; word w is column w % K of row w / K
+    const int lane = threadIdx.x & 31;
+    u32 cv[K];      // value of each projected column when it is a left column
+    bool isnew[K];  // projected column is the expanded one
+#pragma unroll
+    for (int x = 0; x < K; x++) {
+      const int src = fz.pj[x];
+      isnew[x] = src >= a;
+      cv[x] = src < a ? __ldg(s.col[src] + r) : 0u;
+    }
+    const u32* dsrc = R.dst + aux;
+    for (i64 j0 = 0; j0 < c; j0 += 32) {
+      const i64 j = j0 + lane;
+      const u32 nv = j < c ? __ldg(dsrc + j) : 0u;
+      const i64 base = pos + j0;
+      const int rows = (int)min((i64)32, c - j0);
+#pragma unroll
+      for (int x = 0; x < K; x++) {
+        const int w = x * 32 + lane;
+        const int rr = w / K, cc = w - rr * K;
+        u32 val = cv[0];
+#pragma unroll
+        for (int y = 1; y < K; y++) val = cc == y ? cv[y] : val;
+        bool nw = isnew[0];
+#pragma unroll
+        for (int y = 1; y < K; y++) nw = cc == y ? isnew[y] : nw;
+        const u32 nvr = __shfl_sync(0xffffffffu, nv, rr);
+        if (rr < rows && base + rr < fz.cap) fz.stage[base * K + w] = nw ? nvr : val;
+      }
+    }
+  }
+  __device__ void emit_row_warp(const DTable& s, i64 r, u32 aux, i64 c, i64 pos) const {
+    if (fz.stage) {
+      switch (fz.k) {
+        case 1: row_warp_fused<1>(s, r, aux, c, pos); return;
+        case 2: row_warp_fused<2>(s, r, aux, c, pos); return;
+        case 3: row_warp_fused<3>(s, r, aux, c, pos); return;
+        case 4: row_warp_fused<4>(s, r, aux, c, pos); return;
+        default: break;
+      }
+      for (i64 j0 = 0; j0 < c; j0 += 32) {
+        const i64 j = j0 + (threadIdx.x & 31);
+        emit_chunk_fused(s, r, j < c ? __ldg(R.dst + aux + j) : 0u, j0, c, pos);
+      }
+      return;
+    }
+    switch (a) {
+      case 1: row_warp_cols<1>(s, r, aux, c, pos); return;
+      case 2: row_warp_cols<2>(s, r, aux, c, pos); return;
+      case 3: row_warp_cols<3>(s, r, aux, c, pos); return;
+      case 4: row_warp_cols<4>(s, r, aux, c, pos); return;
+      default: break;
+    }
+    const int lane = threadIdx.x & 31;  // generic arity
+    for (i64 j = lane; j < c; j += 32) {
+      if (pos + j >= cap) break;
+      const i64 g = pos + j;
+      for (int cc = 0; cc < a; cc++) out[(i64)cc * cap + g] = __ldg(s.col[cc] + r);
+      out[(i64)a * cap + g] = __ldg(R.dst + aux + j);
     }
   }
   // Fused row-major output of candidates [j0, j0+32) (value nv per lane).
@@ -779,10 +846,11 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_drain(E e, ChunkQueue q, Expo
     const u32 idx = s_idx;
     if (idx >= n) break;
     const Chunk ch = q.items[idx];
-    if constexpr (E::kWarpEmit) {
-      const i64 c_end = (i64)ch.j0 + ch.len, pos0 = ch.pos - (i64)ch.j0;
-      for (u32 j = (threadIdx.x >> 5) * 32; j < ch.len; j += TS_THREADS)
-        e.emit_warp(s_in, ch.r, ch.aux, (i64)ch.j0 + j, c_end, pos0);
+    if constexpr (E::kWarpEmit) {  // each warp writes a 128-candidate slice of the piece
+      constexpr u32 SL = CHUNK / (TS_THREADS / 32);
+      const u32 w0 = (threadIdx.x >> 5) * SL;
+      if (w0 < ch.len)
+        e.emit_row_warp(s_in, ch.r, ch.aux + ch.j0 + w0, (i64)min(SL, ch.len - w0), ch.pos + w0);
     } else {
       for (u32 j = threadIdx.x; j < ch.len; j += TS_THREADS)
         e.emit(s_in, ch.r, ch.aux, (i64)ch.j0 + j, ch.pos + j);
