@@ -262,6 +262,15 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     }
     __syncthreads();
     const i64 gbase = s_base;
+    // Tiles whose rows average < WARP_ROW candidates: staged, coalesced writes.
+    if constexpr (P::kWindow) {
+      if (total <= (i64)WARP_ROW * TS_TILE &&
+          p.scatter_window(s_in, base, s_pre, s_aux, total, gbase)) {
+        if ((i64)t == ntiles - 1 && tid == 0) p.finish(gbase + total);
+        __syncthreads();
+        continue;
+      }
+    }
     // Scatter (TS_ITEMS == 1: thread tid owns tile row tid).  Rows with fewer
     // than WARP_ROW candidates are written by their own thread (consecutive
     // rows are adjacent in the output, so a warp's stores stay dense); longer
@@ -340,6 +349,7 @@ struct ExpandP {
   static constexpr bool kAccumE = false;
   static constexpr bool kDefer = true;
   static constexpr bool kWarpEmit = true;
+  static constexpr bool kWindow = true;
   ChunkQueue dq;
   const DTable* L;
   Orient R;
@@ -500,6 +510,68 @@ struct ExpandP {
       out[(i64)a * cap + g] = __ldg(R.dst + aux + j);
     }
   }
+  // Tiles of short rows: stage the tile's output in shared-memory windows of
+  // WIN slots, then write each window with coalesced stores (thread-per-row
+  // stores of short runs would scatter).  Each thread fills 8 consecutive
+  // slots (one binary search, then a merge-path walk); slots are XOR-swizzled
+  // so neither the fill nor the flush has bank conflicts.  Returns false when
+  // the output is too wide for the window (caller uses the tiered path).
+  static constexpr int WIN = 2048, WIN_W = 4;
+  __device__ static int swz(int sl) { return sl ^ ((sl >> 5) & 7); }
+  __device__ bool scatter_window(const DTable& s, i64 base, const i64* pre, const u32* auxv,
+                                 i64 total, i64 gbase) const {
+    const int width = fz.stage ? fz.k : a + 1;
+    if (width > WIN_W || width < 1) return false;
+    __shared__ u32 win[WIN_W * WIN];
+    const int tid = threadIdx.x;
+    for (i64 w = 0; w < total; w += WIN) {
+      const int nw = (int)min((i64)WIN, total - w);
+      const int s0 = 8 * tid;
+      if (s0 < nw) {
+        const i64 slot0 = w + s0;
+        int lo = 0, hi = TS_TILE;  // pre[lo] <= slot0 < pre[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (pre[mid] <= slot0) lo = mid; else hi = mid;
+        }
+        int r = lo;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const int sl = s0 + i;
+          if (sl < nw) {
+            const i64 slot = w + sl;
+            while (slot >= pre[r + 1]) r++;
+            const u32 nv = __ldg(R.dst + auxv[r] + (slot - pre[r]));
+            const int q = swz(sl);
+            if (fz.stage) {
+              for (int x = 0; x < width; x++) {
+                const int src = fz.pj[x];
+                win[x * WIN + q] = src < a ? __ldg(s.col[src] + base + r) : nv;
+              }
+            } else {
+              for (int cc = 0; cc < a; cc++) win[cc * WIN + q] = __ldg(s.col[cc] + base + r);
+              win[a * WIN + q] = nv;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      const i64 g0 = gbase + w;
+      if (fz.stage) {  // row-major: word idx = row * width + x
+        const int words = nw * width;
+        for (int idx = tid; idx < words; idx += TS_THREADS) {
+          const int row = idx / width, x = idx - row * width;
+          if (g0 + row < fz.cap) fz.stage[g0 * width + idx] = win[x * WIN + swz(row)];
+        }
+      } else {
+        for (int cc = 0; cc < width; cc++)
+          for (int i = tid; i < nw; i += TS_THREADS)
+            if (g0 + i < cap) out[(i64)cc * cap + g0 + i] = win[cc * WIN + swz(i)];
+      }
+      __syncthreads();
+    }
+    return true;
+  }
   // Fused row-major output of candidates [j0, j0+32) (value nv per lane).
   __device__ void emit_chunk_fused(const DTable& s, i64 r, u32 nv, i64 j0, i64 c, i64 pos) const {
     const int lane = threadIdx.x & 31;
@@ -532,6 +604,7 @@ struct ExpandP {
 //   F_SELF  (?x p ?x):              (L[li], L[li]) in M       E = kept rows
 enum { F_PAIR = 0, F_CONST = 1, F_SELF = 2 };
 struct FilterP {
+  static constexpr bool kWindow = false;
   static constexpr bool kWarpEmit = false;
   static constexpr bool kAccumE = true;
   static constexpr bool kDefer = false;
@@ -863,6 +936,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_drain(E e, ChunkQueue q, Expo
 // DISTINCT over packed row-major rows: a row survives iff it wins the CAS
 // into an open-addressing set keyed by the whole tuple (executor.py:360-367).
 struct DistinctP {
+  static constexpr bool kWindow = false;
   static constexpr bool kWarpEmit = false;
   static constexpr bool kAccumE = false;
   static constexpr bool kDefer = false;
@@ -1100,6 +1174,7 @@ __global__ void k_row_counts(const u32* __restrict__ Lk, i64 n, Orient X, i64* _
 // index) table: keep a candidate iff every further shared variable agrees
 // (executor.py:186-191); emit left ++ right[rcols] row-major.
 struct TFilterP {
+  static constexpr bool kWindow = false;
   static constexpr bool kWarpEmit = false;
   static constexpr bool kAccumE = false;
   static constexpr bool kDefer = false;
