@@ -21,6 +21,8 @@
  * Generators
  *   lubm      LUBM/UBA-style university data (universities -> departments ->
  *             faculty/students/courses/publications/research groups).
+ *   watdiv    WatDiv-style e-commerce/social data (users, products, reviews,
+ *             offers, retailers, websites, purchases), Zipf-skewed links.
  *   powerlaw  bit-exact restatement of generate.py (generate.py:17-64):
  *             CPython's MT19937 + random.choices(cum_weights=...) over a Zipf
  *             predicate distribution and i^-NODE_SKEW endpoint weights.
@@ -470,6 +472,190 @@ static void gen_lubm(int univs, int pool) {
 }
 
 /* ------------------------------------------------------------------ */
+/* WatDiv-style generator (configs[3]).  Entity model after the WatDiv  */
+/* benchmark's schema: users, products, reviews, offers, retailers,    */
+/* websites, purchases, cities/countries, genres, topics, ...  Entity  */
+/* counts scale with --scale (scale 1000 ~ 100M triples); link         */
+/* targets are Zipf-skewed so popular products/users become hubs.      */
+/* ------------------------------------------------------------------ */
+#define WSDBM "http://db.uwaterloo.ca/~galuc/wsdbm/"
+#define SORG "http://schema.org/"
+#define GR "http://purl.org/goodrelations/"
+#define REV "http://purl.org/stuff/rev#"
+#define OG "http://ogp.me/ns#"
+#define FOAF "http://xmlns.com/foaf/"
+#define DC "http://purl.org/dc/terms/"
+#define GN "http://www.geonames.org/ontology#"
+#define MO "http://purl.org/ontology/mo/"
+
+/* Zipf(s) sample in [0, n) by inverse CDF on a precomputed table. */
+typedef struct { double* cum; uint32_t n; } Zipf;
+static Zipf zipf_make(uint32_t n, double s) {
+  Zipf z;
+  z.n = n;
+  z.cum = xmalloc(sizeof(double) * n);
+  double acc = 0;
+  for (uint32_t i = 0; i < n; i++) { acc += pow((double)(i + 1), -s); z.cum[i] = acc; }
+  return z;
+}
+static uint32_t zipf_draw(const Zipf* z) {
+  double x = (double)(rnext() >> 11) * (1.0 / 9007199254740992.0) * z->cum[z->n - 1];
+  uint32_t lo = 0, hi = z->n - 1;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) / 2;
+    if (x < z->cum[mid]) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+static int rchance(double p) { return (double)(rnext() >> 11) * (1.0 / 9007199254740992.0) < p; }
+
+static void gen_watdiv(int scale) {
+  const uint32_t nU = 3000u * scale, nP = 750u * scale, nR = 4500u * scale, nO = 2700u * scale;
+  const uint32_t nRet = 36u * scale, nW = 150u * scale, nPur = 4500u * scale;
+  const uint32_t nCity = 240, nCountry = 25, nGenre = 21, nSub = 145, nCat = 15, nTopic = 250;
+  const uint32_t nLang = 25, nRole = 3, nAge = 9;
+  Zipf zU = zipf_make(nU, 0.8), zP = zipf_make(nP, 0.8), zW = zipf_make(nW, 0.7);
+  Zipf zTopic = zipf_make(nTopic, 1.0), zSub = zipf_make(nSub, 0.9), zCity = zipf_make(nCity, 1.0);
+  char e[256], x[256], lit[256];
+#define ENT(buf, kind, i) snprintf(buf, sizeof buf, WSDBM "%s%u", kind, (unsigned)(i))
+  for (uint32_t i = 0; i < nCity; i++) {
+    ENT(e, "City", i);
+    ENT(x, "Country", i % nCountry);
+    T(e, GN "parentCountry", x);
+  }
+  for (uint32_t i = 0; i < nSub; i++) {
+    ENT(e, "SubGenre", i);
+    ENT(x, "Genre", i % nGenre);
+    T(e, OG "tag", x);
+    T(e, RDF_TYPE, WSDBM "SubGenre");
+  }
+  for (uint32_t i = 0; i < nW; i++) {
+    ENT(e, "Website", i);
+    snprintf(lit, sizeof lit, "\"http://www.website%u.com/\"", i);
+    T(e, SORG "url", lit);
+    snprintf(lit, sizeof lit, "\"%u\"", (unsigned)rrange(1, 100000));
+    T(e, WSDBM "hits", lit);
+    ENT(x, "Language", rrange(0, nLang - 1));
+    T(e, SORG "language", x);
+  }
+  for (uint32_t i = 0; i < nP; i++) {
+    ENT(e, "Product", i);
+    ENT(x, "ProductCategory", rrange(0, nCat - 1));
+    T(e, RDF_TYPE, x);
+    snprintf(lit, sizeof lit, "\"caption %u\"", i);
+    if (rchance(0.5)) T(e, SORG "caption", lit);
+    snprintf(lit, sizeof lit, "\"text %u\"", i);
+    if (rchance(0.3)) T(e, SORG "text", lit);
+    snprintf(lit, sizeof lit, "\"description %u\"", i);
+    if (rchance(0.7)) T(e, SORG "description", lit);
+    snprintf(lit, sizeof lit, "\"keywords %u\"", i % 1000);
+    if (rchance(0.3)) T(e, SORG "keywords", lit);
+    snprintf(lit, sizeof lit, "\"title %u\"", i);
+    T(e, OG "title", lit);
+    int ng = rrange(1, 3);
+    for (int g = 0; g < ng; g++) { ENT(x, "SubGenre", zipf_draw(&zSub)); T(e, WSDBM "hasGenre", x); }
+    int nt = rrange(0, 4);
+    for (int g = 0; g < nt; g++) { ENT(x, "Topic", zipf_draw(&zTopic)); T(e, OG "tag", x); }
+    if (rchance(0.4)) { ENT(x, "Website", zipf_draw(&zW)); T(e, FOAF "homepage", x); }
+    snprintf(lit, sizeof lit, "\"%d\"", rrange(1, 5));
+    if (rchance(0.3)) T(e, SORG "contentRating", lit);
+    snprintf(lit, sizeof lit, "\"%dMB\"", rrange(1, 500));
+    if (rchance(0.3)) T(e, SORG "contentSize", lit);
+    if (rchance(0.2)) { ENT(x, "Language", rrange(0, nLang - 1)); T(e, SORG "language", x); }
+    if (rchance(0.1)) { ENT(x, "Retailer", rrange(0, nRet - 1)); T(e, SORG "publisher", x); }
+    if (rchance(0.1)) { snprintf(lit, sizeof lit, "\"trailer %u\"", i); T(e, SORG "trailer", lit); }
+    if (rchance(0.1)) { ENT(x, "User", zipf_draw(&zU)); T(e, SORG "director", x); }
+    if (rchance(0.2)) { ENT(x, "User", zipf_draw(&zU)); T(e, SORG "actor", x); }
+    if (rchance(0.1)) { ENT(x, "User", zipf_draw(&zU)); T(x, MO "artist", e); }
+    if (rchance(0.05)) { ENT(x, "User", zipf_draw(&zU)); T(e, MO "conductor", x); }
+  }
+  for (uint32_t i = 0; i < nR; i++) {
+    ENT(e, "Review", i);
+    ENT(x, "Product", zipf_draw(&zP));
+    T(x, REV "hasReview", e);
+    ENT(x, "User", zipf_draw(&zU));
+    T(e, REV "reviewer", x);
+    snprintf(lit, sizeof lit, "\"%d\"", rrange(1, 10));
+    T(e, REV "rating", lit);
+    snprintf(lit, sizeof lit, "\"review title %u\"", i % 5000);
+    if (rchance(0.5)) T(e, REV "title", lit);
+    snprintf(lit, sizeof lit, "\"review text %u\"", i);
+    if (rchance(0.5)) T(e, REV "text", lit);
+    snprintf(lit, sizeof lit, "\"%d\"", rrange(0, 100));
+    if (rchance(0.3)) T(e, REV "totalVotes", lit);
+  }
+  for (uint32_t i = 0; i < nRet; i++) {
+    ENT(e, "Retailer", i);
+    snprintf(lit, sizeof lit, "\"Retailer %u Inc.\"", i);
+    T(e, SORG "legalName", lit);
+    ENT(x, "User", zipf_draw(&zU));
+    T(e, SORG "employee", x);
+  }
+  for (uint32_t i = 0; i < nO; i++) {
+    ENT(e, "Offer", i);
+    ENT(x, "Retailer", rrange(0, nRet - 1));
+    T(x, GR "offers", e);
+    ENT(x, "Product", zipf_draw(&zP));
+    T(e, GR "includes", x);
+    snprintf(lit, sizeof lit, "\"%d.%02d\"", rrange(1, 500), rrange(0, 99));
+    T(e, GR "price", lit);
+    snprintf(lit, sizeof lit, "\"SN%u\"", i);
+    T(e, GR "serialNumber", lit);
+    snprintf(lit, sizeof lit, "\"2019-%02d-%02d\"", rrange(1, 12), rrange(1, 28));
+    T(e, GR "validFrom", lit);
+    snprintf(lit, sizeof lit, "\"2020-%02d-%02d\"", rrange(1, 12), rrange(1, 28));
+    T(e, GR "validThrough", lit);
+    snprintf(lit, sizeof lit, "\"%d\"", rrange(1, 50));
+    T(e, SORG "eligibleQuantity", lit);
+    ENT(x, "Country", rrange(0, nCountry - 1));
+    T(e, SORG "eligibleRegion", x);
+    snprintf(lit, sizeof lit, "\"2020-%02d-%02d\"", rrange(1, 12), rrange(1, 28));
+    T(e, SORG "priceValidUntil", lit);
+  }
+  for (uint32_t i = 0; i < nU; i++) {
+    ENT(e, "User", i);
+    snprintf(lit, sizeof lit, "\"user%u@example.org\"", i);
+    T(e, SORG "email", lit);
+    ENT(x, "Role", rrange(0, nRole - 1));
+    T(e, RDF_TYPE, x);
+    ENT(x, "Gender", rrange(0, 1));
+    if (rchance(0.6)) T(e, WSDBM "gender", x);
+    ENT(x, "AgeGroup", rrange(0, nAge - 1));
+    if (rchance(0.5)) T(e, FOAF "age", x);
+    snprintf(lit, sizeof lit, "\"family%u\"", i % 2000);
+    if (rchance(0.7)) T(e, FOAF "familyName", lit);
+    snprintf(lit, sizeof lit, "\"given%u\"", i % 1000);
+    if (rchance(0.7)) T(e, FOAF "givenName", lit);
+    ENT(x, "Country", zipf_draw(&zCity) % nCountry);
+    if (rchance(0.5)) T(e, SORG "nationality", x);
+    ENT(x, "City", zipf_draw(&zCity));
+    if (rchance(0.4)) T(e, DC "Location", x);
+    snprintf(lit, sizeof lit, "\"job %d\"", rrange(0, 200));
+    if (rchance(0.05)) T(e, SORG "jobTitle", lit);
+    if (rchance(0.1)) { ENT(x, "Website", zipf_draw(&zW)); T(e, FOAF "homepage", x); }
+    int nf = rchance(0.4) ? rrange(1, 20) : 0;
+    for (int k = 0; k < nf; k++) { ENT(x, "User", zipf_draw(&zU)); T(e, WSDBM "follows", x); }
+    int nfr = rchance(0.4) ? rrange(1, 10) : 0;
+    for (int k = 0; k < nfr; k++) { ENT(x, "User", zipf_draw(&zU)); T(e, WSDBM "friendOf", x); }
+    int nl = rchance(0.25) ? rrange(1, 5) : 0;
+    for (int k = 0; k < nl; k++) { ENT(x, "Product", zipf_draw(&zP)); T(e, WSDBM "likes", x); }
+    int ns = rchance(0.1) ? rrange(1, 3) : 0;
+    for (int k = 0; k < ns; k++) { ENT(x, "Website", zipf_draw(&zW)); T(e, WSDBM "subscribes", x); }
+  }
+  for (uint32_t i = 0; i < nPur; i++) {
+    ENT(e, "Purchase", i);
+    ENT(x, "User", zipf_draw(&zU));
+    T(x, WSDBM "makesPurchase", e);
+    ENT(x, "Product", zipf_draw(&zP));
+    T(e, WSDBM "purchaseFor", x);
+    snprintf(lit, sizeof lit, "\"2019-%02d-%02d\"", rrange(1, 12), rrange(1, 28));
+    T(e, WSDBM "purchaseDate", lit);
+  }
+#undef ENT
+  free(zU.cum); free(zP.cum); free(zW.cum); free(zTopic.cum); free(zSub.cum); free(zCity.cum);
+}
+
+/* ------------------------------------------------------------------ */
 /* generate.py restatement (power-law)                                */
 /* CPython MT19937 + random.choices(cum_weights=...), bit-exact.      */
 /* ------------------------------------------------------------------ */
@@ -596,6 +782,7 @@ static void usage(void) {
   fprintf(stderr,
           "usage:\n"
           "  gsmgen lubm --univ U [--seed S] [--pool P] --out DIR [--nt FILE]\n"
+          "  gsmgen watdiv --scale F [--seed S] --out DIR [--nt FILE]\n"
           "  gsmgen powerlaw --triples T --predicates P [--zipf Z] [--seed S]\n"
           "                  [--nodes N] [--node-skew X] --out DIR [--nt FILE]\n");
   exit(1);
@@ -605,7 +792,7 @@ int main(int argc, char** argv) {
   if (argc < 2) usage();
   const char* mode = argv[1];
   const char *out = NULL, *nt = NULL;
-  long long univ = 1, seed = 0, pool = 0, triples = 0, predicates = 0, nodes = 0;
+  long long univ = 1, seed = 0, pool = 0, triples = 0, predicates = 0, nodes = 0, scale = 1;
   double zipf = 1.0, node_skew = 0.5;
   for (int i = 2; i < argc; i++) {
     const char* a = argv[i];
@@ -614,6 +801,7 @@ int main(int argc, char** argv) {
     if (!strcmp(a, "--out")) out = v;
     else if (!strcmp(a, "--nt")) nt = v;
     else if (!strcmp(a, "--univ")) univ = atoll(v);
+    else if (!strcmp(a, "--scale")) scale = atoll(v);
     else if (!strcmp(a, "--seed")) seed = atoll(v);
     else if (!strcmp(a, "--pool")) pool = atoll(v);
     else if (!strcmp(a, "--triples")) triples = atoll(v);
@@ -636,6 +824,10 @@ int main(int argc, char** argv) {
     g_rng = (uint64_t)seed * 0x2545F4914F6CDD1DULL + 0x1234567ULL;
     if (pool <= 0) pool = univ > 1000 ? univ : 1000;
     gen_lubm((int)univ, (int)pool);
+  } else if (!strcmp(mode, "watdiv")) {
+    if (scale < 1) die("--scale must be >= 1");
+    g_rng = (uint64_t)seed * 0x9E3779B97F4A7C15ULL + 0xABCDEFULL;
+    gen_watdiv((int)scale);
   } else if (!strcmp(mode, "powerlaw")) {
     if (triples < 1 || predicates < 1) die("--triples and --predicates must be >= 1");
     if (seed < 0) seed = -seed;

@@ -47,6 +47,7 @@ def _check_invariants(d):
     ("lubm", ["--univ", "1", "--seed", "0"]),
     ("lubm", ["--univ", "2", "--seed", "5"]),
     ("powerlaw", ["--triples", "5000", "--predicates", "7", "--seed", "11"]),
+    ("watdiv", ["--scale", "1", "--seed", "2"]),
 ])
 def test_generated_store_invariants(tmp_path, kind, args):
     d = tmp_path / "s"
@@ -66,6 +67,7 @@ def test_lubm_deterministic(tmp_path):
 @pytest.mark.parametrize("kind,args", [
     ("lubm", ["--univ", "1", "--seed", "0"]),
     ("powerlaw", ["--triples", "20000", "--predicates", "6", "--seed", "3"]),
+    ("watdiv", ["--scale", "1", "--seed", "0"]),
 ])
 def test_byte_identical_to_reference_build(tmp_path, kind, args):
     mine, ref = tmp_path / "mine", tmp_path / "ref"

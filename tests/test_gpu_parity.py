@@ -128,6 +128,14 @@ def test_lubm_vs_oracle(univ, store_factory):
         _oracle_compare(store, text)
 
 
+def test_watdiv_vs_oracle(store_factory):
+    """WatDiv-style store (configs[3] model), the 20 L/S/F/C templates."""
+    store = g.load(store_factory("watdiv", scale=5, seed=1))
+    qdir = GOLDEN.parents[1] / "datagen" / "queries" / "watdiv"
+    for f in sorted(qdir.glob("*.rq")):
+        _oracle_compare(store, f.read_text(), row_budget=1 << 62)
+
+
 def test_partition_union_is_whole(store_factory):
     store = g.load(store_factory("lubm", univ=2, seed=1))
     for name, text in lubm_queries():

@@ -89,3 +89,28 @@ def test_fingerprint_array_matches_scalar():
     rows = [(1, 2, 3), (4, 5, 6), (1, 2, 3), (7, 8, 9)]
     assert orc.fingerprint(rows) == orc.fingerprint_array(np.array(rows))
     assert orc.fingerprint([]) == orc.fingerprint_array(np.zeros((0, 3)))
+
+
+def test_watdiv_oracle_matches_reference(store_factory):
+    """WatDiv-style store + the 20 L/S/F/C templates: the C oracle equals the
+    reference executor row for row (skipped without the reference install)."""
+    gsmat = pytest.importorskip("gsmat")
+    from gsmat import executor, planner, qparser, storage
+
+    from conftest import REPO
+
+    d = store_factory("watdiv", scale=2, seed=0)
+    host = HostStore(d)
+    ref = storage.load(d)
+    prep = orc.PreparedStore(host.matrices)
+    for f in sorted((REPO / "datagen" / "queries" / "watdiv").glob("*.rq")):
+        text = f.read_text()
+        q, plan = plan_for(host, text)
+        rows, srows, spre = orc.run(prep, [s.pattern for s in plan.steps], q.projection, q.distinct)
+        rq = qparser.bind_constants(qparser.parse_query(text), ref.dictionary)
+        rp = planner.make_plan(rq, ref.stats)
+        rep = executor.ExecutionReport()
+        res = executor.execute(rq, rp, ref, row_budget=1 << 62, report=rep)
+        assert rows == res.rows, f.stem
+        assert srows == [s.rows for s in rep.steps], f.stem
+        assert spre == [s.prealloc_total for s in rep.steps], f.stem

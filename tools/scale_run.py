@@ -18,6 +18,7 @@ Row budget is 2^62 in both engines.  One JSON line per query,
 then a summary line.  Usage:
     python tools/scale_run.py --univ 1000 [--reps 5] [--skip-oracle-above 400000000]
     python tools/scale_run.py --kind powerlaw --triples 200000000 --predicates 40
+    python tools/scale_run.py --kind watdiv --scale 1000      (configs[3], ~104M triples)
 """
 from __future__ import annotations
 
@@ -37,7 +38,8 @@ sys.path.insert(0, str(REPO))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--kind", choices=["lubm", "powerlaw"], default="lubm")
+    ap.add_argument("--kind", choices=["lubm", "powerlaw", "watdiv"], default="lubm")
+    ap.add_argument("--scale", type=int, default=1000, help="watdiv scale (1000 ~ 100M triples)")
     ap.add_argument("--univ", type=int, default=1000)
     ap.add_argument("--triples", type=int, default=100_000_000)
     ap.add_argument("--predicates", type=int, default=40)
@@ -63,6 +65,8 @@ def main():
                "--out", store_dir]
         if args.kind == "lubm":
             gen += ["--univ", str(args.univ)]
+        elif args.kind == "watdiv":
+            gen += ["--scale", str(args.scale)]
         else:  # generate.py's model (Zipf predicates, i^-0.5 endpoints, nodes = triples/4)
             gen += ["--triples", str(args.triples), "--predicates", str(args.predicates)]
         subprocess.run(gen, check=True, stdout=subprocess.DEVNULL)
@@ -79,7 +83,7 @@ def main():
         qfiles = sorted((REPO / "datagen/queries/lubm").glob("*.rq")) + \
             sorted((REPO / "datagen/queries/lubm_complex").glob("*.rq"))
     else:
-        qfiles = sorted((REPO / "datagen/queries/powerlaw").glob("*.rq"))
+        qfiles = sorted((REPO / f"datagen/queries/{args.kind}").glob("*.rq"))
     summary = {"gpu_ms": 0.0, "cpu_s": 0.0, "join_rows": 0, "parity_ok": 0, "parity_checked": 0}
     for qf in qfiles:
         q = g.bind_constants(g.parse_query(qf.read_text()), store.dictionary)
