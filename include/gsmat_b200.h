@@ -205,6 +205,13 @@ gsm_status gsm_result_device_ptr(const gsm_result* res, uint64_t* device_ptr);
 
 gsm_status gsm_result_free(gsm_result* res);
 
+/* Batch helpers: shapes of n results (n_rows[i], n_cols[i]), and copy of
+ * result i into host_rows[i] (skipped when NULL) followed by
+ * gsm_result_free of every result when free_after != 0. */
+gsm_status gsm_results_shape(gsm_result* const* res, int32_t n, int64_t* n_rows, int32_t* n_cols);
+gsm_status gsm_results_copy(gsm_result* const* res, int32_t n, uint32_t* const* host_rows,
+                            int32_t free_after);
+
 /* ---- diagnostics ------------------------------------------------------ */
 
 /* Thread-local message of the last failing call (empty string if none). */

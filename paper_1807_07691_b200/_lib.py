@@ -45,6 +45,8 @@ EXPORTS = (
     "gsm_result_copy",
     "gsm_result_device_ptr",
     "gsm_result_free",
+    "gsm_results_shape",
+    "gsm_results_copy",
     "gsm_last_error",
     "gsm_kernel_launches",
 )
@@ -140,6 +142,8 @@ def lib() -> C.CDLL:
             "gsm_result_copy": (i32, [vp, vp]),
             "gsm_result_device_ptr": (i32, [vp, P(C.c_uint64)]),
             "gsm_result_free": (i32, [vp]),
+            "gsm_results_shape": (i32, [P(vp), i32, P(i64), P(i32)]),
+            "gsm_results_copy": (i32, [P(vp), i32, P(vp), i32]),
             "gsm_last_error": (C.c_char_p, []),
             "gsm_kernel_launches": (i64, []),
         }

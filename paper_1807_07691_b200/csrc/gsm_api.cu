@@ -79,6 +79,30 @@ gsm_status gsm_result_device_ptr(const gsm_result* res, uint64_t* device_ptr) {
   return GSM_OK;
 }
 
+gsm_status gsm_results_shape(gsm_result* const* res, int32_t n, int64_t* n_rows, int32_t* n_cols) {
+  if (n < 0 || (n > 0 && (!res || !n_rows || !n_cols))) return gsm::set_error(GSM_ERR_VALUE, "bad arguments");
+  for (int i = 0; i < n; i++) {
+    n_rows[i] = res[i] ? res[i]->n : 0;
+    n_cols[i] = res[i] ? res[i]->k : 0;
+  }
+  return GSM_OK;
+}
+
+gsm_status gsm_results_copy(gsm_result* const* res, int32_t n, uint32_t* const* host_rows,
+                            int32_t free_after) {
+  if (n < 0 || (n > 0 && !res)) return gsm::set_error(GSM_ERR_VALUE, "bad arguments");
+  gsm_status first = GSM_OK;
+  for (int i = 0; i < n; i++) {
+    if (res[i] && host_rows && host_rows[i] && first == GSM_OK) {
+      gsm_status st = gsm_result_copy(res[i], host_rows[i]);
+      if (st != GSM_OK) first = st;
+    }
+  }
+  if (free_after)
+    for (int i = 0; i < n; i++) gsm_result_free(res[i]);
+  return first;
+}
+
 gsm_status gsm_result_free(gsm_result* res) {
   if (!res) return GSM_OK;
   if (res->rows) {

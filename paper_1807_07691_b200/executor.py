@@ -288,18 +288,27 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
         if not plan.steps:
             raise ValueError("cannot execute an empty plan")
         steps, arr, proj_arr, nproj = compile_plan(query, plan)
-        rep_struct, bufs = _new_report(len(steps)) if reports is not None else (None, None)
-        prepared.append((steps, arr, proj_arr, rep_struct, bufs))
+        tmpl = plan.__dict__.get("_gsm_query")
+        if tmpl is None or tmpl[0] is not arr:
+            rec = _lib.Query()
+            rec.steps = arr
+            rec.n_steps = len(steps)
+            rec.proj = proj_arr
+            rec.n_proj = nproj
+            rec.distinct = 1 if query.distinct else 0
+            rec.part_index, rec.part_count = 0, 1
+            tmpl = (arr, rec)
+            try:
+                plan.__dict__["_gsm_query"] = tmpl
+            except (AttributeError, TypeError):
+                pass
+        qarr[i] = tmpl[1]
         q = qarr[i]
-        q.steps = arr
-        q.n_steps = len(steps)
-        q.proj = proj_arr
-        q.n_proj = nproj
-        q.distinct = 1 if query.distinct else 0
         q.row_budget = budget
         q.budget_mode = budget_mode
-        q.part_index, q.part_count = 0, 1
+        rep_struct, bufs = _new_report(len(steps)) if reports is not None else (None, None)
         q.report = C.pointer(rep_struct) if rep_struct is not None else None
+        prepared.append((steps, arr, proj_arr, rep_struct, bufs))
     outs = (C.c_void_p * n)()
     statuses = (C.c_int32 * n)()
     ms = C.c_float(0.0)
@@ -308,17 +317,21 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
                              C.byref(ms) if batch_timing is not None else None)
     if st != _lib.GSM_OK:
         msg = _lib.last_error()
-        for i in range(n):
-            if outs[i]:
-                L.gsm_result_free(outs[i])
+        L.gsm_results_copy(outs, n, None, 1)
         _lib.raise_status(st, msg)
+    # two calls for all results: shapes, then copy + free
+    nrows = (C.c_int64 * n)()
+    ncols = (C.c_int32 * n)()
+    L.gsm_results_shape(outs, n, nrows, ncols)
+    arrays = [np.empty((int(nrows[i]), int(ncols[i])), dtype=np.uint32) for i in range(n)]
+    dsts = (C.c_void_p * n)(*[a.ctypes.data if a.size else None for a in arrays])
+    _lib.check(L.gsm_results_copy(outs, n, dsts, 1))
     results = []
     for i, (query, plan) in enumerate(items):
-        out = _fetch(L, C.c_void_p(outs[i]))
         steps, _, _, rep_struct, bufs = prepared[i]
         if reports is not None:
             _fill_report(reports[i], steps, rep_struct, *bufs)
-        results.append(BindingTable(tuple(query.projection), array=out))
+        results.append(BindingTable(tuple(query.projection), array=arrays[i]))
     if batch_timing is not None:
         batch_timing.append(ms.value / 1e3)
     return results
