@@ -478,12 +478,6 @@ def run_reference(args):
             "config": {"workload": f"LUBM-style U={args.univ} ({store.triple_count} triples), "
                                    "Q1-Q14, one step = 14 queries",
                        "univ": args.univ, "seed": args.seed},
-            "sequential": {"value": round(rows_all / dev_seq, 1) if dev_seq > 0 else 0.0,
-                           "ms_per_step": round(1e3 * dev_seq / args.steps, 4),
-                           "e2e": round(rows_all / wall_seq, 1) if wall_seq > 0 else 0.0,
-                           "e2e_ms_per_step": round(1e3 * wall_seq / args.steps, 4),
-                           "note": "queries one at a time (value/e2e above: the step's 14 "
-                                   "queries as one execute_batch call on 14 streams)"},
             "latency_ms": lat,
             "cpu_baseline": {"value": round(value, 1), "unit": "rows/s", "cores": cores,
                              "kind": "reference",
