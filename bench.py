@@ -62,6 +62,7 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
     ap.add_argument("--only-probe", action="store_true", help="run only the kernel probe (ncu)")
+    ap.add_argument("--probe", default=None, help="with --only-probe: run just this probe")
     return ap.parse_args()
 
 
@@ -78,9 +79,11 @@ PROBES = [
 ]
 
 
-def run_probe(g, store, peaks, reps=5):
+def run_probe(g, store, peaks, reps=5, only=None):
     out = {}
     for name, text in PROBES:
+        if only and name != only:
+            continue
         q = g.bind_constants(g.parse_query(text), store.dictionary)
         plan = g.make_plan(q, store.stats)
         best = None
@@ -215,7 +218,7 @@ def run_ours(args):
         triples = store.triple_count
         flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=f"cuda:{local}")  # 256 MB > L2
         if args.only_probe:
-            print(json.dumps(run_probe(g, store, _peaks()[0], reps=5)))
+            print(json.dumps(run_probe(g, store, _peaks()[0], reps=5, only=args.probe)))
             return
 
         items = [(q, plan) for _, q, plan in queries]

@@ -15,6 +15,10 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:ExpandP -s 15 -c 3 \
     -o $out/prof_expand_lubm python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-probe \
     > $out/ncu_expand_lubm.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:ExpandP -c 1 \
-    -o $out/prof_expand_probe python bench.py --only-probe > $out/ncu_probe.log 2>&1
+# skip the first launches of each probe (the first execution may overflow the
+# arena and re-run): capture a steady-state launch
+for p in memberOf_coworkers takesCourse_classmates; do
+  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:ExpandP -s 3 -c 1 \
+      -o $out/prof_probe_$p python bench.py --only-probe --probe $p > $out/ncu_probe_$p.log 2>&1
+done
 echo done
