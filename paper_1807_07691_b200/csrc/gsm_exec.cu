@@ -13,11 +13,13 @@
 //
 // Every join kernel is a single pass of "count -> scan -> scatter" (the
 // paper's Alg. 4 N/P pre-allocation, executor.py:197-215) fused into one
-// persistent kernel: tiles of 1024 left rows compute their candidate counts
-// (the N of each row), a decoupled look-back publishes tile prefixes (P), and
-// the same block scatters its rows' outputs into [P, P+N) with a
-// load-balanced output-slot -> row binary search, so hub rows of the
-// power-law tail are spread over all 256 threads of the tile.
+// persistent kernel: blocks take 256-row tiles from an atomic counter, each
+// thread computes its row's candidate count (N), the block scans the tile
+// and a warp-parallel decoupled look-back yields the tile's output offset
+// (P); the same block then scatters the tile's outputs into [P, P+N) by
+// degree tier: short rows through a swizzled shared-memory window (coalesced
+// stores), rows of >= 32 candidates warp-cooperatively, and hub rows of the
+// power-law tail (>= 256) as 1024-output pieces drained by k_drain on every SM.
 #include <algorithm>
 #include <utility>
 #include <cstdio>
