@@ -208,6 +208,8 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     s_nlong = 0;
   }
   p.prepare(s_in);
+  u32 wtag = 0;  // load-balanced scatter: round tag of the row-start marks
+  if constexpr (P::kWindow) P::window_init();
   __syncthreads();
   const i64 n = p.rows(s_in);
   const i64 ntiles = (n + TS_TILE - 1) / TS_TILE;
@@ -215,6 +217,8 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   i64 e_acc = 0;
   for (bool first = true; ntiles > 0; first = false) {
     if (!first) {
+      // every tile was taken by some block's first grab: skip the atomic
+      if (ntiles <= (i64)gridDim.x) break;
       if (tid == 0) {
         s_tile = atomicAdd(ts.counter, 1u);
         s_nlong = 0;
@@ -229,7 +233,21 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       const int rl = i * TS_THREADS + tid;
       const i64 r = base + rl;
       u32 aux = 0, c = 0;
-      if (r < n) c = p.count(s_in, r, aux, e_acc);
+      if constexpr (P::kWindow) {
+        // the tile's left columns, for the load-balanced scatter (issued
+        // before the count's dependent lookups so the loads overlap)
+        u32 lv[P::WIN_A];
+        const int na = r < n ? p.staged_cols() : 0;
+#pragma unroll
+        for (int cc = 0; cc < P::WIN_A; cc++)
+          if (cc < na) lv[cc] = __ldg(s_in.col[cc] + r);
+        if (r < n) c = p.count(s_in, r, aux, e_acc);
+#pragma unroll
+        for (int cc = 0; cc < P::WIN_A; cc++)
+          if (cc < na) P::left_tile()[cc][rl] = lv[cc];
+      } else {
+        if (r < n) c = p.count(s_in, r, aux, e_acc);
+      }
       s_aux[rl] = aux;
       s_pre[rl] = c;
     }
@@ -258,21 +276,22 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     if (tid == TS_THREADS - 1) s_pre[TS_TILE] = run;
     __syncthreads();
     const i64 total = s_pre[TS_TILE];
+    // Tiles whose rows average < WARP_ROW candidates: load-balanced scatter
+    // (does its own look-back, overlapped with its first loads).
+    if constexpr (P::kWindow) {
+      if (total > 0 && total <= (i64)WARP_ROW * TS_TILE && p.window_ok()) {
+        p.scatter_balanced(s_pre, s_aux, total, ts, t, s_base, wtag);
+        if ((i64)t == ntiles - 1 && tid == 0) p.finish(s_base + total);
+        __syncthreads();
+        continue;
+      }
+    }
     if (warp == 0) {
       const i64 b = lookback_warp(ts, t, total);
       if (lane == 0) s_base = b;
     }
     __syncthreads();
     const i64 gbase = s_base;
-    // Tiles whose rows average < WARP_ROW candidates: staged, coalesced writes.
-    if constexpr (P::kWindow) {
-      if (total <= (i64)WARP_ROW * TS_TILE &&
-          p.scatter_window(s_in, base, s_pre, s_aux, total, gbase)) {
-        if ((i64)t == ntiles - 1 && tid == 0) p.finish(gbase + total);
-        __syncthreads();
-        continue;
-      }
-    }
     // Scatter (TS_ITEMS == 1: thread tid owns tile row tid).  Rows with fewer
     // than WARP_ROW candidates are written by their own thread (consecutive
     // rows are adjacent in the output, so a warp's stores stay dense); longer
@@ -512,67 +531,147 @@ struct ExpandP {
       out[(i64)a * cap + g] = __ldg(R.dst + aux + j);
     }
   }
-  // Tiles of short rows: stage the tile's output in shared-memory windows of
-  // WIN slots, then write each window with coalesced stores (thread-per-row
-  // stores of short runs would scatter).  Each thread fills 8 consecutive
-  // slots (one binary search, then a merge-path walk); slots are XOR-swizzled
-  // so neither the fill nor the flush has bank conflicts.  Returns false when
-  // the output is too wide for the window (caller uses the tiered path).
-  static constexpr int WIN = 2048, WIN_W = 4;
-  __device__ static int swz(int sl) { return sl ^ ((sl >> 5) & 7); }
-  __device__ bool scatter_window(const DTable& s, i64 base, const i64* pre, const u32* auxv,
-                                 i64 total, i64 gbase) const {
-    const int width = fz.stage ? fz.k : a + 1;
-    if (width > WIN_W || width < 1) return false;
-    __shared__ u32 win[WIN_W * WIN];
-    const int tid = threadIdx.x;
-    for (i64 w = 0; w < total; w += WIN) {
-      const int nw = (int)min((i64)WIN, total - w);
-      const int s0 = 8 * tid;
-      if (s0 < nw) {
-        const i64 slot0 = w + s0;
-        int lo = 0, hi = TS_TILE;  // pre[lo] <= slot0 < pre[hi]
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (pre[mid] <= slot0) lo = mid; else hi = mid;
-        }
-        int r = lo;
+  // Tiles of short rows (average < WARP_ROW candidates): load-balanced
+  // scatter.  Output slots, not rows, are dealt to threads: in a round over
+  // the window [w, w + WIN), slot w + warp*256 + i*32 + lane (i < SLOTS)
+  // belongs to thread (warp, lane), so every store instruction covers 32
+  // consecutive output slots whatever the row lengths.  A slot's row comes
+  // from "row start" marks in shared memory (row+1 written at the slot where
+  // each row's output begins, tagged with the round so marks never need
+  // clearing): within a 32-slot chunk, a ballot over the marks and one
+  // shuffle give every lane its row; the chunk's carry-in row is the previous
+  // chunk's last (a binary search for the warp's first chunk).  All SLOTS
+  // neighbour loads are issued before any store; the tile's look-back runs
+  // while the first round's loads are in flight.  Left values come from the
+  // tile's left columns staged in shared memory by the count phase.
+  static constexpr int WIN = 2048, WIN_A = 8, SLOTS = WIN / TS_THREADS, MARK_BITS = 9;
+  static constexpr u32 TAG_MAX = (1u << (32 - MARK_BITS)) - 1;
+  __device__ static u32 (*left_tile())[TS_TILE] {
+    __shared__ u32 lt[WIN_A][TS_TILE];
+    return lt;
+  }
+  __device__ static u32 (*marks())[WIN] {
+    __shared__ u32 mk[2][WIN];
+    return mk;
+  }
+  __device__ static i64* row_src() {  // per row: dst index of output slot 0
+    __shared__ i64 rs[TS_TILE];
+    return rs;
+  }
+  __device__ static void window_init() {  // smem is undefined at kernel start
+    u32* mk = &marks()[0][0];
+    for (int i = threadIdx.x; i < 2 * WIN; i += TS_THREADS) mk[i] = 0;
+  }
+  __device__ int staged_cols() const { return a <= WIN_A ? a : 0; }
+  __device__ bool window_ok() const { return a <= WIN_A && (!fz.stage || (fz.k >= 1 && fz.k <= 4)); }
+  __device__ static int find_row(const i64* pre, i64 slot) {
+    int lo = 0, hi = TS_TILE;  // largest lo with pre[lo] <= slot (pre[0] = 0)
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-          const int sl = s0 + i;
-          if (sl < nw) {
-            const i64 slot = w + sl;
-            while (slot >= pre[r + 1]) r++;
-            const u32 nv = __ldg(R.dst + auxv[r] + (slot - pre[r]));
-            const int q = swz(sl);
-            if (fz.stage) {
-              for (int x = 0; x < width; x++) {
-                const int src = fz.pj[x];
-                win[x * WIN + q] = src < a ? __ldg(s.col[src] + base + r) : nv;
-              }
+    for (int it = 0; it < 8; it++) {
+      const int mid = (lo + hi) >> 1;
+      if (pre[mid] <= slot) lo = mid; else hi = mid;
+    }
+    return lo;
+  }
+  // A = left arity for columnar output (0: runtime a); K = fused row-major width (0: columnar)
+  template <int A, int K>
+  __device__ void balanced_rounds(const i64* pre, i64 total, const TileSync& ts, u32 t,
+                                  i64& s_base, u32& wtag) const {
+    static_assert(TS_TILE == 256, "find_row searches 2^8 rows; marks hold row+1 in 9 bits");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    u32 (*lt)[TS_TILE] = left_tile();
+    const i64* rsrc = row_src();
+    i64 gbase = 0;
+    int q = 0;
+    for (i64 w = 0; w < total; w += WIN, q++) {
+      if (wtag == TAG_MAX) {  // tag wrap: clear the marks once (uniform branch)
+        __syncthreads();
+        window_init();
+        __syncthreads();
+        wtag = 0;
+      }
+      const u32 tag = ++wtag;
+      u32* m = marks()[q & 1];
+      {
+        const i64 p0 = pre[tid];
+        if (pre[tid + 1] > p0 && p0 >= w && p0 < w + WIN) m[p0 - w] = (tag << MARK_BITS) | (u32)(tid + 1);
+      }
+      __syncthreads();
+      const int ws = warp * (32 * SLOTS);  // this warp's first slot in the window
+      int carry = w + ws < total ? find_row(pre, w + ws) : 0;
+      int rr[SLOTS];
+#pragma unroll
+      for (int i = 0; i < SLOTS; i++) {
+        const int sl = ws + i * 32 + lane;
+        const u32 mv = m[sl];
+        const u32 bal = __ballot_sync(0xffffffffu, (mv >> MARK_BITS) == tag);
+        const u32 le = bal & (0xffffffffu >> (31 - lane));
+        const int srcl = le ? 31 - __clz((int)le) : 0;
+        const int rv = (int)(__shfl_sync(0xffffffffu, mv, srcl) & ((1u << MARK_BITS) - 1)) - 1;
+        const int row = le ? rv : carry;
+        carry = __shfl_sync(0xffffffffu, row, 31);
+        rr[i] = w + sl < total ? row : -1;
+      }
+      u32 nv[SLOTS];
+#pragma unroll
+      for (int i = 0; i < SLOTS; i++) {
+        const i64 slot = w + ws + i * 32 + lane;
+        nv[i] = rr[i] >= 0 ? __ldg(R.dst + (rsrc[rr[i]] + slot)) : 0u;
+      }
+      if (q == 0) {  // the tile's output offset, while the loads are in flight
+        if (warp == 0) {
+          const i64 b = lookback_warp(ts, t, total);
+          if (lane == 0) s_base = b;
+        }
+        __syncthreads();
+        gbase = s_base;
+      }
+#pragma unroll
+      for (int i = 0; i < SLOTS; i++) {
+        const i64 g = gbase + w + ws + i * 32 + lane;
+        const int r = rr[i];
+        if (r < 0) continue;
+        if constexpr (K == 0) {
+          if (g < cap) {
+            if constexpr (A > 0) {
+#pragma unroll
+              for (int cc = 0; cc < A; cc++) out[(i64)cc * cap + g] = lt[cc][r];
             } else {
-              for (int cc = 0; cc < a; cc++) win[cc * WIN + q] = __ldg(s.col[cc] + base + r);
-              win[a * WIN + q] = nv;
+              for (int cc = 0; cc < a; cc++) out[(i64)cc * cap + g] = lt[cc][r];
+            }
+            out[(i64)a * cap + g] = nv[i];
+          }
+        } else {
+          if (g < fz.cap) {
+            u32* o = fz.stage + g * K;
+#pragma unroll
+            for (int x = 0; x < K; x++) {
+              const int src = fz.pj[x];
+              o[x] = src < a ? lt[src][r] : nv[i];
             }
           }
         }
       }
-      __syncthreads();
-      const i64 g0 = gbase + w;
-      if (fz.stage) {  // row-major: word idx = row * width + x
-        const int words = nw * width;
-        for (int idx = tid; idx < words; idx += TS_THREADS) {
-          const int row = idx / width, x = idx - row * width;
-          if (g0 + row < fz.cap) fz.stage[g0 * width + idx] = win[x * WIN + swz(row)];
-        }
-      } else {
-        for (int cc = 0; cc < width; cc++)
-          for (int i = tid; i < nw; i += TS_THREADS)
-            if (g0 + i < cap) out[(i64)cc * cap + g0 + i] = win[cc * WIN + swz(i)];
-      }
-      __syncthreads();
     }
-    return true;
+  }
+  __device__ void scatter_balanced(const i64* pre, const u32* auxv, i64 total, const TileSync& ts,
+                                   u32 t, i64& s_base, u32& wtag) const {
+    row_src()[threadIdx.x] = (i64)auxv[threadIdx.x] - pre[threadIdx.x];  // read after round 0's barrier
+    if (fz.stage) {
+      switch (fz.k) {
+        case 1: balanced_rounds<0, 1>(pre, total, ts, t, s_base, wtag); return;
+        case 2: balanced_rounds<0, 2>(pre, total, ts, t, s_base, wtag); return;
+        case 3: balanced_rounds<0, 3>(pre, total, ts, t, s_base, wtag); return;
+        default: balanced_rounds<0, 4>(pre, total, ts, t, s_base, wtag); return;
+      }
+    }
+    switch (a) {
+      case 1: balanced_rounds<1, 0>(pre, total, ts, t, s_base, wtag); return;
+      case 2: balanced_rounds<2, 0>(pre, total, ts, t, s_base, wtag); return;
+      case 3: balanced_rounds<3, 0>(pre, total, ts, t, s_base, wtag); return;
+      case 4: balanced_rounds<4, 0>(pre, total, ts, t, s_base, wtag); return;
+      default: balanced_rounds<0, 0>(pre, total, ts, t, s_base, wtag); return;
+    }
   }
   // Fused row-major output of candidates [j0, j0+32) (value nv per lane).
   __device__ void emit_chunk_fused(const DTable& s, i64 r, u32 nv, i64 j0, i64 c, i64 pos) const {
@@ -771,6 +870,8 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
   }
   for (bool first = true; ntiles > 0; first = false) {
     if (!first) {
+      // every tile was taken by some block's first grab: skip the atomic
+      if (ntiles <= (i64)gridDim.x) break;
       if (tid == 0) {
         s_tile = atomicAdd(ts.counter, 1u);
         s_nlong = 0;

@@ -192,11 +192,45 @@ def test_reference_objects_drop_in():
         g.execute(q, plan, st, row_budget=0)
 
 
+UB = "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
+RDF = "PREFIX rdf: <http://www.w3.org/1999/02/22-rdf-syntax-ns#> "
+# Expand steps of mid-degree rows (courses: ~5-50 students) under every
+# output layout of the load-balanced scatter: projected widths 1-5 (fused
+# row-major up to 4, then unfused), left arities 2-9 (columnar specialisations
+# 1-4, generic, and above the shared-memory staging limit).
+LAYOUT_QUERIES = [
+    UB + "SELECT ?y WHERE { ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }",
+    UB + "SELECT ?y ?x WHERE { ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }",
+    UB + "SELECT * WHERE { ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }",
+    UB + "SELECT * WHERE { ?x ub:memberOf ?d . ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }",
+    UB + "SELECT ?c ?y ?d ?x WHERE { ?x ub:memberOf ?d . ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }",
+    UB + "SELECT * WHERE { ?x ub:memberOf ?d . ?x ub:emailAddress ?e . ?x ub:takesCourse ?c . "
+    "?y ub:takesCourse ?c . }",
+    UB + "SELECT * WHERE { ?x ub:memberOf ?d . ?x ub:emailAddress ?e . ?x ub:telephone ?t . "
+    "?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }",
+    UB + "SELECT * WHERE { ?x ub:memberOf ?d . ?x ub:emailAddress ?e . ?x ub:telephone ?t . "
+    "?x ub:name ?n . ?d ub:subOrganizationOf ?u . ?x ub:undergraduateDegreeFrom ?v . "
+    "?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }",
+    UB + "SELECT * WHERE { ?x ub:memberOf ?d . ?x ub:emailAddress ?e . ?x ub:telephone ?t . "
+    "?x ub:name ?n . ?d ub:subOrganizationOf ?u . ?x ub:undergraduateDegreeFrom ?v . "
+    "?x ub:advisor ?ad . ?x ub:takesCourse ?c . ?y ub:takesCourse ?c . }",
+    UB + "SELECT ?y WHERE { ?x ub:teacherOf ?c . ?y ub:takesCourse ?c . }",
+]
+
+
+def test_expand_layouts_vs_oracle(store_factory):
+    store = g.load(store_factory("lubm", univ=1, seed=3))
+    for text in LAYOUT_QUERIES:
+        res = _oracle_compare(store, text, row_budget=1 << 62)
+        assert len(res) > 0, text
+
+
 def test_execution_variants_agree(store_factory):
     """Graph replay, programmatic dependent launch, step fusion and hub
-    deferral are pure optimisations: each query gives the same bag and the
-    same per-step report with them switched off (GSM_NO_GRAPHS / GSM_NO_PDL /
-    GSM_NO_FUSION / GSM_NO_DEFER), and repeated (replayed) executions agree."""
+    deferral and projection fusion are pure optimisations: each query gives
+    the same bag and the same per-step report with them switched off
+    (GSM_NO_GRAPHS / GSM_NO_PDL / GSM_NO_FUSION / GSM_NO_DEFER /
+    GSM_NO_PROJ_FUSION), and repeated (replayed) executions agree."""
     import json
     import os
     import subprocess
@@ -205,7 +239,8 @@ def test_execution_variants_agree(store_factory):
     d = store_factory("lubm", univ=2, seed=4)
     texts = [t for _, t in lubm_queries()] + [
         (GOLDEN.parents[1] / "datagen/queries/lubm_complex" / f).read_text()
-        for f in sorted(os.listdir(GOLDEN.parents[1] / "datagen/queries/lubm_complex"))]
+        for f in sorted(os.listdir(GOLDEN.parents[1] / "datagen/queries/lubm_complex"))
+    ] + LAYOUT_QUERIES
     script = (
         "import json, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
         "import paper_1807_07691_b200 as g\n"
@@ -227,7 +262,8 @@ def test_execution_variants_agree(store_factory):
     )
     results = {}
     for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION", "GSM_NO_DEFER",
-                    "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER"):
+                    "GSM_NO_PROJ_FUSION",
+                    "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER,GSM_NO_PROJ_FUSION"):
         env = dict(os.environ)
         for k in filter(None, variant.split(",")):
             env[k] = "1"
