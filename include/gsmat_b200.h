@@ -110,6 +110,13 @@ gsm_status gsm_store_create(int32_t device, int64_t node_count, int32_t max_pid,
 gsm_status gsm_store_put_predicate(gsm_store* store, int32_t pid, const uint64_t* so_pairs,
                                    const uint64_t* os_pairs, int64_t nnz);
 
+/* Sharded stores (SURVEY.md §8(e) sharded mode): one shard's part of a
+ * predicate — the CSR rows it owns (so pairs whose subject is in its id
+ * range) and the CSC rows it owns (os pairs whose object is in its range),
+ * so the two orientations hold different pair counts. */
+gsm_status gsm_store_put_predicate_shard(gsm_store* store, int32_t pid, const uint64_t* so_pairs,
+                                         int64_t nnz_so, const uint64_t* os_pairs, int64_t nnz_os);
+
 /* Replaces PredicateMatrix.__post_init__ / build_aux (storage.py:38-53,66-72):
  * builds the device row indexes (aux arrays, key -> segment lookup, diagonal
  * lists) for every uploaded predicate and validates sortedness. */
@@ -142,6 +149,37 @@ gsm_status gsm_execute(gsm_context* ctx, const gsm_pattern* steps, int32_t n_ste
                        const int32_t* proj, int32_t n_proj, int32_t distinct,
                        int64_t row_budget, int32_t budget_mode, int64_t part_index,
                        int64_t part_count, gsm_report* report, gsm_result** out);
+
+/* Sharded mode, one step at a time: like gsm_execute, but
+ * step 0 is the caller's binding table instead of a scan — `seed_rows` is a
+ * DEVICE pointer to n_seed x seed_k row-major uint32 ids whose columns bind
+ * variables seed_vars[0..seed_k) — and `steps` (n_steps patterns, possibly
+ * none) are joined onto it with the same rules as executor.py:340-356.  The
+ * report arrays hold n_steps + 1 entries (entry 0 = the seed).  Never cached
+ * as a CUDA graph (the seed buffer changes per call). */
+gsm_status gsm_execute_seeded(gsm_context* ctx, const uint32_t* seed_rows, int64_t n_seed,
+                              const int32_t* seed_vars, int32_t seed_k, const gsm_pattern* steps,
+                              int32_t n_steps, const int32_t* proj, int32_t n_proj,
+                              int32_t distinct, int64_t row_budget, int32_t budget_mode,
+                              gsm_report* report, gsm_result** out);
+
+/* Sharded-mode exchange (the partition side of an all-to-all): groups the
+ * DEVICE rows `rows` (n x k row-major uint32) by destination shard and writes
+ * them to the DEVICE buffer out_rows (destination 0 first), with the number
+ * of rows per destination in counts[parts] (host).  Destination = the shard
+ * owning the id in column key_col (owner(id) = (id-1)*parts/node_count, the
+ * subject/object id ranges a sharded store is split by), or, with key_col < 0,
+ * a hash of the whole row (distributed DISTINCT).  Synchronous. */
+gsm_status gsm_partition_rows(gsm_context* ctx, const uint32_t* rows, int64_t n, int32_t k,
+                              int32_t key_col, int64_t node_count, int32_t parts,
+                              uint32_t* out_rows, int64_t* counts);
+
+/* Sharded-mode cross product (executor.py:155-165) on DEVICE row-major
+ * tables: out[g] = left[g / n_right] ++ right[g % n_right], out holding
+ * n_left * n_right rows of a + b ids (caller-allocated).  Synchronous; the
+ * budget rule is the caller's (it needs the global |L|). */
+gsm_status gsm_cross_rows(gsm_context* ctx, const uint32_t* left, int64_t n_left, int32_t a,
+                          const uint32_t* right, int64_t n_right, int32_t b, uint32_t* out);
 
 /* One query of a batch: the arguments of gsm_execute. */
 typedef struct {

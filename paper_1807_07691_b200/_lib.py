@@ -33,6 +33,7 @@ EXPORTS = (
     "gsm_device_count",
     "gsm_store_create",
     "gsm_store_put_predicate",
+    "gsm_store_put_predicate_shard",
     "gsm_store_finalize",
     "gsm_store_device_bytes",
     "gsm_store_free",
@@ -40,6 +41,9 @@ EXPORTS = (
     "gsm_context_free",
     "gsm_execute",
     "gsm_execute_batch",
+    "gsm_execute_seeded",
+    "gsm_partition_rows",
+    "gsm_cross_rows",
     "gsm_table_join",
     "gsm_result_shape",
     "gsm_result_copy",
@@ -124,6 +128,7 @@ def lib() -> C.CDLL:
             "gsm_device_count": (i32, [P(i32)]),
             "gsm_store_create": (i32, [i32, i64, i32, P(vp)]),
             "gsm_store_put_predicate": (i32, [vp, i32, vp, vp, i64]),
+            "gsm_store_put_predicate_shard": (i32, [vp, i32, vp, i64, vp, i64]),
             "gsm_store_finalize": (i32, [vp]),
             "gsm_store_device_bytes": (i32, [vp, P(i64)]),
             "gsm_store_free": (i32, [vp]),
@@ -134,6 +139,13 @@ def lib() -> C.CDLL:
                 [vp, P(Pattern), i32, P(i32), i32, i32, i64, i32, i64, i64, P(Report), P(vp)],
             ),
             "gsm_execute_batch": (i32, [P(vp), i32, P(Query), P(i32), P(vp), P(C.c_float)]),
+            "gsm_execute_seeded": (
+                i32,
+                [vp, vp, i64, P(i32), i32, P(Pattern), i32, P(i32), i32, i32, i64, i32,
+                 P(Report), P(vp)],
+            ),
+            "gsm_partition_rows": (i32, [vp, vp, i64, i32, i32, i64, i32, vp, P(i64)]),
+            "gsm_cross_rows": (i32, [vp, vp, i64, i32, vp, i64, i32, vp]),
             "gsm_table_join": (
                 i32,
                 [vp, vp, i64, i32, vp, i64, i32, P(i32), P(i32), i32, i64, i32, P(i64), vp, P(vp)],

@@ -178,6 +178,55 @@ __device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
   return excl;
 }
 
+// Block-wide decoupled look-back: all TS_THREADS threads inspect one
+// predecessor each per round (256 tiles per round instead of 32), since the
+// whole block waits for the tile offset anyway.  The tile's aggregate must
+// already be published (lb_publish).  Returns the exclusive prefix (to every
+// thread) and publishes the inclusive prefix.
+struct LBShared {
+  int first[TS_THREADS / 32];
+  i64 sum[TS_THREADS / 32];
+};
+__device__ __forceinline__ void lb_publish(const TileSync& ts, u32 t, i64 agg) {
+  if (threadIdx.x == 0) st_release_u64(ts.status + t, lb_word(ts.epoch, t == 0 ? 2 : 1, agg));
+}
+__device__ i64 lookback_block(const TileSync& ts, u32 t, i64 agg, LBShared& sh) {
+  if (t == 0) return 0;  // tile 0 published its inclusive prefix in lb_publish
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = TS_THREADS / 32;
+  i64 excl = 0;
+  i64 top = (i64)t - 1;
+  for (;;) {
+    const i64 j = top - tid;
+    u64 w = 0;
+    u32 fl = 2;  // before tile 0: an inclusive prefix of 0
+    if (j >= 0) {
+      do {
+        w = ld_acquire_u64(ts.status + j);
+        fl = ((u32)(w >> 42) == ts.epoch) ? (u32)(w >> 40) & 3u : 0u;
+      } while (fl == 0);
+    }
+    const u32 bal = __ballot_sync(0xffffffffu, fl == 2);
+    if (lane == 0) sh.first[warp] = bal ? warp * 32 + __ffs(bal) - 1 : (1 << 30);
+    __syncthreads();
+    int first = sh.first[0];
+#pragma unroll
+    for (int i = 1; i < NW; i++) first = min(first, sh.first[i]);
+    i64 v = (tid <= first && j >= 0) ? (i64)(w & LB_MASK) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh.sum[warp] = v;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NW; i++) excl += sh.sum[i];
+    __syncthreads();  // sh is reused by the next round / the next tile
+    if (first < (1 << 30)) break;
+    top -= TS_THREADS;
+  }
+  if (tid == 0) st_release_u64(ts.status + t, lb_word(ts.epoch, 2, excl + agg));
+  return excl;
+}
+
 // ---------------------------------------------------------------------------
 // The fused count/scan/scatter kernel, parameterised by a row policy P:
 //   P::prepare(DTable& smem)   copy the input descriptor into shared memory
@@ -192,7 +241,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   __shared__ i64 s_pre[TS_TILE + 1];
   __shared__ u32 s_aux[TS_TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
-  __shared__ i64 s_base;
+  __shared__ LBShared s_lb;
   __shared__ u32 s_tile;
   __shared__ int s_long[TS_TILE];
   __shared__ int s_nlong;
@@ -276,22 +325,18 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     if (tid == TS_THREADS - 1) s_pre[TS_TILE] = run;
     __syncthreads();
     const i64 total = s_pre[TS_TILE];
+    lb_publish(ts, t, total);  // successors can start summing right away
     // Tiles whose rows average < WARP_ROW candidates: load-balanced scatter
     // (does its own look-back, overlapped with its first loads).
     if constexpr (P::kWindow) {
       if (total > 0 && total <= (i64)WARP_ROW * TS_TILE && p.window_ok()) {
-        p.scatter_balanced(s_pre, s_aux, total, ts, t, s_base, wtag);
-        if ((i64)t == ntiles - 1 && tid == 0) p.finish(s_base + total);
+        const i64 gb = p.scatter_balanced(s_pre, s_aux, total, ts, t, s_lb, wtag);
+        if ((i64)t == ntiles - 1 && tid == 0) p.finish(gb + total);
         __syncthreads();
         continue;
       }
     }
-    if (warp == 0) {
-      const i64 b = lookback_warp(ts, t, total);
-      if (lane == 0) s_base = b;
-    }
-    __syncthreads();
-    const i64 gbase = s_base;
+    const i64 gbase = lookback_block(ts, t, total, s_lb);
     // Scatter (TS_ITEMS == 1: thread tid owns tile row tid).  Rows with fewer
     // than WARP_ROW candidates are written by their own thread (consecutive
     // rows are adjacent in the output, so a warp's stores stay dense); longer
@@ -575,8 +620,8 @@ struct ExpandP {
   }
   // A = left arity for columnar output (0: runtime a); K = fused row-major width (0: columnar)
   template <int A, int K>
-  __device__ void balanced_rounds(const i64* pre, i64 total, const TileSync& ts, u32 t,
-                                  i64& s_base, u32& wtag) const {
+  __device__ i64 balanced_rounds(const i64* pre, i64 total, const TileSync& ts, u32 t,
+                                 LBShared& lb, u32& wtag) const {
     static_assert(TS_TILE == 256, "find_row searches 2^8 rows; marks hold row+1 in 9 bits");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     u32 (*lt)[TS_TILE] = left_tile();
@@ -618,14 +663,7 @@ struct ExpandP {
         const i64 slot = w + ws + i * 32 + lane;
         nv[i] = rr[i] >= 0 ? __ldg(R.dst + (rsrc[rr[i]] + slot)) : 0u;
       }
-      if (q == 0) {  // the tile's output offset, while the loads are in flight
-        if (warp == 0) {
-          const i64 b = lookback_warp(ts, t, total);
-          if (lane == 0) s_base = b;
-        }
-        __syncthreads();
-        gbase = s_base;
-      }
+      if (q == 0) gbase = lookback_block(ts, t, total, lb);  // while the loads are in flight
 #pragma unroll
       for (int i = 0; i < SLOTS; i++) {
         const i64 g = gbase + w + ws + i * 32 + lane;
@@ -653,24 +691,25 @@ struct ExpandP {
         }
       }
     }
+    return gbase;
   }
-  __device__ void scatter_balanced(const i64* pre, const u32* auxv, i64 total, const TileSync& ts,
-                                   u32 t, i64& s_base, u32& wtag) const {
+  __device__ i64 scatter_balanced(const i64* pre, const u32* auxv, i64 total, const TileSync& ts,
+                                  u32 t, LBShared& lb, u32& wtag) const {
     row_src()[threadIdx.x] = (i64)auxv[threadIdx.x] - pre[threadIdx.x];  // read after round 0's barrier
     if (fz.stage) {
       switch (fz.k) {
-        case 1: balanced_rounds<0, 1>(pre, total, ts, t, s_base, wtag); return;
-        case 2: balanced_rounds<0, 2>(pre, total, ts, t, s_base, wtag); return;
-        case 3: balanced_rounds<0, 3>(pre, total, ts, t, s_base, wtag); return;
-        default: balanced_rounds<0, 4>(pre, total, ts, t, s_base, wtag); return;
+        case 1: return balanced_rounds<0, 1>(pre, total, ts, t, lb, wtag);
+        case 2: return balanced_rounds<0, 2>(pre, total, ts, t, lb, wtag);
+        case 3: return balanced_rounds<0, 3>(pre, total, ts, t, lb, wtag);
+        default: return balanced_rounds<0, 4>(pre, total, ts, t, lb, wtag);
       }
     }
     switch (a) {
-      case 1: balanced_rounds<1, 0>(pre, total, ts, t, s_base, wtag); return;
-      case 2: balanced_rounds<2, 0>(pre, total, ts, t, s_base, wtag); return;
-      case 3: balanced_rounds<3, 0>(pre, total, ts, t, s_base, wtag); return;
-      case 4: balanced_rounds<4, 0>(pre, total, ts, t, s_base, wtag); return;
-      default: balanced_rounds<0, 0>(pre, total, ts, t, s_base, wtag); return;
+      case 1: return balanced_rounds<1, 0>(pre, total, ts, t, lb, wtag);
+      case 2: return balanced_rounds<2, 0>(pre, total, ts, t, lb, wtag);
+      case 3: return balanced_rounds<3, 0>(pre, total, ts, t, lb, wtag);
+      case 4: return balanced_rounds<4, 0>(pre, total, ts, t, lb, wtag);
+      default: return balanced_rounds<0, 0>(pre, total, ts, t, lb, wtag);
     }
   }
   // Fused row-major output of candidates [j0, j0+32) (value nv per lane).
@@ -1213,12 +1252,13 @@ __global__ void k_pack(const DTable* T, ProjArgs pj, int k, u32* dev_out, i64 de
 // Table-level joins (gsm_table_join): sm_join / parallel_sm_join /
 // cross_product on arbitrary binding tables.
 // ---------------------------------------------------------------------------
-// Row-major host rows -> struct-of-arrays columns (column stride = n).
-__global__ void k_rows_to_cols(const u32* __restrict__ rm, i64 n, int a, u32* __restrict__ cols) {
+// Row-major rows -> struct-of-arrays columns (column stride ld >= n).
+__global__ void k_rows_to_cols(const u32* __restrict__ rm, i64 n, int a, u32* __restrict__ cols,
+                               i64 ld) {
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n * a; i += stride) {
     const i64 r = i / a, c = i - r * a;
-    cols[c * n + r] = rm[i];
+    cols[c * ld + r] = rm[i];
   }
 }
 
@@ -1320,6 +1360,60 @@ __global__ void k_cross_rows(const u32* __restrict__ L, i64 nl, int a, const u32
 }
 
 }  // namespace gsm
+
+// ---------------------------------------------------------------------------
+// Sharded-mode exchange: group binding rows by the shard
+// that owns the next step's key (subject / object id ranges), or by a hash of
+// the whole row for a distributed DISTINCT.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 shard_of(const u32* row, int k, int key_col, u64 node_count, u32 parts) {
+  if (key_col >= 0) {
+    const u32 id = row[key_col];
+    if (id == 0 || node_count == 0) return 0;
+    const u64 o = ((u64)(id - 1) * parts) / node_count;
+    return o < parts ? (u32)o : parts - 1;
+  }
+  u64 h = 0x9E3779B97F4A7C15ull;
+  for (int c = 0; c < k; c++) {
+    h ^= row[c];
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 31;
+  }
+  return (u32)(h % parts);
+}
+
+__global__ void k_part_count(const u32* __restrict__ rows, i64 n, int k, int key_col, u64 node_count,
+                             u32 parts, unsigned long long* __restrict__ counts) {
+  extern __shared__ unsigned int s_hist[];
+  for (u32 d = threadIdx.x; d < parts; d += blockDim.x) s_hist[d] = 0;
+  __syncthreads();
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride)
+    atomicAdd(&s_hist[shard_of(rows + r * k, k, key_col, node_count, parts)], 1u);
+  __syncthreads();
+  for (u32 d = threadIdx.x; d < parts; d += blockDim.x)
+    if (s_hist[d]) atomicAdd(counts + d, (unsigned long long)s_hist[d]);
+}
+
+// cursor[d] starts at destination d's first output row; one atomic per
+// (warp, destination) via match_any.
+__global__ void k_part_scatter(const u32* __restrict__ rows, i64 n, int k, int key_col, u64 node_count,
+                               u32 parts, unsigned long long* __restrict__ cursor, u32* __restrict__ out) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (i64 base = (i64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const i64 r = base + threadIdx.x;
+    const bool live = r < n;
+    const u32 d = live ? shard_of(rows + r * k, k, key_col, node_count, parts) : 0xFFFFFFFFu;
+    const u32 peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long pos = 0;
+    if (live && lane == leader) pos = atomicAdd(cursor + d, (unsigned long long)__popc(peers));
+    pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(peers & ((1u << lane) - 1));
+    if (live)
+      for (int c = 0; c < k; c++) out[(i64)pos * k + c] = rows[r * k + c];
+  }
+}
 
 // ===========================================================================
 // Host orchestration
@@ -1690,6 +1784,12 @@ struct QueryArgs {
   int32_t budget_mode;
   int64_t part, parts;
   gsm_report* rep;
+  // Seeded execution (gsm_execute_seeded): step 0 is this device table
+  // (row-major seed_n x seed_k) instead of a scan; seed_k < 0 = not seeded.
+  const u32* seed = nullptr;
+  int64_t seed_n = 0;
+  const int32_t* seed_vars = nullptr;
+  int32_t seed_k = -1;
 };
 
 // Per-query host state between launch and completion.
@@ -1755,7 +1855,9 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
 
   // Prepared plan: replay the captured launch sequence with the saved
   // query-block image and fresh epochs — no re-planning on the host.
-  if (c->use_graphs) {
+  // (Seeded queries read a caller buffer: never cached.)
+  const bool graphs = c->use_graphs && qa.seed_k < 0;
+  if (graphs) {
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
       const auto& P = it->second;
@@ -1791,8 +1893,18 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   u32* dC = c->d_block->counters;
 
   // ---- step 0: scan ----
-  int cur = ex.scan_table(steps[0], 0);
-  std::vector<int> schema = pattern_schema(steps[0]);
+  int cur;
+  std::vector<int> schema;
+  if (qa.seed_k >= 0) {  // the caller's table, transposed into arena half A
+    cur = ex.new_table(qa.seed_k, H_A);
+    hb->tables[cur].n = qa.seed_n;
+    ex.ub[cur] = qa.seed_n;
+    hb->stats[0].rows = qa.seed_n;
+    schema.assign(qa.seed_vars, qa.seed_vars + qa.seed_k);
+  } else {
+    cur = ex.scan_table(steps[0], 0);
+    schema = pattern_schema(steps[0]);
+  }
   ex.plan[0].kind = S_SCAN;
   ex.plan[0].schema = schema;
   ex.plan[0].out_table = cur;
@@ -2088,6 +2200,13 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     if (timing) GSM_CUDA(record(c->ev_q0));
     GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
     if (timing) GSM_CUDA(record(c->ev[0]));
+    if (qa.seed_k > 0 && qa.seed_n > 0) {
+      const i64 cells = qa.seed_n * qa.seed_k;
+      k_rows_to_cols<<<(int)std::max<i64>(1, std::min<i64>(c->grid_ts, (cells + 255) / 256)), 256, 0, st>>>(
+          qa.seed, qa.seed_n, qa.seed_k, reinterpret_cast<u32*>(ex.buf(H_A)), ex.cap_for(qa.seed_k));
+      GSM_CUDA(cudaGetLastError());
+      nk++;
+    }
     if (ex.res.njobs > 0) {
       GSM_CUDA(launch(c->use_pdl, k_resolve, 1, 64, st, ex.res, dT, dS));
       nk++;
@@ -2195,7 +2314,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     S.kinds[q] = (int)ex.plan[q].kind;
     S.arities[q] = (int)ex.plan[q].schema.size();
   }
-  if (c->use_graphs) {
+  if (graphs) {
     cudaGraphExec_t ge = nullptr;
     {
       if (c->graphs.size() >= 1024) ctx_clear_graphs(c);
@@ -2250,6 +2369,17 @@ static gsm_status validate_query(const gsm_context* c, const QueryArgs& q) {
     if (p.s_var >= GSM_MAX_VARS || p.o_var >= GSM_MAX_VARS || p.s_var < -1 || p.o_var < -1)
       return set_error(GSM_ERR_VALUE, "variable index out of range");
   }
+  if (q.seed_k >= 0) {
+    if (q.seed_k > GSM_MAX_VARS || q.seed_n < 0 || (q.seed_k > 0 && !q.seed_vars) ||
+        (q.seed_k > 0 && q.seed_n > 0 && !q.seed))
+      return set_error(GSM_ERR_VALUE, "bad seed table");
+    for (int i = 0; i < q.seed_k; i++) {
+      if (q.seed_vars[i] < 0 || q.seed_vars[i] >= GSM_MAX_VARS)
+        return set_error(GSM_ERR_VALUE, "seed variable index out of range");
+      for (int j = 0; j < i; j++)
+        if (q.seed_vars[j] == q.seed_vars[i]) return set_error(GSM_ERR_VALUE, "duplicate seed variable");
+    }
+  }
   return GSM_OK;
 }
 
@@ -2257,6 +2387,13 @@ static gsm_status begin_query(gsm_context* c, const QueryArgs& q, ExecState& S) 
   gsm_status v = validate_query(c, q);
   if (v != GSM_OK) return v;
   GSM_CUDA(cudaSetDevice(c->device));
+  if (q.seed_k > 0 && q.seed_n > 0) {  // the seed must fit one arena half
+    const size_t need = 8 * (size_t)q.seed_k * (size_t)q.seed_n;
+    if (c->arena_bytes < need) {
+      gsm_status s2 = ctx_set_arena(c, need + need / 4);
+      if (s2 != GSM_OK) return s2;
+    }
+  }
   S.timing = q.rep && q.rep->device_ms;
   return launch_query(c, q, S);
 }
@@ -2493,6 +2630,28 @@ gsm_status gsm_execute(gsm_context* c, const gsm_pattern* steps, int32_t n, cons
   return complete_query(c, qa, S, out);
 }
 
+gsm_status gsm_execute_seeded(gsm_context* c, const uint32_t* seed_rows, int64_t n_seed,
+                              const int32_t* seed_vars, int32_t seed_k, const gsm_pattern* steps,
+                              int32_t n_steps, const int32_t* proj, int32_t n_proj,
+                              int32_t distinct, int64_t budget, int32_t budget_mode,
+                              gsm_report* rep, gsm_result** out) {
+  *out = nullptr;
+  if (n_steps < 0 || n_steps >= GSM_MAX_STEPS || (n_steps > 0 && !steps))
+    return set_error(GSM_ERR_VALUE, "bad seeded plan");
+  std::vector<gsm_pattern> all((size_t)n_steps + 1);
+  all[0] = gsm_pattern{-1, -1, 0, 0, 0, 1};  // placeholder: step 0 is the seed
+  for (int i = 0; i < n_steps; i++) all[(size_t)i + 1] = steps[i];
+  QueryArgs qa{all.data(), n_steps + 1, proj, n_proj, distinct, budget, budget_mode, 0, 1, rep};
+  qa.seed = seed_rows;
+  qa.seed_n = n_seed;
+  qa.seed_vars = seed_vars;
+  qa.seed_k = seed_k;
+  ExecState S;
+  gsm_status st = begin_query(c, qa, S);
+  if (st != GSM_OK) return st;
+  return complete_query(c, qa, S, out);
+}
+
 gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
                              gsm_status* statuses, gsm_result** outs, float* device_ms) {
   if (n_queries < 0 || (n_queries > 0 && (!ctxs || !queries || !outs)))
@@ -2679,7 +2838,7 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
   TJ_CUDA(alloc((void**)&Lcols, 4 * (size_t)n_left * a));
   if (n_left * a) {
     k_rows_to_cols<<<std::max(1, std::min(c->grid_ts, (int)((n_left * a + 255) / 256))), 256, 0, st>>>(
-        dL, n_left, a, Lcols);
+        dL, n_left, a, Lcols, n_left);
     count_launch();
   }
   i64* dcnt;
@@ -2778,6 +2937,64 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
     return set_error(GSM_ERR_RESOURCE, msg);
   }
   *out = r;
+  return GSM_OK;
+}
+
+gsm_status gsm_partition_rows(gsm_context* c, const uint32_t* rows, int64_t n, int32_t k,
+                              int32_t key_col, int64_t node_count, int32_t parts,
+                              uint32_t* out_rows, int64_t* counts) {
+  if (!c) return set_error(GSM_ERR_VALUE, "null context");
+  if (n < 0 || k < 0 || k > GSM_MAX_VARS || parts < 1 || parts > 4096 || key_col >= k || !counts ||
+      (n > 0 && k > 0 && (!rows || !out_rows)))
+    return set_error(GSM_ERR_VALUE, "bad partition arguments");
+  GSM_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  for (int d = 0; d < parts; d++) counts[d] = 0;
+  if (n == 0) return GSM_OK;
+  if (k == 0) {  // zero-arity rows carry no key: all to destination 0
+    counts[0] = n;
+    return GSM_OK;
+  }
+  unsigned long long* dcnt = nullptr;
+  GSM_CUDA(cudaMallocAsync((void**)&dcnt, 16 * (size_t)parts, st));
+  GSM_CUDA(cudaMemsetAsync(dcnt, 0, 8 * (size_t)parts, st));
+  const int grid = (int)std::max<i64>(1, std::min<i64>(c->grid_ts, (n + 255) / 256));
+  k_part_count<<<grid, 256, 4 * (size_t)parts, st>>>(rows, n, k, key_col, (u64)node_count, (u32)parts, dcnt);
+  count_launch();
+  std::vector<unsigned long long> h((size_t)parts);
+  GSM_CUDA(cudaMemcpyAsync(h.data(), dcnt, 8 * (size_t)parts, cudaMemcpyDeviceToHost, st));
+  GSM_CUDA(cudaStreamSynchronize(st));
+  std::vector<unsigned long long> cur((size_t)parts);
+  unsigned long long acc = 0;
+  for (int d = 0; d < parts; d++) {
+    counts[d] = (int64_t)h[(size_t)d];
+    cur[(size_t)d] = acc;
+    acc += h[(size_t)d];
+  }
+  unsigned long long* dcur = dcnt + parts;
+  GSM_CUDA(cudaMemcpyAsync(dcur, cur.data(), 8 * (size_t)parts, cudaMemcpyHostToDevice, st));
+  k_part_scatter<<<grid, 256, 0, st>>>(rows, n, k, key_col, (u64)node_count, (u32)parts, dcur, out_rows);
+  count_launch();
+  GSM_CUDA(cudaGetLastError());
+  GSM_CUDA(cudaFreeAsync(dcnt, st));
+  GSM_CUDA(cudaStreamSynchronize(st));
+  return GSM_OK;
+}
+
+gsm_status gsm_cross_rows(gsm_context* c, const uint32_t* left, int64_t n_left, int32_t a,
+                          const uint32_t* right, int64_t n_right, int32_t b, uint32_t* out) {
+  if (!c) return set_error(GSM_ERR_VALUE, "null context");
+  if (n_left < 0 || n_right < 0 || a < 0 || b < 0 || a + b > GSM_MAX_VARS)
+    return set_error(GSM_ERR_VALUE, "bad cross product arguments");
+  const i64 total = Exec::sat_mul(n_left, n_right);
+  if (total == 0 || a + b == 0) return GSM_OK;
+  if ((a && !left) || (b && !right) || !out) return set_error(GSM_ERR_VALUE, "null table");
+  GSM_CUDA(cudaSetDevice(c->device));
+  const int grid = (int)std::max<i64>(1, std::min<i64>((i64)c->grid_ts * 4, (total + 255) / 256));
+  k_cross_rows<<<grid, 256, 0, c->stream>>>(left, n_left, a, right, n_right, b, out);
+  count_launch();
+  GSM_CUDA(cudaGetLastError());
+  GSM_CUDA(cudaStreamSynchronize(c->stream));
   return GSM_OK;
 }
 

@@ -243,23 +243,31 @@ gsm_status gsm_store_create(int32_t device, int64_t node_count, int32_t max_pid,
 
 gsm_status gsm_store_put_predicate(gsm_store* s, int32_t pid, const uint64_t* so_pairs,
                                    const uint64_t* os_pairs, int64_t nnz) {
+  return gsm_store_put_predicate_shard(s, pid, so_pairs, nnz, os_pairs, nnz);
+}
+
+gsm_status gsm_store_put_predicate_shard(gsm_store* s, int32_t pid, const uint64_t* so_pairs,
+                                         int64_t nnz_so, const uint64_t* os_pairs, int64_t nnz_os) {
   if (!s) return set_error(GSM_ERR_VALUE, "null store");
   if (s->finalized) return set_error(GSM_ERR_VALUE, "store already finalized");
   if (pid < 1 || pid > s->max_pid) return set_error(GSM_ERR_UNKNOWN_PREDICATE, "no matrix for predicate id " + std::to_string(pid));
-  if (nnz < 0 || nnz >= 0xFFFFFFF0LL)
+  if (nnz_so < 0 || nnz_so >= 0xFFFFFFF0LL || nnz_os < 0 || nnz_os >= 0xFFFFFFF0LL)
     return set_error(GSM_ERR_VALUE, "predicate pair count must be < 2^32");
-  if (nnz > 0 && (!so_pairs || !os_pairs)) return set_error(GSM_ERR_VALUE, "null pair array");
+  if ((nnz_so > 0 && !so_pairs) || (nnz_os > 0 && !os_pairs)) return set_error(GSM_ERR_VALUE, "null pair array");
   GSM_CUDA(cudaSetDevice(s->device));
   PredDev& p = s->preds[pid];
   if (p.present) return set_error(GSM_ERR_VALUE, "predicate uploaded twice");
   p.present = 1;
   const i64 CHUNK = 1 << 24;  // 16M pairs = 256 MiB staging
+  const i64 nmax = std::max(nnz_so, nnz_os);
   u64* stage = nullptr;
-  if (nnz > 0) GSM_CUDA(cudaMalloc(&stage, 16 * (size_t)std::min<i64>(nnz, CHUNK)));
+  if (nmax > 0) GSM_CUDA(cudaMalloc(&stage, 16 * (size_t)std::min<i64>(nmax, CHUNK)));
   const uint64_t* hosts[2] = {so_pairs, os_pairs};
+  const i64 counts[2] = {nnz_so, nnz_os};
   Orient* ors[2] = {&p.so, &p.os};
   for (int w = 0; w < 2; w++) {
     Orient& o = *ors[w];
+    const i64 nnz = counts[w];
     u32 *src, *dst;
     GSM_CUDA(store_alloc(s, (void**)&src, 4 * (size_t)nnz));
     GSM_CUDA(store_alloc(s, (void**)&dst, 4 * (size_t)nnz));
@@ -299,9 +307,9 @@ gsm_status gsm_store_put_predicate(gsm_store* s, int32_t pid, const uint64_t* so
     }
   }
   if (stage) cudaFree(stage);
-  build_host_aux(so_pairs, nnz, s->aux_so[pid]);
-  build_host_aux(os_pairs, nnz, s->aux_os[pid]);
-  s->max_nnz = std::max<u32>(s->max_nnz, (u32)nnz);
+  build_host_aux(so_pairs, nnz_so, s->aux_so[pid]);
+  build_host_aux(os_pairs, nnz_os, s->aux_os[pid]);
+  s->max_nnz = std::max<u32>(s->max_nnz, (u32)nmax);
   GSM_CUDA(cudaGetLastError());
   return GSM_OK;
 }

@@ -68,12 +68,13 @@ class DeviceStore:
     """A store whose predicate matrices are resident on one CUDA device."""
 
     def __init__(self, dictionary, matrices: dict[int, PairMatrix], stats: dict[int, StatEntry],
-                 node_count: int, device: int = 0):
+                 node_count: int, device: int = 0, shard: tuple[int, int] | None = None):
         self.dictionary = dictionary
         self.matrices = matrices
         self.stats = stats
         self.device = device
         self.node_count = int(node_count)
+        self.shard = shard  # (index, count) of a sharded store, else None
         self._handle = C.c_void_p()
         self._ctx = threading.local()
         self._contexts: list[C.c_void_p] = []
@@ -87,8 +88,8 @@ class DeviceStore:
             m = matrices[pid]
             so = np.ascontiguousarray(m.so, dtype=np.uint64)
             os_ = np.ascontiguousarray(m.os, dtype=np.uint64)
-            _lib.check(L.gsm_store_put_predicate(self._handle, pid, so.ctypes.data,
-                                                 os_.ctypes.data, so.shape[0]))
+            _lib.check(L.gsm_store_put_predicate_shard(self._handle, pid, so.ctypes.data,
+                                                       so.shape[0], os_.ctypes.data, os_.shape[0]))
         _lib.check(L.gsm_store_finalize(self._handle))
 
     @staticmethod
@@ -168,8 +169,25 @@ def _read_pairs(path: Path) -> np.ndarray:
     return arr.reshape(-1, 2)
 
 
-def load(directory: Path | str, device: int = 0) -> DeviceStore:
-    """storage.load (storage.py:222-271) into device memory."""
+def shard_owner(ids: np.ndarray, node_count: int, shards: int) -> np.ndarray:
+    """Owner shard of node ids: contiguous id ranges, owner(id) =
+    (id - 1) * shards // node_count (the device's shard_of, gsm_exec.cu)."""
+    ids = np.asarray(ids, dtype=np.uint64)
+    if node_count <= 0:
+        return np.zeros(ids.shape, dtype=np.int64)
+    o = ((np.maximum(ids, 1) - 1) * np.uint64(shards)) // np.uint64(node_count)
+    return np.minimum(o, shards - 1).astype(np.int64)
+
+
+def load(directory: Path | str, device: int = 0, shard: tuple[int, int] | None = None) -> DeviceStore:
+    """storage.load (storage.py:222-271) into device memory.
+
+    ``shard=(i, n)`` keeps only shard i of n (SURVEY.md §8(e) sharded mode):
+    the CSR rows of subjects and the CSC rows of objects whose ids fall in
+    range i (:func:`shard_owner`).  Validation and ``stats`` are global, so
+    every shard plans a query identically."""
+    if shard is not None and not (0 <= shard[0] < shard[1]):
+        raise ValueError(f"bad shard {shard}")
     directory = Path(directory)
     meta_path = directory / META_FILE
     if not meta_path.exists():
@@ -212,11 +230,14 @@ def load(directory: Path | str, device: int = 0) -> DeviceStore:
             )
         if os_.shape[0] != so.shape[0]:
             raise StoreFormatError(f"{os_path}: {os_.shape[0]} pairs but {so_path} has {so.shape[0]}")
-        matrices[pid] = PairMatrix(pid, so, os_)
         total += so.shape[0]
+        if shard is not None:
+            so = so[shard_owner(so[:, 0], node_count, shard[1]) == shard[0]]
+            os_ = os_[shard_owner(os_[:, 0], node_count, shard[1]) == shard[0]]
+        matrices[pid] = PairMatrix(pid, so, os_)
     if total != triple_count:
         raise StoreFormatError(f"meta declares {triple_count} triples but store holds {total}")
-    return DeviceStore(dictionary, matrices, stats, node_count, device=device)
+    return DeviceStore(dictionary, matrices, stats, node_count, device=device, shard=shard)
 
 
 # Reference Store objects are unhashable dataclasses: cache by id() and keep
