@@ -21,6 +21,7 @@
 // stores), rows of >= 32 candidates warp-cooperatively, and hub rows of the
 // power-law tail (>= 256) as 1024-output pieces drained by k_drain on every SM.
 #include <algorithm>
+#include <atomic>
 #include <utility>
 #include <cstdio>
 #include <cstdlib>
@@ -1507,6 +1508,7 @@ struct gsm_context {
   bool use_fusion = true;  // fuse [filters][expand][filters] step groups into one kernel
   bool use_defer = true;   // spread hub rows over all SMs (k_drain)
   bool use_proj_fusion = true;  // write the projected result from the last join
+  bool use_batch_graph = true;  // a repeated batch replays as one graph (gsm_execute_batch)
   // A prepared plan: the captured launch sequence plus what the host needs
   // to replay and complete it without re-planning.
   struct GraphEntry {
@@ -1522,6 +1524,19 @@ struct gsm_context {
     std::vector<int> kinds, arities;
   };
   std::unordered_map<std::string, GraphEntry> graphs;
+  // A prepared batch (gsm_execute_batch with this context first): the launch
+  // sequences of several queries on several contexts captured as ONE graph
+  // (fork/join over the contexts' streams), so a repeated batch costs one
+  // graph launch instead of one per query.  Valid while every member
+  // context's buffers are unchanged (bufgen).
+  struct BatchEntry {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<u64> bufgens;
+    std::vector<GraphEntry> metas;  // per query (exec unused)
+  };
+  std::unordered_map<std::string, BatchEntry> batches;
+  u64 bufgen = 0;  // process-unique; renewed whenever captured pointers change
+  cudaEvent_t ev_fork = nullptr;
 };
 
 namespace gsm {
@@ -1533,9 +1548,17 @@ namespace {
 
 // Captured graphs embed arena / staging / status pointers: drop them whenever
 // one of those buffers is reallocated.
+u64 next_bufgen() {
+  static std::atomic<u64> g{0};
+  return ++g;
+}
+
 void ctx_clear_graphs(gsm_context* c) {
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
   c->graphs.clear();
+  for (auto& kv : c->batches) cudaGraphExecDestroy(kv.second.exec);
+  c->batches.clear();
+  c->bufgen = next_bufgen();
 }
 
 gsm_status ctx_set_arena(gsm_context* c, size_t bytes) {
@@ -1715,6 +1738,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* nf = getenv("GSM_NO_FUSION")) c->use_fusion = !(nf[0] == '1');
   if (const char* nd = getenv("GSM_NO_DEFER")) c->use_defer = !(nd[0] == '1');
   if (const char* npf = getenv("GSM_NO_PROJ_FUSION")) c->use_proj_fusion = !(npf[0] == '1');
+  if (const char* nb = getenv("GSM_NO_BATCH_GRAPH")) c->use_batch_graph = !(nb[0] == '1');
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
     return st;
@@ -1730,7 +1754,8 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(cuda_error(e, "cudaEventCreate"));
   if ((e = cudaEventCreate(&c->ev_q0)) != cudaSuccess || (e = cudaEventCreate(&c->ev_q1)) != cudaSuccess ||
       (e = cudaEventCreate(&c->ev_q2)) != cudaSuccess || (e = cudaEventCreate(&c->ev_b0)) != cudaSuccess ||
-      (e = cudaEventCreate(&c->ev_b1)) != cudaSuccess || (e = cudaEventCreate(&c->ev_done)) != cudaSuccess)
+      (e = cudaEventCreate(&c->ev_b1)) != cudaSuccess || (e = cudaEventCreate(&c->ev_done)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess)
     return fail(cuda_error(e, "cudaEventCreate"));
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -1767,7 +1792,7 @@ gsm_status gsm_context_free(gsm_context* c) {
   if (c->ev_q0) cudaEventDestroy(c->ev_q0);
   if (c->ev_q1) cudaEventDestroy(c->ev_q1);
   if (c->ev_q2) cudaEventDestroy(c->ev_q2);
-  for (cudaEvent_t ev : {c->ev_b0, c->ev_b1, c->ev_done})
+  for (cudaEvent_t ev : {c->ev_b0, c->ev_b1, c->ev_done, c->ev_fork})
     if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1805,7 +1830,51 @@ struct ExecState {
   bool timing = false;
   std::string plan_key;
   std::vector<int> kinds, arities;  // per step (report, budget checks)
+  // Batch capture: the caller holds c->stream inside a stream capture; only
+  // issue the launch sequence into it and describe it in `meta`.
+  bool capture_only = false;
+  gsm_context::GraphEntry meta;
+  cudaStream_t sync_stream = nullptr;  // first completion waits here (batch graph)
 };
+
+// Restore a prepared plan into the context: query-block image with fresh
+// epochs, and the host-side facts the completion needs.
+static void apply_entry(gsm_context* c, const gsm_context::GraphEntry& P, ExecState& S) {
+  QueryBlock* hb = c->h_block;
+  memcpy(hb, P.image.data(), P.image.size());
+  for (int i = 0; i < P.n_epochs; i++) hb->epochs[i] = next_epoch(c);
+  S.pack_stat = P.pack_stat;
+  S.pack_cap = P.pack_cap;
+  S.pack_out = P.pack_out;
+  S.fused = P.fused;
+  S.kernels = P.kernels;
+  S.h2d = P.h2d;
+  S.kinds = P.kinds;
+  S.arities = P.arities;
+}
+
+// Plan key: everything a query's launch sequence derives from, including the
+// D2H size guess (the last result size of this plan rounded up to a power of
+// two, >= 4 KiB, else 64 KiB; never more than the staging buffer), which this
+// sets in c->guess.  S.plan_key gets the key without the guess.
+static std::string query_key(gsm_context* c, const QueryArgs& qa, ExecState& S) {
+  std::string key;
+  auto put = [&key](const void* p, size_t b) { key.append(reinterpret_cast<const char*>(p), b); };
+  put(qa.steps, sizeof(gsm_pattern) * (size_t)qa.n);
+  put(qa.proj, sizeof(int32_t) * (size_t)qa.n_proj);
+  const i64 scal[] = {qa.n, qa.n_proj, qa.distinct != 0, S.allow_fuse, S.timing, qa.budget, qa.part, qa.parts};
+  put(scal, sizeof scal);
+  auto lb = c->last_bytes.find(key);
+  size_t g = 65536;
+  if (lb != c->last_bytes.end()) {
+    g = 4096;
+    while (g < lb->second) g <<= 1;
+  }
+  c->guess = std::min(g, c->stage_bytes);
+  S.plan_key = key;
+  key.append(reinterpret_cast<const char*>(&c->guess), sizeof c->guess);
+  return key;
+}
 
 // Plan the query and enqueue its whole launch sequence (as a CUDA graph
 // replay when possible) on the context's stream.  Does not synchronize.
@@ -1825,53 +1894,21 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   u32*& pack_out = S.pack_out;
   int& kernels = S.kernels;
   i64& h2d = S.h2d;
-  std::string& last_key = S.plan_key;
   kernels = 0;
   QueryBlock* hb = c->h_block;
   cudaStream_t st = c->stream;
 
-  // Plan key: everything the launch sequence's parameters derive from.
-  std::string key;
-  {
-    auto put = [&key](const void* p, size_t b) { key.append(reinterpret_cast<const char*>(p), b); };
-    put(steps, sizeof(gsm_pattern) * (size_t)n);
-    put(proj, sizeof(int32_t) * (size_t)n_proj);
-    const i64 scal[] = {n, n_proj, distinct, allow_fuse, timing, budget, part, parts};
-    put(scal, sizeof scal);
-  }
-  {
-    // D2H size guess: the last result size of this plan rounded up to a power
-    // of two (>= 4 KiB), else 64 KiB; never more than the staging buffer.
-    auto lb = c->last_bytes.find(key);
-    size_t g = 65536;
-    if (lb != c->last_bytes.end()) {
-      g = 4096;
-      while (g < lb->second) g <<= 1;
-    }
-    c->guess = std::min(g, c->stage_bytes);
-  }
-  last_key = key;
-  key.append(reinterpret_cast<const char*>(&c->guess), sizeof c->guess);
+  std::string key = query_key(c, qa, S);
 
   // Prepared plan: replay the captured launch sequence with the saved
   // query-block image and fresh epochs — no re-planning on the host.
   // (Seeded queries read a caller buffer: never cached.)
-  const bool graphs = c->use_graphs && qa.seed_k < 0;
+  const bool graphs = c->use_graphs && qa.seed_k < 0 && !S.capture_only;
   if (graphs) {
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
-      const auto& P = it->second;
-      memcpy(hb, P.image.data(), P.image.size());
-      for (int i = 0; i < P.n_epochs; i++) hb->epochs[i] = next_epoch(c);
-      pack_stat = P.pack_stat;
-      pack_cap = P.pack_cap;
-      pack_out = P.pack_out;
-      S.fused = P.fused;
-      kernels = P.kernels;
-      h2d = P.h2d;
-      S.kinds = P.kinds;
-      S.arities = P.arities;
-      GSM_CUDA(cudaGraphLaunch(P.exec, st));
+      apply_entry(c, it->second, S);
+      GSM_CUDA(cudaGraphLaunch(it->second.exec, st));
       count_launch(kernels);
       return GSM_OK;
     }
@@ -2314,6 +2351,24 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     S.kinds[q] = (int)ex.plan[q].kind;
     S.arities[q] = (int)ex.plan[q].schema.size();
   }
+  if (S.capture_only) {  // the caller's capture records the sequence
+    capturing = true;
+    gsm_status is = issue();
+    capturing = false;
+    if (is != GSM_OK) return is;
+    gsm_context::GraphEntry& P = S.meta;
+    P.kernels = kernels;
+    P.image.assign(reinterpret_cast<const char*>(hb), reinterpret_cast<const char*>(hb) + used);
+    P.n_epochs = n_epoch_slots;
+    P.pack_stat = pack_stat;
+    P.pack_cap = pack_cap;
+    P.pack_out = pack_out;
+    P.fused = S.fused;
+    P.h2d = h2d;
+    P.kinds = S.kinds;
+    P.arities = S.arities;
+    return GSM_OK;
+  }
   if (graphs) {
     cudaGraphExec_t ge = nullptr;
     {
@@ -2419,7 +2474,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
       gsm_status stt = launch_query(c, qa, S);
       if (stt != GSM_OK) return stt;
     }
-    GSM_CUDA(cudaStreamSynchronize(c->stream));
+    GSM_CUDA(cudaStreamSynchronize(attempt == 0 && S.sync_stream ? S.sync_stream : c->stream));
     memcpy(c->h_block->stats, c->h_stage, sizeof(StepStat) * (size_t)(n + 1));
     const QueryBlock* hb = c->h_block;
     // Budget checks in plan order (executor.py:158-163, 192-193, 237-241).
@@ -2652,6 +2707,114 @@ gsm_status gsm_execute_seeded(gsm_context* c, const uint32_t* seed_rows, int64_t
   return complete_query(c, qa, S, out);
 }
 
+namespace {
+// Make sure the next `need` epochs of a context need no status re-zeroing
+// (next_epoch's wrap enqueues a memset on the context's own stream, which a
+// batch graph launched on another stream would not be ordered after).
+gsm_status epoch_headroom(gsm_context* c, int need) {
+  if (c->epoch + (u32)need + 1 <= EPOCH_MAX) return GSM_OK;
+  GSM_CUDA(cudaMemsetAsync(c->d_status, 0, c->n_status * sizeof(u64), c->stream));
+  GSM_CUDA(cudaStreamSynchronize(c->stream));
+  c->epoch = 0;
+  return GSM_OK;
+}
+
+// Enqueue a whole batch as ONE graph launch on ctxs[0]'s stream (captured on
+// first use as a fork/join over the contexts' streams, then replayed).
+// Returns false (nothing enqueued, S reset) when the batch cannot use a
+// prepared batch graph; the caller then launches the queries one by one.
+bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>& qa,
+                        std::vector<ExecState>& S, bool timed) {
+  gsm_context* c0 = ctxs[0];
+  if (n < 2 || !c0->use_batch_graph) return false;
+  for (int i = 0; i < n; i++) {
+    if (!ctxs[i]->use_graphs || ctxs[i]->device != c0->device || qa[i].seed_k >= 0) return false;
+    if (validate_query(ctxs[i], qa[i]) != GSM_OK) return false;
+  }
+  if (cudaSetDevice(c0->device) != cudaSuccess) return false;
+  for (int i = 0; i < n; i++)
+    if (epoch_headroom(ctxs[i], GSM_MAX_STEPS + 4) != GSM_OK) return false;
+  std::string bkey;
+  std::vector<std::string> keys((size_t)n);
+  for (int i = 0; i < n; i++) {
+    S[i].timing = qa[i].rep && qa[i].rep->device_ms;
+    keys[i] = query_key(ctxs[i], qa[i], S[i]);
+    const gsm_context* cp = ctxs[i];
+    bkey.append(reinterpret_cast<const char*>(&cp), sizeof cp);
+    const u64 kl = keys[i].size();
+    bkey.append(reinterpret_cast<const char*>(&kl), sizeof kl);
+    bkey += keys[i];
+  }
+  cudaStream_t s0 = c0->stream;
+  auto it = c0->batches.find(bkey);
+  if (it != c0->batches.end()) {
+    bool ok = true;
+    for (int i = 0; i < n && ok; i++) ok = it->second.bufgens[i] == ctxs[i]->bufgen;
+    if (!ok) {
+      cudaGraphExecDestroy(it->second.exec);
+      c0->batches.erase(it);
+      it = c0->batches.end();
+    }
+  }
+  if (it == c0->batches.end()) {
+    // Capture: fork every context's stream off s0, issue each query's launch
+    // sequence on its own stream, join back into s0.
+    if (c0->batches.size() >= 64) {
+      for (auto& kv : c0->batches) cudaGraphExecDestroy(kv.second.exec);
+      c0->batches.clear();
+    }
+    if (cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    bool ok = cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
+    for (int i = 1; i < n && ok; i++) ok = cudaStreamWaitEvent(ctxs[i]->stream, c0->ev_fork, 0) == cudaSuccess;
+    for (int i = 0; i < n && ok; i++) {
+      S[i].capture_only = true;
+      ok = launch_query(ctxs[i], qa[i], S[i]) == GSM_OK;
+      S[i].capture_only = false;
+    }
+    for (int i = 1; i < n && ok; i++)
+      ok = cudaEventRecord(ctxs[i]->ev_done, ctxs[i]->stream) == cudaSuccess &&
+           cudaStreamWaitEvent(s0, ctxs[i]->ev_done, 0) == cudaSuccess;
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(s0, &g);
+    cudaGraphExec_t ge = nullptr;
+    if (ok && ce == cudaSuccess && g) ok = cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+    else ok = false;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+      cudaGetLastError();
+      for (int i = 0; i < n; i++) S[i] = ExecState();
+      return false;
+    }
+    gsm_context::BatchEntry E;
+    E.exec = ge;
+    for (int i = 0; i < n; i++) {
+      E.bufgens.push_back(ctxs[i]->bufgen);
+      E.metas.push_back(std::move(S[i].meta));
+    }
+    it = c0->batches.emplace(bkey, std::move(E)).first;
+    // the capture planned every query: its query-block image is in place
+    for (int i = 0; i < n; i++) count_launch(S[i].kernels);
+  } else {
+    for (int i = 0; i < n; i++) {
+      ctxs[i]->gen++;
+      apply_entry(ctxs[i], it->second.metas[i], S[i]);
+      count_launch(S[i].kernels);
+    }
+  }
+  if (timed && cudaEventRecord(c0->ev_b0, s0) != cudaSuccess) return false;
+  if (cudaGraphLaunch(it->second.exec, s0) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (timed) cudaEventRecord(c0->ev_b1, s0);
+  for (int i = 0; i < n; i++) S[i].sync_stream = s0;
+  return true;
+}
+}  // namespace
+
 gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
                              gsm_status* statuses, gsm_result** outs, float* device_ms) {
   if (n_queries < 0 || (n_queries > 0 && (!ctxs || !queries || !outs)))
@@ -2667,27 +2830,33 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
   std::vector<std::string> msg((size_t)n_queries);
   const bool timed = device_ms && n_queries > 0;
   if (device_ms) *device_ms = 0.f;
-  if (timed) {  // all streams start after ev_b0 ...
-    GSM_CUDA(cudaSetDevice(ctxs[0]->device));
-    GSM_CUDA(cudaEventRecord(ctxs[0]->ev_b0, ctxs[0]->stream));
-    for (int i = 1; i < n_queries; i++) GSM_CUDA(cudaStreamWaitEvent(ctxs[i]->stream, ctxs[0]->ev_b0, 0));
-  }
-  // Phase 1: enqueue every query on its own context's stream (they overlap).
   for (int i = 0; i < n_queries; i++) {
     const gsm_query& q = queries[i];
     qa[i] = QueryArgs{q.steps, q.n_steps, q.proj, q.n_proj, q.distinct, q.row_budget,
                       q.budget_mode, q.part_index, q.part_count, q.report};
-    st[i] = begin_query(ctxs[i], qa[i], S[i]);
-    if (st[i] != GSM_OK) msg[i] = gsm_last_error();
   }
-  if (timed) {  // ... and ev_b1 on stream 0 follows all of them
-    for (int i = 1; i < n_queries; i++) {
-      GSM_CUDA(cudaEventRecord(ctxs[i]->ev_done, ctxs[i]->stream));
-      GSM_CUDA(cudaStreamWaitEvent(ctxs[0]->stream, ctxs[i]->ev_done, 0));
+  // Fast path: the whole batch as one prepared graph launch.
+  const bool as_graph = launch_batch_graph(ctxs, n_queries, qa, S, timed);
+  if (!as_graph) {
+    if (timed) {  // all streams start after ev_b0 ...
+      GSM_CUDA(cudaSetDevice(ctxs[0]->device));
+      GSM_CUDA(cudaEventRecord(ctxs[0]->ev_b0, ctxs[0]->stream));
+      for (int i = 1; i < n_queries; i++) GSM_CUDA(cudaStreamWaitEvent(ctxs[i]->stream, ctxs[0]->ev_b0, 0));
     }
-    GSM_CUDA(cudaEventRecord(ctxs[0]->ev_b1, ctxs[0]->stream));
+    // Enqueue every query on its own context's stream (they overlap).
+    for (int i = 0; i < n_queries; i++) {
+      st[i] = begin_query(ctxs[i], qa[i], S[i]);
+      if (st[i] != GSM_OK) msg[i] = gsm_last_error();
+    }
+    if (timed) {  // ... and ev_b1 on stream 0 follows all of them
+      for (int i = 1; i < n_queries; i++) {
+        GSM_CUDA(cudaEventRecord(ctxs[i]->ev_done, ctxs[i]->stream));
+        GSM_CUDA(cudaStreamWaitEvent(ctxs[0]->stream, ctxs[i]->ev_done, 0));
+      }
+      GSM_CUDA(cudaEventRecord(ctxs[0]->ev_b1, ctxs[0]->stream));
+    }
   }
-  // Phase 2: complete in order (budget checks, retries, result hand-off).
+  // Complete in order (budget checks, retries, result hand-off).
   gsm_status first = GSM_OK;
   std::string first_msg;
   for (int i = 0; i < n_queries; i++) {

@@ -285,17 +285,32 @@ def test_execute_batch_matches_sequential(store_factory):
     the same bags and reports as one-by-one execution; errors propagate."""
     store = g.load(store_factory("lubm", univ=3, seed=2))
     items = [_plan(store, text) for _, text in lubm_queries()]
-    seq = [g.execute(q, p, store) for q, p in items]
-    for rep_round in range(3):  # first round captures graphs, later rounds replay
-        reps = [g.ExecutionReport() for _ in items]
+    seq_reps = [g.ExecutionReport() for _ in items]
+    seq = [g.execute(q, p, store, report=r) for (q, p), r in zip(items, seq_reps)]
+    # first round captures the batch graph, later rounds replay it; a round
+    # without reports is a different prepared batch
+    for rep_round, with_reports in enumerate([True, True, False, True, False]):
+        reps = [g.ExecutionReport() for _ in items] if with_reports else None
         timing = []
         got = g.execute_batch(items, store, reports=reps, batch_timing=timing)
         assert len(got) == len(seq)
-        for a, b, (q, p), r in zip(got, seq, items, reps):
+        for i, (a, b, (q, p)) in enumerate(zip(got, seq, items)):
             assert orc.fingerprint_array(a.array) == orc.fingerprint_array(b.array)
             assert a.schema == b.schema
-            assert len(r.steps) == len(p.steps)
+            if with_reports:
+                r = reps[i]
+                assert len(r.steps) == len(p.steps)
+                assert [s.rows for s in r.steps] == [s.rows for s in seq_reps[i].steps]
+                assert ([s.prealloc_total for s in r.steps]
+                        == [s.prealloc_total for s in seq_reps[i].steps])
         assert timing and timing[0] > 0
+    # a subset batch on the same contexts, then the full batch again
+    sub = g.execute_batch(items[5:9], store)
+    for a, b in zip(sub, seq[5:9]):
+        assert orc.fingerprint_array(a.array) == orc.fingerprint_array(b.array)
+    again = g.execute_batch(items, store)
+    for a, b in zip(again, seq):
+        assert orc.fingerprint_array(a.array) == orc.fingerprint_array(b.array)
     # a budget violation in one query raises the reference's error
     q9 = dict(lubm_queries())["q09"]
     bad = items[:3] + [_plan(store, q9)]
