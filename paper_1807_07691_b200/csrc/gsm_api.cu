@@ -72,7 +72,12 @@ gsm_status gsm_result_device_ptr(const gsm_result* res, uint64_t* device_ptr) {
   if (res->staged) {  // the device copy of staged rows lives in the context's result buffer
     if (gsm::context_generation(res->ctx) != res->gen)
       return gsm::set_error(GSM_ERR_VALUE, "result invalidated by a later gsm_execute on its context");
-    *device_ptr = (uint64_t)(uintptr_t)gsm::context_device_rows(res->ctx);
+    u32* d = const_cast<u32*>(gsm::context_device_rows(res->ctx));
+    if (res->zc && res->n > 0) {  // zero-copy result: give it a device copy first
+      GSM_CUDA(cudaSetDevice(res->device));
+      GSM_CUDA(cudaMemcpy(d, res->staged, (size_t)res->n * (size_t)res->k * 4, cudaMemcpyHostToDevice));
+    }
+    *device_ptr = (uint64_t)(uintptr_t)d;
     return GSM_OK;
   }
   *device_ptr = (uint64_t)(uintptr_t)res->rows;

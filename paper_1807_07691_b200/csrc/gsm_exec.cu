@@ -42,6 +42,7 @@ constexpr int TS_TILE = TS_THREADS * TS_ITEMS;
 constexpr u64 LB_MASK = (1ull << 40) - 1;
 constexpr int WARP_ROW = 32;  // rows with >= this many candidates are written by a warp
 constexpr u32 EPOCH_MAX = (1u << 22) - 1;
+constexpr size_t ZC_BYTES = (size_t)16 << 10;  // results up to this size are written to host memory directly
 
 struct TileSync {
   u64* status;            // one word per tile: epoch:22 | flag:2 | value:40
@@ -1189,12 +1190,28 @@ struct ResolveArgs {
   ResolveJob job[GSM_MAX_STEPS];
   int njobs;
 };
-__global__ void k_resolve(ResolveArgs args, DTable* tables, StepStat* stats) {
+// First kernel of every query: installs the query block and takes fresh
+// look-back epochs, then resolves the constant-endpoint scans (k_resolve's
+// jobs).  A replayed graph copies a device-resident image of the block
+// (src), so a query needs no host->device copy; src == nullptr when the host
+// uploaded the block itself.  Epochs come from a per-context device counter
+// that the host mirrors (reserve_epochs), so tile status words never need
+// re-zeroing between launches.
+__global__ void k_init(const uint4* __restrict__ src, uint4* __restrict__ dst, int words16, u32* ctr,
+                       u32* epochs, int n_epochs, ResolveArgs res, DTable* tables, StepStat* stats) {
   pdl_wait();
   pdl_trigger();
+  if (src)
+    for (int i = threadIdx.x; i < words16; i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0 && n_epochs > 0) {
+    const u32 base = *ctr;
+    for (int i = 0; i < n_epochs; i++) epochs[i] = base + 1 + (u32)i;
+    *ctr = base + (u32)n_epochs;
+  }
   const int i = threadIdx.x;
-  if (i >= args.njobs) return;
-  const ResolveJob& jb = args.job[i];
+  if (i >= res.njobs) return;
+  const ResolveJob& jb = res.job[i];
   const uint2 sg = seg_lookup(jb.R, jb.k1);
   i64 n;
   if (jb.kind == J_SEG) {
@@ -1495,6 +1512,9 @@ struct gsm_context {
   cudaEvent_t ev_q2 = nullptr;  // end of the (un-captured) DISTINCT tail
   cudaEvent_t ev_b0 = nullptr, ev_b1 = nullptr, ev_done = nullptr;  // batch timing
   // Result staging: [step counters (STAGE_HEAD bytes) | projected rows].
+  u32* d_ctr = nullptr;     // device epoch counter (mirrored by `epoch`)
+  u32* hd_stage = nullptr;  // device alias of h_stage (zero-copy results)
+  u32* hd_rows = nullptr;   // = hd_stage + STAGE_HEAD
   u32* h_stage = nullptr;  // pinned host copy
   u32* d_stage = nullptr;  // device buffer written by the query's last kernel(s)
   u32* h_rows = nullptr;   // = h_stage + STAGE_HEAD
@@ -1521,6 +1541,8 @@ struct gsm_context {
     u32* pack_out = nullptr;
     bool fused = false;
     i64 h2d = 0;
+    bool zc = false;
+    char* d_image = nullptr;  // device copy of `image` (k_init's source)
     std::vector<int> kinds, arities;
   };
   std::unordered_map<std::string, GraphEntry> graphs;
@@ -1553,10 +1575,19 @@ u64 next_bufgen() {
   return ++g;
 }
 
+void free_batch(gsm_context::BatchEntry& b) {
+  cudaGraphExecDestroy(b.exec);
+  for (auto& m : b.metas)
+    if (m.d_image) cudaFree(m.d_image);
+}
+
 void ctx_clear_graphs(gsm_context* c) {
-  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+  for (auto& kv : c->graphs) {
+    cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.d_image) cudaFree(kv.second.d_image);
+  }
   c->graphs.clear();
-  for (auto& kv : c->batches) cudaGraphExecDestroy(kv.second.exec);
+  for (auto& kv : c->batches) free_batch(kv.second);
   c->batches.clear();
   c->bufgen = next_bufgen();
 }
@@ -1582,6 +1613,7 @@ gsm_status ctx_set_arena(gsm_context* c, size_t bytes) {
   c->n_status = max_rows / TS_TILE + 2;
   GSM_CUDA(cudaMalloc(&c->d_status, c->n_status * sizeof(u64)));
   GSM_CUDA(cudaMemset(c->d_status, 0, c->n_status * sizeof(u64)));
+  GSM_CUDA(cudaMemset(c->d_ctr, 0, sizeof(u32)));
   c->epoch = 0;
   return GSM_OK;
 }
@@ -1591,7 +1623,7 @@ gsm_status ctx_set_stage(gsm_context* c, size_t bytes) {
   if (c->h_stage) {
     cudaFreeHost(c->h_stage);
     cudaFree(c->d_stage);
-    c->h_stage = c->d_stage = c->h_rows = c->d_rows = nullptr;
+    c->h_stage = c->d_stage = c->h_rows = c->d_rows = c->hd_stage = c->hd_rows = nullptr;
     c->stage_bytes = 0;
   }
   bytes = (bytes + 4095) & ~(size_t)4095;
@@ -1599,16 +1631,22 @@ gsm_status ctx_set_stage(gsm_context* c, size_t bytes) {
   GSM_CUDA(cudaMalloc(&c->d_stage, bytes + STAGE_HEAD));
   c->h_rows = c->h_stage + STAGE_HEAD / 4;
   c->d_rows = c->d_stage + STAGE_HEAD / 4;
+  GSM_CUDA(cudaHostGetDevicePointer((void**)&c->hd_stage, c->h_stage, 0));
+  c->hd_rows = c->hd_stage + STAGE_HEAD / 4;
   c->stage_bytes = bytes;
   return GSM_OK;
 }
 
-u32 next_epoch(gsm_context* c) {
-  if (++c->epoch > EPOCH_MAX) {
+// Account for `n` epochs that a k_init enqueued next on c->stream will take
+// from the device counter; on wrap-around, re-zero the tile status words and
+// the counter first (stream-ordered).
+void reserve_epochs(gsm_context* c, int n) {
+  if (c->epoch + (u32)n > EPOCH_MAX) {
     cudaMemsetAsync(c->d_status, 0, c->n_status * sizeof(u64), c->stream);
-    c->epoch = 1;
+    cudaMemsetAsync(c->d_ctr, 0, sizeof(u32), c->stream);
+    c->epoch = 0;
   }
-  return c->epoch;
+  c->epoch += (u32)n;
 }
 
 int index_of(const std::vector<int>& v, int x) {
@@ -1704,7 +1742,7 @@ struct Exec {
       j.R = m->so;
       j.k1 = p.s_const;
       j.k2 = p.o_const;
-      d.n = 1;  // upper bound until k_resolve writes the real value
+      d.n = 1;  // upper bound until k_init resolves the real value
     }
     ub[t] = d.n;
     return t;
@@ -1746,6 +1784,8 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   cudaError_t e;
   if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(cuda_error(e, "cudaStreamCreate"));
+  if ((e = cudaMalloc(&c->d_ctr, 16)) != cudaSuccess) return fail(cuda_error(e, "cudaMalloc(epoch counter)"));
+  if ((e = cudaMemset(c->d_ctr, 0, 16)) != cudaSuccess) return fail(cuda_error(e, "cudaMemset"));
   if ((e = cudaMalloc(&c->d_block, sizeof(QueryBlock))) != cudaSuccess)
     return fail(cuda_error(e, "cudaMalloc(query block)"));
   if ((e = cudaMallocHost(&c->h_block, sizeof(QueryBlock))) != cudaSuccess)
@@ -1782,6 +1822,7 @@ gsm_status gsm_context_free(gsm_context* c) {
   if (c->arena) cudaFree(c->arena);
   if (c->d_status) cudaFree(c->d_status);
   if (c->d_block) cudaFree(c->d_block);
+  if (c->d_ctr) cudaFree(c->d_ctr);
   if (c->h_block) cudaFreeHost(c->h_block);
   if (c->d_slots) cudaFree(c->d_slots);
   if (c->d_chunks) cudaFree(c->d_chunks);
@@ -1833,6 +1874,8 @@ struct ExecState {
   // Batch capture: the caller holds c->stream inside a stream capture; only
   // issue the launch sequence into it and describe it in `meta`.
   bool capture_only = false;
+  char* pre_image = nullptr;  // batch capture: the d_image buffer to use
+  bool zc = false;            // counters and result rows written straight to pinned host memory
   gsm_context::GraphEntry meta;
   cudaStream_t sync_stream = nullptr;  // first completion waits here (batch graph)
 };
@@ -1840,9 +1883,8 @@ struct ExecState {
 // Restore a prepared plan into the context: query-block image with fresh
 // epochs, and the host-side facts the completion needs.
 static void apply_entry(gsm_context* c, const gsm_context::GraphEntry& P, ExecState& S) {
-  QueryBlock* hb = c->h_block;
-  memcpy(hb, P.image.data(), P.image.size());
-  for (int i = 0; i < P.n_epochs; i++) hb->epochs[i] = next_epoch(c);
+  reserve_epochs(c, P.n_epochs);  // k_init takes them on the device
+  S.zc = P.zc;
   S.pack_stat = P.pack_stat;
   S.pack_cap = P.pack_cap;
   S.pack_out = P.pack_out;
@@ -2192,7 +2234,13 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   pack_out = reinterpret_cast<u32*>(ex.buf(ph));
   pack_cap = n_proj ? (i64)(ex.half / (4 * (size_t)n_proj)) : ((i64)1 << 62);
   pack_stat = n;
-  const i64 stage_cap = n_proj ? (i64)(c->stage_bytes / (4 * (size_t)n_proj)) : ((i64)1 << 62);
+  // Zero-copy results: when this plan's last result was small, the last
+  // kernel writes the step counters and the projected rows straight into the
+  // pinned staging buffer (no device->host copy in the launch sequence).
+  S.zc = c->guess <= ZC_BYTES;
+  const size_t stage_lim = S.zc ? std::min<size_t>(c->stage_bytes, ZC_BYTES) : c->stage_bytes;
+  const i64 stage_cap = n_proj ? (i64)(stage_lim / (4 * (size_t)n_proj)) : ((i64)1 << 62);
+  u32* const stage_rows = S.zc ? c->hd_rows : c->d_rows;
   // Fuse the projection into the last join when it is an expand/filter and
   // the result goes to the host staging buffer (no DISTINCT).
   bool fused = false;
@@ -2200,7 +2248,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       (launches.back().kind == S_EXPAND || launches.back().kind == S_FILTER ||
        launches.back().kind == S_GROUP)) {
     FusedOut fz;
-    fz.stage = c->d_rows;
+    fz.stage = stage_rows;
     fz.cap = stage_cap;
     fz.k = n_proj;
     for (int j = 0; j < n_proj; j++) fz.pj[j] = pj_idx[j];
@@ -2217,7 +2265,11 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   int n_epoch_slots = 0;
   for (auto& L : launches)
     if (L.kind == S_EXPAND || L.kind == S_FILTER || L.kind == S_GROUP)
-      hb->epochs[n_epoch_slots++] = next_epoch(c);
+      n_epoch_slots++;
+  // k_init takes them from the device counter; mirror it (any wrap-around
+  // re-zeroing is enqueued here, before a capture starts — a batch capture
+  // made room beforehand, epoch_headroom)
+  reserve_epochs(c, n_epoch_slots);
   ProjArgs pa{};
   for (int j = 0; j < n_proj; j++) pa.col[j] = pj_idx[j];
   const size_t used = offsetof(QueryBlock, tables) + sizeof(DTable) * (size_t)ex.ntables;
@@ -2226,6 +2278,18 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // The whole query as one stream-ordered sequence: H2D of the query block,
   // the kernels, D2H of the step counters.  Nothing here writes host memory.
   bool capturing = false;
+  // Graph modes: the device image of the query block that k_init copies.
+  char* d_image = nullptr;
+  if (S.capture_only) {
+    d_image = S.pre_image;
+  } else if (graphs) {
+    GSM_CUDA(cudaMalloc(&d_image, sizeof(QueryBlock)));
+    cudaError_t ce = cudaMemcpy(d_image, hb, used, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+      cudaFree(d_image);
+      return cuda_error(ce, "cudaMemcpy(query image)");
+    }
+  }
   // Under stream capture an event record must be an external node to be
   // timeable; outside capture the flag is illegal.
   auto record = [&](cudaEvent_t ev) -> cudaError_t {
@@ -2235,17 +2299,19 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   auto issue = [&]() -> gsm_status {
     int nk = 0;
     if (timing) GSM_CUDA(record(c->ev_q0));
-    GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
-    if (timing) GSM_CUDA(record(c->ev[0]));
+    // the query block: a replayed graph copies its device image in k_init;
+    // otherwise it is uploaded here
+    if (!d_image) GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
+    if (timing) GSM_CUDA(record(c->ev[0]));  // step 0 (scan) = k_init's constant resolution
+    GSM_CUDA(launch(c->use_pdl, k_init, 1, 256, st, reinterpret_cast<const uint4*>(d_image),
+                    reinterpret_cast<uint4*>(c->d_block), d_image ? (int)((used + 15) / 16) : 0, c->d_ctr,
+                    c->d_block->epochs, n_epoch_slots, ex.res, dT, dS));
+    nk++;
     if (qa.seed_k > 0 && qa.seed_n > 0) {
       const i64 cells = qa.seed_n * qa.seed_k;
       k_rows_to_cols<<<(int)std::max<i64>(1, std::min<i64>(c->grid_ts, (cells + 255) / 256)), 256, 0, st>>>(
           qa.seed, qa.seed_n, qa.seed_k, reinterpret_cast<u32*>(ex.buf(H_A)), ex.cap_for(qa.seed_k));
       GSM_CUDA(cudaGetLastError());
-      nk++;
-    }
-    if (ex.res.njobs > 0) {
-      GSM_CUDA(launch(c->use_pdl, k_resolve, 1, 64, st, ex.res, dT, dS));
       nk++;
     }
     if (parts > 1) {
@@ -2255,7 +2321,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     }
     if (timing) GSM_CUDA(record(c->ev[1]));
     // the query's last kernel exports the step counters to the stage head
-    const ExportArgs xlast{dS, reinterpret_cast<StepStat*>(c->d_stage), n + 1, c->d_block->done};
+    const ExportArgs xlast{dS, reinterpret_cast<StepStat*>(S.zc ? c->hd_stage : c->d_stage), n + 1,
+                           c->d_block->done};
     int last_launch = -1;
     for (int i = (int)launches.size() - 1; i >= 0 && fused; i--)
       if (launches[i].kind != S_EMPTY) {
@@ -2328,7 +2395,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     if (!fused) {
       // DISTINCT reads the packed rows on the device, so only plain
       // projections are packed straight into the pinned staging buffer.
-      u32* host_dst = distinct ? nullptr : c->d_rows;
+      u32* host_dst = distinct ? nullptr : stage_rows;
       GSM_CUDA(launch(c->use_pdl, k_pack, ex.grid_for_rows(ex.ub[cur], 256), 256, st,
                       (const DTable*)(dT + cur), pa, n_proj, pack_out, pack_cap, host_dst,
                       stage_cap, dS + pack_stat, xlast));
@@ -2336,11 +2403,12 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     }
     if (timing) GSM_CUDA(record(c->ev_q1));
     GSM_CUDA(cudaGetLastError());
-    // ONE copy: the step counters (exported by the last kernel) and the
-    // result rows up to this plan's expected size; the host fetches any
-    // remainder after the sync (rare: only when the result grew).
-    GSM_CUDA(cudaMemcpyAsync(c->h_stage, c->d_stage, STAGE_HEAD + (distinct ? 0 : c->guess),
-                             cudaMemcpyDeviceToHost, st));
+    // Not zero-copy: ONE copy of the step counters (exported by the last
+    // kernel) and the result rows up to this plan's expected size; the host
+    // fetches any remainder after the sync (rare: only when the result grew).
+    if (!S.zc)
+      GSM_CUDA(cudaMemcpyAsync(c->h_stage, c->d_stage, STAGE_HEAD + (distinct ? 0 : c->guess),
+                               cudaMemcpyDeviceToHost, st));
     kernels = nk;
     return GSM_OK;
   };
@@ -2365,6 +2433,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     P.pack_out = pack_out;
     P.fused = S.fused;
     P.h2d = h2d;
+    P.zc = S.zc;
+    P.d_image = d_image;
     P.kinds = S.kinds;
     P.arities = S.arities;
     return GSM_OK;
@@ -2379,14 +2449,17 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       capturing = false;
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(st, &g);
-      if (is != GSM_OK) {
+      if (is != GSM_OK || ce != cudaSuccess) {
         if (g) cudaGraphDestroy(g);
-        return is;
+        cudaFree(d_image);
+        return is != GSM_OK ? is : cuda_error(ce, "cudaStreamEndCapture");
       }
-      if (ce != cudaSuccess) return cuda_error(ce, "cudaStreamEndCapture");
       ce = cudaGraphInstantiate(&ge, g, 0);
       cudaGraphDestroy(g);
-      if (ce != cudaSuccess) return cuda_error(ce, "cudaGraphInstantiate");
+      if (ce != cudaSuccess) {
+        cudaFree(d_image);
+        return cuda_error(ce, "cudaGraphInstantiate");
+      }
       gsm_context::GraphEntry P;
       P.exec = ge;
       P.kernels = kernels;
@@ -2397,6 +2470,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       P.pack_out = pack_out;
       P.fused = S.fused;
       P.h2d = h2d;
+      P.zc = S.zc;
+      P.d_image = d_image;
       P.kinds = S.kinds;
       P.arities = S.arities;
       c->graphs.emplace(key, std::move(P));
@@ -2517,10 +2592,12 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
       need_arity = n_proj;
     }
     if (!ovf && hb->stats[pack_stat].pad == 3) {
-      // The fused projection outgrew the pinned staging buffer: re-run with a
-      // device-side pack, and grow staging (<= 1 GiB) for the next query.
+      // The fused projection outgrew the pinned staging buffer (or the
+      // zero-copy limit): re-run with a device-side pack, and grow staging
+      // (<= 1 GiB) for the next query.
       size_t want = (size_t)hb->stats[pack_stat].rows * 4 * (size_t)std::max(n_proj, 1);
-      if (want <= ((size_t)1 << 30)) ctx_set_stage(c, want + want / 4);
+      c->last_bytes[plan_key] = want;
+      if (want > c->stage_bytes && want <= ((size_t)1 << 30)) ctx_set_stage(c, want + want / 4);
       S.allow_fuse = false;
       continue;
     }
@@ -2613,9 +2690,11 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     dp.cap_out = nrows;
     dp.st = c->d_block->stats + pack_stat + 1;
     GSM_CUDA(cudaMemsetAsync(c->d_block->counters + GSM_MAX_STEPS + 2, 0, 4, st));
-    c->h_block->epochs[GSM_MAX_STEPS + 2] = next_epoch(c);
-    GSM_CUDA(cudaMemcpyAsync(c->d_block->epochs + GSM_MAX_STEPS + 2,
-                             c->h_block->epochs + GSM_MAX_STEPS + 2, 4, cudaMemcpyHostToDevice, st));
+    reserve_epochs(c, 1);
+    k_init<<<1, 32, 0, st>>>(nullptr, nullptr, 0, c->d_ctr, c->d_block->epochs + GSM_MAX_STEPS + 2, 1,
+                             ResolveArgs{}, nullptr, nullptr);
+    count_launch();
+    kernels++;
     TileSync ts{c->d_status, c->d_block->counters + GSM_MAX_STEPS + 2,
                 c->d_block->epochs + GSM_MAX_STEPS + 2, 0};
     k_tilescan<DistinctP><<<c->grid_ts, TS_THREADS, 0, st>>>(dp, ts, ExportArgs{});
@@ -2637,12 +2716,10 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     r->n = nrows;
     r->staged = c->h_rows;
     const size_t bytes = (size_t)nrows * row_bytes;
-    if (bytes > c->guess)
+    if (!S.zc && bytes > c->guess)
       GSM_CUDA(cudaMemcpy(reinterpret_cast<char*>(c->h_rows) + c->guess,
                           reinterpret_cast<char*>(c->d_rows) + c->guess, bytes - c->guess,
                           cudaMemcpyDeviceToHost));
-    c->last_bytes[plan_key] = bytes;
-    if (c->last_bytes.size() > 4096) c->last_bytes.clear();
   } else {
     // Result larger than the staging buffer: keep it on the device, and grow
     // the staging buffer (up to 1 GiB) for the next query.
@@ -2657,6 +2734,10 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     GSM_CUDA(cudaStreamSynchronize(st));
     if (bytes > c->stage_bytes && bytes <= ((size_t)1 << 30)) ctx_set_stage(c, bytes + bytes / 4);
   }
+  // the next D2H size guess / zero-copy choice for this plan
+  if (c->last_bytes.size() > 4096) c->last_bytes.clear();
+  c->last_bytes[plan_key] = (size_t)nrows * row_bytes;
+  r->zc = staged && S.zc && !distinct;
   if (rep) {
     rep->kernels = kernels;
     rep->h2d_bytes = h2d;
@@ -2709,11 +2790,12 @@ gsm_status gsm_execute_seeded(gsm_context* c, const uint32_t* seed_rows, int64_t
 
 namespace {
 // Make sure the next `need` epochs of a context need no status re-zeroing
-// (next_epoch's wrap enqueues a memset on the context's own stream, which a
+// (reserve_epochs' wrap enqueues a memset on the context's own stream, which a
 // batch graph launched on another stream would not be ordered after).
 gsm_status epoch_headroom(gsm_context* c, int need) {
   if (c->epoch + (u32)need + 1 <= EPOCH_MAX) return GSM_OK;
   GSM_CUDA(cudaMemsetAsync(c->d_status, 0, c->n_status * sizeof(u64), c->stream));
+  GSM_CUDA(cudaMemsetAsync(c->d_ctr, 0, sizeof(u32), c->stream));
   GSM_CUDA(cudaStreamSynchronize(c->stream));
   c->epoch = 0;
   return GSM_OK;
@@ -2760,17 +2842,31 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     // Capture: fork every context's stream off s0, issue each query's launch
     // sequence on its own stream, join back into s0.
     if (c0->batches.size() >= 64) {
-      for (auto& kv : c0->batches) cudaGraphExecDestroy(kv.second.exec);
+      for (auto& kv : c0->batches) free_batch(kv.second);
       c0->batches.clear();
     }
+    // device images of the query blocks (filled after the capture)
+    std::vector<char*> imgs((size_t)n, nullptr);
+    auto drop_imgs = [&]() {
+      for (char* p : imgs)
+        if (p) cudaFree(p);
+    };
+    for (int i = 0; i < n; i++)
+      if (cudaMalloc(&imgs[i], sizeof(QueryBlock)) != cudaSuccess) {
+        cudaGetLastError();
+        drop_imgs();
+        return false;
+      }
     if (cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
+      drop_imgs();
       return false;
     }
     bool ok = cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
     for (int i = 1; i < n && ok; i++) ok = cudaStreamWaitEvent(ctxs[i]->stream, c0->ev_fork, 0) == cudaSuccess;
     for (int i = 0; i < n && ok; i++) {
       S[i].capture_only = true;
+      S[i].pre_image = imgs[i];
       ok = launch_query(ctxs[i], qa[i], S[i]) == GSM_OK;
       S[i].capture_only = false;
     }
@@ -2783,9 +2879,17 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     if (ok && ce == cudaSuccess && g) ok = cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
     else ok = false;
     if (g) cudaGraphDestroy(g);
+    for (int i = 0; i < n && ok; i++)
+      ok = cudaMemcpy(imgs[i], S[i].meta.image.data(), S[i].meta.image.size(), cudaMemcpyHostToDevice) ==
+           cudaSuccess;
     if (!ok) {
       cudaGetLastError();
-      for (int i = 0; i < n; i++) S[i] = ExecState();
+      if (ge) cudaGraphExecDestroy(ge);
+      drop_imgs();
+      for (int i = 0; i < n; i++) {
+        // the captured plans took epochs from the host mirror only
+        S[i] = ExecState();
+      }
       return false;
     }
     gsm_context::BatchEntry E;

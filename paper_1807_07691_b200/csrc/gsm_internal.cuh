@@ -37,6 +37,7 @@ struct gsm_result {
   const u32* staged = nullptr; // rows in the context's pinned staging buffer
   const gsm_context* ctx = nullptr;
   u64 gen = 0;                 // staging generation the rows belong to
+  bool zc = false;             // staged rows were written to host memory only (no device copy)
 };
 
 namespace gsm {

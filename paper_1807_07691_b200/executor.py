@@ -261,6 +261,56 @@ def _fill_report(report, steps, rep_struct, rows_buf, pre_buf, ms_buf, kind_buf,
     report.kernels += int(rep_struct.kernels)
 
 
+
+class _PreparedBatch:
+    """ctypes records of one batch of (query, plan) items, reused while the
+    plans keep their compiled encoding (see :func:`compile_plan`)."""
+
+    __slots__ = ("items", "compiled", "ctx_arr", "qarr", "outs", "statuses", "nrows", "ncols",
+                 "dsts", "ms", "steps", "schemas")
+
+
+def _prepared_batch(dstore, items, budget_mode: int, budget: int) -> _PreparedBatch:
+    compiled = [compile_plan(q, p) for q, p in items]
+    key = (tuple(map(id, compiled)), budget_mode, budget)
+    cache = dstore.__dict__.setdefault("_batch_prep", {})
+    prep = cache.get(key)
+    if prep is not None and all(a is b for a, b in zip(prep.compiled, compiled)):
+        return prep
+    n = len(items)
+    prep = _PreparedBatch()
+    prep.items = items  # keeps the compiled encodings (and so their ids) alive
+    prep.compiled = compiled
+    ctxs = dstore.context_pool(n)
+    prep.ctx_arr = (C.c_void_p * n)(*[c.value for c in ctxs])
+    prep.qarr = (_lib.Query * n)()
+    for i, ((query, plan), (steps, arr, proj_arr, nproj)) in enumerate(zip(items, compiled)):
+        if not steps:
+            raise ValueError("cannot execute an empty plan")
+        q = prep.qarr[i]
+        q.steps = arr
+        q.n_steps = len(steps)
+        q.proj = proj_arr
+        q.n_proj = nproj
+        q.distinct = 1 if query.distinct else 0
+        q.part_index, q.part_count = 0, 1
+        q.row_budget = budget
+        q.budget_mode = budget_mode
+        q.report = None
+    prep.outs = (C.c_void_p * n)()
+    prep.statuses = (C.c_int32 * n)()
+    prep.nrows = (C.c_int64 * n)()
+    prep.ncols = (C.c_int32 * n)()
+    prep.dsts = (C.c_void_p * n)()
+    prep.ms = C.c_float(0.0)
+    prep.steps = [c[0] for c in compiled]
+    prep.schemas = [tuple(q.projection) for q, _ in items]
+    if len(cache) >= 64:
+        cache.clear()
+    cache[key] = prep
+    return prep
+
+
 def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW_BUDGET,
                   reports: list | None = None, batch_timing: list | None = None) -> list[BindingTable]:
     """Evaluate independent queries concurrently (``gsm_execute_batch``).
@@ -280,58 +330,49 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
     n = len(items)
     budget_mode = _lib.GSM_BUDGET_SEQUENTIAL if mode == "sequential" else _lib.GSM_BUDGET_PARALLEL
     budget = min(int(row_budget), (1 << 63) - 1)
-    ctxs = dstore.context_pool(n)
-    ctx_arr = (C.c_void_p * n)(*[c.value for c in ctxs])
-    qarr = (_lib.Query * n)()
-    prepared = []  # keeps every ctypes buffer alive until the call returns
-    for i, (query, plan) in enumerate(items):
-        if not plan.steps:
-            raise ValueError("cannot execute an empty plan")
-        steps, arr, proj_arr, nproj = compile_plan(query, plan)
-        tmpl = plan.__dict__.get("_gsm_query")
-        if tmpl is None or tmpl[0] is not arr:
-            rec = _lib.Query()
-            rec.steps = arr
-            rec.n_steps = len(steps)
-            rec.proj = proj_arr
-            rec.n_proj = nproj
-            rec.distinct = 1 if query.distinct else 0
-            rec.part_index, rec.part_count = 0, 1
-            tmpl = (arr, rec)
-            try:
-                plan.__dict__["_gsm_query"] = tmpl
-            except (AttributeError, TypeError):
-                pass
-        qarr[i] = tmpl[1]
-        q = qarr[i]
-        q.row_budget = budget
-        q.budget_mode = budget_mode
-        rep_struct, bufs = _new_report(len(steps)) if reports is not None else (None, None)
-        q.report = C.pointer(rep_struct) if rep_struct is not None else None
-        prepared.append((steps, arr, proj_arr, rep_struct, bufs))
-    outs = (C.c_void_p * n)()
-    statuses = (C.c_int32 * n)()
-    ms = C.c_float(0.0)
+    prep = _prepared_batch(dstore, items, budget_mode, budget)
+    qarr = prep.qarr
+    rep_bufs = None
+    if reports is not None:
+        rep_bufs = []
+        for i, (_, plan) in enumerate(items):
+            rep_struct, bufs = _new_report(len(plan.steps))
+            qarr[i].report = C.pointer(rep_struct)
+            rep_bufs.append((rep_struct, bufs))
     L = _lib.lib()
-    st = L.gsm_execute_batch(ctx_arr, n, qarr, statuses, outs,
-                             C.byref(ms) if batch_timing is not None else None)
+    ms = prep.ms
+    try:
+        st = L.gsm_execute_batch(prep.ctx_arr, n, qarr, prep.statuses, prep.outs,
+                                 C.byref(ms) if batch_timing is not None else None)
+    finally:
+        if reports is not None:
+            for i in range(n):
+                qarr[i].report = None
+    outs = prep.outs
     if st != _lib.GSM_OK:
         msg = _lib.last_error()
         L.gsm_results_copy(outs, n, None, 1)
         _lib.raise_status(st, msg)
-    # two calls for all results: shapes, then copy + free
-    nrows = (C.c_int64 * n)()
-    ncols = (C.c_int32 * n)()
+    # shapes, then ONE host buffer for all results (views per query), copy + free
+    nrows, ncols = prep.nrows, prep.ncols
     L.gsm_results_shape(outs, n, nrows, ncols)
-    arrays = [np.empty((int(nrows[i]), int(ncols[i])), dtype=np.uint32) for i in range(n)]
-    dsts = (C.c_void_p * n)(*[a.ctypes.data if a.size else None for a in arrays])
+    sizes = [int(nrows[i]) * int(ncols[i]) for i in range(n)]
+    buf = np.empty(sum(sizes), dtype=np.uint32)
+    base = buf.ctypes.data
+    arrays = []
+    dsts = prep.dsts
+    off = 0
+    for i in range(n):
+        arrays.append(buf[off:off + sizes[i]].reshape(int(nrows[i]), int(ncols[i])))
+        dsts[i] = base + 4 * off if sizes[i] else None
+        off += sizes[i]
     _lib.check(L.gsm_results_copy(outs, n, dsts, 1))
     results = []
     for i, (query, plan) in enumerate(items):
-        steps, _, _, rep_struct, bufs = prepared[i]
         if reports is not None:
-            _fill_report(reports[i], steps, rep_struct, *bufs)
-        results.append(BindingTable(tuple(query.projection), array=arrays[i]))
+            rep_struct, bufs = rep_bufs[i]
+            _fill_report(reports[i], prep.steps[i], rep_struct, *bufs)
+        results.append(BindingTable(prep.schemas[i], array=arrays[i]))
     if batch_timing is not None:
         batch_timing.append(ms.value / 1e3)
     return results
