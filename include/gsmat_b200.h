@@ -117,6 +117,16 @@ gsm_status gsm_store_put_predicate(gsm_store* store, int32_t pid, const uint64_t
 gsm_status gsm_store_put_predicate_shard(gsm_store* store, int32_t pid, const uint64_t* so_pairs,
                                          int64_t nnz_so, const uint64_t* os_pairs, int64_t nnz_os);
 
+/* Loader fast path for storage.load (storage.py:193-200, 222-271): streams
+ * the n predicates' pair files (p<ID>.so / p<ID>.os, nnz[i] u64 LE pairs
+ * each, sizes already validated by the caller) straight to the device —
+ * pinned double-buffered reads overlapped with the H2D copies and the
+ * narrowing kernels — with the same sortedness / id-range errors as
+ * gsm_store_put_predicate.  Equivalent to n gsm_store_put_predicate calls. */
+gsm_status gsm_store_load_files(gsm_store* store, int32_t n, const int32_t* pids,
+                                const char* const* so_paths, const char* const* os_paths,
+                                const int64_t* nnz);
+
 /* Replaces PredicateMatrix.__post_init__ / build_aux (storage.py:38-53,66-72):
  * builds the device row indexes (aux arrays, key -> segment lookup, diagonal
  * lists) for every uploaded predicate and validates sortedness. */

@@ -34,6 +34,7 @@ EXPORTS = (
     "gsm_store_create",
     "gsm_store_put_predicate",
     "gsm_store_put_predicate_shard",
+    "gsm_store_load_files",
     "gsm_store_finalize",
     "gsm_store_device_bytes",
     "gsm_store_free",
@@ -129,6 +130,7 @@ def lib() -> C.CDLL:
             "gsm_store_create": (i32, [i32, i64, i32, P(vp)]),
             "gsm_store_put_predicate": (i32, [vp, i32, vp, vp, i64]),
             "gsm_store_put_predicate_shard": (i32, [vp, i32, vp, i64, vp, i64]),
+            "gsm_store_load_files": (i32, [vp, i32, P(i32), P(C.c_char_p), P(C.c_char_p), P(i64)]),
             "gsm_store_finalize": (i32, [vp]),
             "gsm_store_device_bytes": (i32, [vp, P(i64)]),
             "gsm_store_free": (i32, [vp]),

@@ -7,9 +7,18 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdio>
+#include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "gsm_internal.cuh"
 
@@ -24,21 +33,6 @@ bool HostAux::find(u32 k, u32& begin, u32& len) const {
   begin = off[i];
   len = off[i + 1] - off[i];
   return true;
-}
-
-static void build_host_aux(const uint64_t* pairs, i64 nnz, HostAux& a) {
-  a.key.clear();
-  a.off.clear();
-  for (i64 i = 0; i < nnz; i++) {
-    u32 k = (u32)pairs[2 * i];
-    if (i == 0 || k != (u32)pairs[2 * i - 2]) {
-      a.key.push_back(k);
-      a.off.push_back((u32)i);
-    }
-  }
-  a.off.push_back((u32)nnz);
-  a.max_run = 0;
-  for (size_t i = 0; i + 1 < a.off.size(); i++) a.max_run = std::max(a.max_run, a.off[i + 1] - a.off[i]);
 }
 
 namespace gsm {
@@ -178,6 +172,48 @@ static gsm_status build_orient(gsm_store* s, Orient& o) {
   return GSM_OK;
 }
 
+// Host copy of an orientation's aux array (storage.py:38-53): run heads
+// selected on the device (cub), then one copy of keys and offsets.
+struct HeadFlag {
+  const u32* src;
+  __device__ bool operator()(const u32& i) const { return i == 0 || src[i] != src[i - 1]; }
+};
+
+static gsm_status build_host_aux(const Orient& o, HostAux& a) {
+  a.key.clear();
+  a.off.clear();
+  a.max_run = 0;
+  if (o.nnz == 0) {
+    a.off.push_back(0);
+    return GSM_OK;
+  }
+  u32 *d_pos, *d_n, *d_key;
+  GSM_CUDA(cudaMalloc(&d_pos, 4 * (size_t)o.nrows + 4));
+  GSM_CUDA(cudaMalloc(&d_key, 4 * (size_t)o.nrows + 4));
+  GSM_CUDA(cudaMalloc(&d_n, 4));
+  thrust::counting_iterator<u32> it(0);
+  size_t tmp_bytes = 0;
+  HeadFlag f{o.src};
+  cub::DeviceSelect::If(nullptr, tmp_bytes, it, d_pos, d_n, (int)o.nnz, f);
+  void* tmp;
+  GSM_CUDA(cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 4));
+  cub::DeviceSelect::If(tmp, tmp_bytes, it, d_pos, d_n, (int)o.nnz, f);
+  k_gather_u32<<<grid_for(o.nrows), 256>>>(d_pos, d_n, o.src, d_key);
+  count_launch(3);
+  a.key.resize(o.nrows);
+  a.off.resize((size_t)o.nrows + 1);
+  GSM_CUDA(cudaMemcpy(a.key.data(), d_key, 4 * (size_t)o.nrows, cudaMemcpyDeviceToHost));
+  GSM_CUDA(cudaMemcpy(a.off.data(), d_pos, 4 * (size_t)o.nrows, cudaMemcpyDeviceToHost));
+  a.off[o.nrows] = o.nnz;
+  for (u32 i = 0; i < o.nrows; i++) a.max_run = std::max(a.max_run, a.off[i + 1] - a.off[i]);
+  cudaFree(tmp);
+  cudaFree(d_pos);
+  cudaFree(d_key);
+  cudaFree(d_n);
+  GSM_CUDA(cudaGetLastError());
+  return GSM_OK;
+}
+
 static gsm_status build_diag(gsm_store* s, PredDev& p) {
   const Orient& o = p.so;
   if (o.nnz == 0) return GSM_OK;
@@ -307,10 +343,237 @@ gsm_status gsm_store_put_predicate_shard(gsm_store* s, int32_t pid, const uint64
     }
   }
   if (stage) cudaFree(stage);
-  build_host_aux(so_pairs, nnz_so, s->aux_so[pid]);
-  build_host_aux(os_pairs, nnz_os, s->aux_os[pid]);
   s->max_nnz = std::max<u32>(s->max_nnz, (u32)nmax);
   GSM_CUDA(cudaGetLastError());
+  return GSM_OK;
+}
+
+// Store loader fast path (storage.load's pair reads, storage.py:193-200,
+// 222-271): every predicate's p<ID>.so / p<ID>.os file is streamed to the
+// device in 32 MiB chunks.  Reader threads pread chunks into a ring of pinned
+// buffers while the calling thread issues, per chunk, the H2D copy and the
+// narrowing kernel on one stream, so disk / page-cache reads, PCIe transfers
+// and the device work overlap.  Sortedness and id-range checks accumulate in
+// per-file device flags, read back once at the end and reported in upload
+// order with put_predicate's messages.
+gsm_status gsm_store_load_files(gsm_store* s, int32_t n, const int32_t* pids,
+                                const char* const* so_paths, const char* const* os_paths,
+                                const int64_t* nnz) {
+  if (!s) return set_error(GSM_ERR_VALUE, "null store");
+  if (s->finalized) return set_error(GSM_ERR_VALUE, "store already finalized");
+  if (n < 0 || (n > 0 && (!pids || !so_paths || !os_paths || !nnz)))
+    return set_error(GSM_ERR_VALUE, "bad arguments");
+  for (int i = 0; i < n; i++) {
+    if (pids[i] < 1 || pids[i] > s->max_pid)
+      return set_error(GSM_ERR_UNKNOWN_PREDICATE, "no matrix for predicate id " + std::to_string(pids[i]));
+    if (nnz[i] < 0 || nnz[i] >= 0xFFFFFFF0LL) return set_error(GSM_ERR_VALUE, "predicate pair count must be < 2^32");
+    if (s->preds[pids[i]].present) return set_error(GSM_ERR_VALUE, "predicate uploaded twice");
+    for (int j = 0; j < i; j++)
+      if (pids[j] == pids[i]) return set_error(GSM_ERR_VALUE, "predicate uploaded twice");
+  }
+  GSM_CUDA(cudaSetDevice(s->device));
+  // files: 2 per predicate (so, os)
+  const int nf = 2 * n;
+  std::vector<int> fds((size_t)nf, -1);
+  auto close_all = [&]() {
+    for (int fd : fds)
+      if (fd >= 0) close(fd);
+  };
+  for (int f = 0; f < nf; f++) {
+    const char* path = (f & 1) ? os_paths[f / 2] : so_paths[f / 2];
+    fds[f] = open(path, O_RDONLY);
+    if (fds[f] < 0) {
+      close_all();
+      return set_error(GSM_ERR_STORE_FORMAT, std::string("cannot open ") + path + ": " + strerror(errno));
+    }
+  }
+  // device columns
+  for (int i = 0; i < n; i++) {
+    PredDev& p = s->preds[pids[i]];
+    for (Orient* o : {&p.so, &p.os}) {
+      u32 *src, *dst;
+      cudaError_t e = store_alloc(s, (void**)&src, 4 * (size_t)nnz[i]);
+      if (e == cudaSuccess) e = store_alloc(s, (void**)&dst, 4 * (size_t)nnz[i]);
+      if (e != cudaSuccess) {
+        close_all();
+        return cuda_error(e, "cudaMalloc(pair columns)");
+      }
+      o->src = src;
+      o->dst = dst;
+      o->nnz = (u32)nnz[i];
+    }
+  }
+  // chunk list in upload order
+  struct Chunk {
+    int f;
+    i64 off, m;
+  };
+  const i64 CH = (i64)1 << 21;  // pairs per chunk (32 MiB)
+  std::vector<Chunk> chunks;
+  i64 max_m = 0;
+  for (int f = 0; f < nf; f++)
+    for (i64 b = 0; b < nnz[f / 2]; b += CH) {
+      const i64 m = std::min(CH, nnz[f / 2] - b);
+      chunks.push_back({f, b, m});
+      max_m = std::max(max_m, m);
+    }
+  const int NS = (int)std::min<size_t>(8, std::max<size_t>(1, chunks.size()));
+  std::vector<u64*> hbuf((size_t)NS, nullptr), dbuf((size_t)NS, nullptr);
+  std::vector<cudaEvent_t> ev((size_t)NS, nullptr);
+  cudaStream_t st = nullptr;
+  u32* d_flags = nullptr;
+  auto release = [&]() {
+    for (int k = 0; k < NS; k++) {
+      if (hbuf[k]) cudaFreeHost(hbuf[k]);
+      if (dbuf[k]) cudaFree(dbuf[k]);
+      if (ev[k]) cudaEventDestroy(ev[k]);
+    }
+    if (st) cudaStreamDestroy(st);
+    if (d_flags) cudaFree(d_flags);
+    close_all();
+  };
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&d_flags, 16 * (size_t)std::max(nf, 1));
+  for (int k = 0; k < NS && e == cudaSuccess && max_m > 0; k++) {
+    e = cudaMallocHost(&hbuf[k], 16 * (size_t)max_m);
+    if (e == cudaSuccess) e = cudaMalloc(&dbuf[k], 16 * (size_t)max_m);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    release();
+    return cuda_error(e, "loader buffers");
+  }
+  {
+    std::vector<u32> init((size_t)4 * std::max(nf, 1));
+    for (int f = 0; f < nf; f++) {
+      init[4 * f] = init[4 * f + 1] = 0xFFFFFFFFu;
+      init[4 * f + 2] = init[4 * f + 3] = 0u;
+    }
+    e = cudaMemcpy(d_flags, init.data(), 16 * (size_t)std::max(nf, 1), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      release();
+      return cuda_error(e, "cudaMemcpy(flags)");
+    }
+  }
+  // pipeline: chunk c uses slot c % NS; readers fill, this thread issues
+  const int nc = (int)chunks.size();
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<char> ready((size_t)nc, 0);
+  int issued = 0;  // chunks whose copy + kernel are enqueued (events recorded)
+  bool failed = false;
+  std::string read_err;
+  std::atomic<int> next{0};
+  auto reader = [&]() {
+    for (;;) {
+      const int c = next.fetch_add(1);
+      if (c >= nc) return;
+      const int k = c % NS;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return failed || issued > c - NS; });
+        if (failed) return;
+      }
+      if (c >= NS) cudaEventSynchronize(ev[k]);  // the slot's previous copy is done
+      const Chunk& ch = chunks[c];
+      char* dst = reinterpret_cast<char*>(hbuf[k]);
+      size_t want = 16 * (size_t)ch.m, got = 0;
+      off_t off = (off_t)(16 * ch.off);
+      while (got < want) {
+        ssize_t r = pread(fds[ch.f], dst + got, want - got, off + (off_t)got);
+        if (r <= 0) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!failed) {
+            failed = true;
+            const int pid = pids[ch.f / 2];
+            read_err = "p" + std::to_string(pid) + ((ch.f & 1) ? ".os" : ".so") +
+                       (r == 0 ? ": unexpected end of file" : std::string(": read error: ") + strerror(errno));
+          }
+          cv.notify_all();
+          return;
+        }
+        got += (size_t)r;
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        ready[c] = 1;
+      }
+      cv.notify_all();
+    }
+  };
+  const int nthreads = std::min(4, std::max(1, nc));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; t++) th.emplace_back(reader);
+  cudaError_t ce = cudaSuccess;
+  for (int c = 0; c < nc && ce == cudaSuccess; c++) {
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return failed || ready[c]; });
+      if (failed) break;
+    }
+    const int k = c % NS;
+    const Chunk& ch = chunks[c];
+    const PredDev& p = s->preds[pids[ch.f / 2]];
+    const Orient& o = (ch.f & 1) ? p.os : p.so;
+    ce = cudaMemcpyAsync(dbuf[k], hbuf[k], 16 * (size_t)ch.m, cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess) {
+      k_narrow_pairs<<<grid_for(ch.m), 256, 0, st>>>(dbuf[k], const_cast<u32*>(o.src), const_cast<u32*>(o.dst), ch.off, ch.m, d_flags + 4 * ch.f);
+      count_launch();
+      ce = cudaEventRecord(ev[k], st);
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      issued = c + 1;
+      if (ce != cudaSuccess) failed = true;
+    }
+    cv.notify_all();
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (ce != cudaSuccess) failed = true;
+    issued = nc + NS;  // release any waiting reader
+  }
+  cv.notify_all();
+  for (auto& t : th) t.join();
+  if (ce != cudaSuccess) {
+    release();
+    return cuda_error(ce, "loader copy");
+  }
+  if (failed) {
+    release();
+    return set_error(GSM_ERR_STORE_FORMAT, read_err);
+  }
+  for (int f = 0; f < nf; f++) {
+    const PredDev& p = s->preds[pids[f / 2]];
+    const Orient& o = (f & 1) ? p.os : p.so;
+    if (o.nnz > 1) {
+      k_check_sorted<<<grid_for(o.nnz), 256, 0, st>>>(o.src, o.dst, o.nnz, d_flags + 4 * f);
+      count_launch();
+    }
+  }
+  std::vector<u32> flags((size_t)4 * std::max(nf, 1));
+  ce = cudaMemcpyAsync(flags.data(), d_flags, 16 * (size_t)std::max(nf, 1), cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  release();
+  if (ce != cudaSuccess) return cuda_error(ce, "loader flags");
+  for (int f = 0; f < nf; f++) {
+    const int pid = pids[f / 2];
+    const char* file = (f & 1) ? "os" : "so";
+    const u32* fl = &flags[4 * (size_t)f];
+    if (fl[2])
+      return set_error(GSM_ERR_STORE_FORMAT, "p" + std::to_string(pid) + "." + file +
+                                                 ": node id >= 2^32 is not supported");
+    if (fl[0] != 0xFFFFFFFFu)
+      return set_error(GSM_ERR_UNSORTED, "pair list not sorted at position " + std::to_string(fl[0]));
+    if (fl[1] != 0xFFFFFFFFu)
+      return set_error(GSM_ERR_STORE_FORMAT, "p" + std::to_string(pid) + "." + file +
+                                                 ": pairs not sorted by (key, value) at position " +
+                                                 std::to_string(fl[1]));
+  }
+  for (int i = 0; i < n; i++) {
+    s->preds[pids[i]].present = 1;
+    s->max_nnz = std::max<u32>(s->max_nnz, (u32)nnz[i]);
+  }
   return GSM_OK;
 }
 
@@ -324,6 +587,8 @@ gsm_status gsm_store_finalize(gsm_store* s) {
     gsm_status st;
     if ((st = build_orient(s, p.so)) != GSM_OK) return st;
     if ((st = build_orient(s, p.os)) != GSM_OK) return st;
+    if ((st = build_host_aux(p.so, s->aux_so[pid])) != GSM_OK) return st;
+    if ((st = build_host_aux(p.os, s->aux_os[pid])) != GSM_OK) return st;
     if ((st = build_diag(s, p)) != GSM_OK) return st;
   }
   GSM_CUDA(cudaDeviceSynchronize());

@@ -68,7 +68,8 @@ class DeviceStore:
     """A store whose predicate matrices are resident on one CUDA device."""
 
     def __init__(self, dictionary, matrices: dict[int, PairMatrix], stats: dict[int, StatEntry],
-                 node_count: int, device: int = 0, shard: tuple[int, int] | None = None):
+                 node_count: int, device: int = 0, shard: tuple[int, int] | None = None,
+                 files: dict[int, tuple[Path, Path]] | None = None):
         self.dictionary = dictionary
         self.matrices = matrices
         self.stats = stats
@@ -84,12 +85,21 @@ class DeviceStore:
         _lib.check(L.gsm_store_create(device, self.node_count, max_pid, C.byref(self._handle)))
         self._finalizer = weakref.finalize(self, DeviceStore._release, self._handle.value,
                                            self._contexts)
-        for pid in sorted(matrices):
-            m = matrices[pid]
-            so = np.ascontiguousarray(m.so, dtype=np.uint64)
-            os_ = np.ascontiguousarray(m.os, dtype=np.uint64)
-            _lib.check(L.gsm_store_put_predicate_shard(self._handle, pid, so.ctypes.data,
-                                                       so.shape[0], os_.ctypes.data, os_.shape[0]))
+        if files is not None:
+            # loader fast path: the library streams the pair files itself
+            pids = sorted(files)
+            n = len(pids)
+            so_p = (C.c_char_p * n)(*[bytes(Path(files[p][0])) for p in pids])
+            os_p = (C.c_char_p * n)(*[bytes(Path(files[p][1])) for p in pids])
+            nnz = (C.c_int64 * n)(*[matrices[p].cardinality for p in pids])
+            _lib.check(L.gsm_store_load_files(self._handle, n, (C.c_int32 * n)(*pids), so_p, os_p, nnz))
+        else:
+            for pid in sorted(matrices):
+                m = matrices[pid]
+                so = np.ascontiguousarray(m.so, dtype=np.uint64)
+                os_ = np.ascontiguousarray(m.os, dtype=np.uint64)
+                _lib.check(L.gsm_store_put_predicate_shard(self._handle, pid, so.ctypes.data,
+                                                           so.shape[0], os_.ctypes.data, os_.shape[0]))
         _lib.check(L.gsm_store_finalize(self._handle))
 
     @staticmethod
@@ -160,11 +170,18 @@ class DeviceStore:
         self._finalizer()
 
 
-def _read_pairs(path: Path) -> np.ndarray:
-    """_pairs_from_bytes (storage.py:193-200) as an (n, 2) uint64 array."""
+def _read_pairs(path: Path, lazy: bool = False) -> np.ndarray:
+    """_pairs_from_bytes (storage.py:193-200) as an (n, 2) uint64 array;
+    ``lazy`` maps the file instead of reading it (the device upload streams
+    the file itself, so the host copy is only paged in if a caller reads
+    ``PairMatrix.so`` / ``.os``)."""
     size = path.stat().st_size
     if size % 16 != 0:
         raise StoreFormatError(f"truncated pair file {path}: {size} bytes")
+    if lazy:
+        if size == 0:
+            return np.zeros((0, 2), dtype=np.uint64)
+        return np.memmap(path, dtype="<u8", mode="r").reshape(-1, 2)
     arr = np.fromfile(path, dtype="<u8")
     return arr.reshape(-1, 2)
 
@@ -216,14 +233,16 @@ def load(directory: Path | str, device: int = 0, shard: tuple[int, int] | None =
         raise StoreFormatError(f"meta declares {pred_count} predicates but stats has {len(stats)}")
 
     matrices: dict[int, PairMatrix] = {}
+    files: dict[int, tuple[Path, Path]] = {}
     total = 0
     for pid in stats:
         so_path = directory / f"p{pid}.so"
         os_path = directory / f"p{pid}.os"
         if not so_path.exists() or not os_path.exists():
             raise StoreFormatError(f"missing pair files for predicate {pid}")
-        so = _read_pairs(so_path)
-        os_ = _read_pairs(os_path)
+        files[pid] = (so_path, os_path)
+        so = _read_pairs(so_path, lazy=shard is None)
+        os_ = _read_pairs(os_path, lazy=shard is None)
         if so.shape[0] != stats[pid].cardinality:
             raise StoreFormatError(
                 f"{so_path}: {so.shape[0]} pairs but stats declares {stats[pid].cardinality}"
@@ -237,7 +256,8 @@ def load(directory: Path | str, device: int = 0, shard: tuple[int, int] | None =
         matrices[pid] = PairMatrix(pid, so, os_)
     if total != triple_count:
         raise StoreFormatError(f"meta declares {triple_count} triples but store holds {total}")
-    return DeviceStore(dictionary, matrices, stats, node_count, device=device, shard=shard)
+    return DeviceStore(dictionary, matrices, stats, node_count, device=device, shard=shard,
+                       files=files if shard is None else None)
 
 
 # Reference Store objects are unhashable dataclasses: cache by id() and keep

@@ -89,7 +89,13 @@ def main():
         q = g.bind_constants(g.parse_query(qf.read_text()), store.dictionary)
         plan = g.make_plan(q, store.stats)
         budget = 1 << 62
-        res = g.execute(q, plan, store, row_budget=budget)
+        try:
+            res = g.execute(q, plan, store, row_budget=budget)
+        except g.ResourceLimitError as e:
+            # not materialisable on one device (nor by the CPU engines)
+            print(json.dumps({"query": qf.stem, "error": str(e)}), flush=True)
+            summary["infeasible"] = summary.get("infeasible", 0) + 1
+            continue
         dev = []
         rep = None
         for _ in range(args.reps):
