@@ -41,12 +41,14 @@ typedef enum {
   GSM_ERR_RESOURCE = 4,        /* ResourceLimitError: row budget (executor.py:158-163,
                                   192-193, 237-241) or device memory exhausted           */
   GSM_ERR_CUDA = 5,            /* driver/runtime failure                                */
-  GSM_ERR_UNSORTED = 6         /* ValueError "pair list not sorted" (storage.py:44-45)  */
+  GSM_ERR_UNSORTED = 6,        /* ValueError "pair list not sorted" (storage.py:44-45)  */
+  GSM_ERR_UNKNOWN_ID = 7       /* UnknownIdError: decode of an absent id (dictionary.py:84-87) */
 } gsm_status;
 
 typedef struct gsm_store gsm_store;
 typedef struct gsm_context gsm_context;
 typedef struct gsm_result gsm_result;
+typedef struct gsm_text gsm_text;
 
 /* One triple pattern of the plan, in plan order (planner.py:73-83 PlanStep.pattern;
  * fields of qparser.EncodedPattern, qparser.py:303-323).  Variables are small
@@ -267,6 +269,27 @@ const char* gsm_last_error(void);
 
 /* Number of kernels this library launched since load (all threads). */
 int64_t gsm_kernel_launches(void);
+
+/* ---- result decoding ------------------------- */
+
+/* Replaces the node half of TermDictionary.load (dictionary.py:107-125) for
+ * decoding: the raw nodes.dict bytes and the [start, end) byte range of every
+ * line (term id i+1 = line i).  Each term is rendered on the device into its
+ * N-Triples surface form (unescape_term, dictionary.py:28-43, then
+ * qparser.format_term, qparser.py:71-78) and kept resident. */
+gsm_status gsm_store_put_dictionary(gsm_store* store, const char* nodes_dict, int64_t nbytes,
+                                    const int64_t* line_starts, const int64_t* line_ends,
+                                    int64_t n_terms);
+
+/* Replaces the CLI's row loop (cli.py:102-105: "\t".join(format_term(
+ * decode_node(v)) for v in row) + newline, per row): rows is a row-major
+ * n_rows x k u32 table of node ids (host or device memory).  The TSV body is
+ * built on the device and returned as a host text object.  An id outside the
+ * dictionary -> GSM_ERR_UNKNOWN_ID ("no node term with id V"). */
+gsm_status gsm_decode_rows(gsm_store* store, const uint32_t* rows, int64_t n_rows, int32_t k,
+                           gsm_text** out);
+gsm_status gsm_text_data(const gsm_text* text, const char** data, int64_t* nbytes);
+gsm_status gsm_text_free(gsm_text* text);
 
 #ifdef __cplusplus
 }

@@ -24,9 +24,13 @@ from .executor import (
     execute_batch,
 )
 from .frontend import Plan, QueryGraph, TriplePattern, bind_constants, make_plan, parse_query
+from .decode import decode_rows, format_term, result_tsv
 from .storage import DeviceStore, StatEntry, from_store, load
 
 __all__ = [
+    "decode_rows",
+    "format_term",
+    "result_tsv",
     "BindingTable",
     "DEFAULT_ROW_BUDGET",
     "DeviceStore",

@@ -22,6 +22,7 @@ GSM_ERR_UNKNOWN_PREDICATE = 3
 GSM_ERR_RESOURCE = 4
 GSM_ERR_CUDA = 5
 GSM_ERR_UNSORTED = 6
+GSM_ERR_UNKNOWN_ID = 7
 
 GSM_BUDGET_SEQUENTIAL = 0
 GSM_BUDGET_PARALLEL = 1
@@ -54,6 +55,10 @@ EXPORTS = (
     "gsm_results_copy",
     "gsm_last_error",
     "gsm_kernel_launches",
+    "gsm_store_put_dictionary",
+    "gsm_decode_rows",
+    "gsm_text_data",
+    "gsm_text_free",
 )
 
 
@@ -132,6 +137,10 @@ def lib() -> C.CDLL:
             "gsm_store_put_predicate_shard": (i32, [vp, i32, vp, i64, vp, i64]),
             "gsm_store_load_files": (i32, [vp, i32, P(i32), P(C.c_char_p), P(C.c_char_p), P(i64)]),
             "gsm_store_finalize": (i32, [vp]),
+            "gsm_store_put_dictionary": (i32, [vp, C.c_char_p, i64, vp, vp, i64]),
+            "gsm_decode_rows": (i32, [vp, vp, i64, i32, P(vp)]),
+            "gsm_text_data": (i32, [vp, P(C.c_void_p), P(i64)]),
+            "gsm_text_free": (i32, [vp]),
             "gsm_store_device_bytes": (i32, [vp, P(i64)]),
             "gsm_store_free": (i32, [vp]),
             "gsm_context_create": (i32, [vp, i64, P(vp)]),
@@ -191,6 +200,9 @@ def raise_status(status: int, msg: str) -> None:
         raise errors.UnknownPredicateError(pid)
     if status in (GSM_ERR_VALUE, GSM_ERR_UNSORTED):
         raise ValueError(msg)
+    if status == GSM_ERR_UNKNOWN_ID:
+        tail = msg.rsplit(" ", 1)[-1] if msg else ""
+        raise errors.UnknownIdError("node", int(tail) if tail.isdigit() else -1)
     raise errors.DeviceError(msg or f"gsm status {status}")
 
 

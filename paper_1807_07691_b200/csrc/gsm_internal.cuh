@@ -24,6 +24,11 @@ struct gsm_store {
   i64 bytes = 0;
   u32 max_nnz = 0;
   bool finalized = false;
+  // rendered node terms for result decoding (gsm_store_put_dictionary):
+  // term v = term_bytes[term_off[v-1], term_off[v])
+  unsigned char* term_bytes = nullptr;
+  u64* term_off = nullptr;
+  i64 n_terms = 0, term_total = 0;
   u32* d_flag = nullptr;  // validation scratch: [0] min unsorted-key pos, [1] min unsorted-value pos, [2] id overflow
 };
 

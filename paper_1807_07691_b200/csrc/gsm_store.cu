@@ -607,6 +607,8 @@ gsm_status gsm_store_free(gsm_store* s) {
   cudaSetDevice(s->device);
   for (void* p : s->allocations) cudaFree(p);
   if (s->d_flag) cudaFree(s->d_flag);
+  if (s->term_bytes) cudaFree(s->term_bytes);
+  if (s->term_off) cudaFree(s->term_off);
   delete s;
   return GSM_OK;
 }
