@@ -230,7 +230,10 @@ def run_ours(args):
             (B) one by one exactly as a user calls execute() (no report), wall
                 clock incl. H2D of the query block and D2H of the result rows;
             (C) the same 14 queries as one execute_batch() call (concurrent
-                streams): device time (events) and wall clock."""
+                streams): device time (events) and wall clock;
+            (D) one by one again, each as a one-query execute_batch() whose
+                device time is taken around the whole launch sequence only
+                (no per-step events): the per-query latency."""
             flush.add_(1)
             torch.cuda.synchronize()
             per_q = []
@@ -250,8 +253,15 @@ def run_ours(args):
             t0 = time.perf_counter()
             g.execute_batch(items, store, batch_timing=bt)
             wall_batch = time.perf_counter() - t0
+            flush.add_(1)
+            torch.cuda.synchronize()
+            lat_q = {}
+            for name, q, plan in queries:
+                one = []
+                g.execute_batch([(q, plan)], store, batch_timing=one)
+                lat_q[name] = one[0]
             return {"per_q": per_q, "wall_seq": wall_seq, "wall_batch": wall_batch,
-                    "dev_batch": bt[0]}
+                    "dev_batch": bt[0], "lat": lat_q}
 
         clk = ClockSampler(local).__enter__()  # sampling starts before warm-up (nvidia-smi start-up)
         time.sleep(0.5)
@@ -275,7 +285,7 @@ def run_ours(args):
         launches = _lib.kernel_launches() - launches0
 
         all_q = [x for st_ in steps for x in st_["per_q"]]
-        dev_seq = sum(rep.device_seconds for _, rep, _ in all_q)
+        dev_seq = sum(sum(st_["lat"].values()) for st_ in steps)
         dev_s = sum(st_["dev_batch"] for st_ in steps)
         wall_seq = sum(st_["wall_seq"] for st_ in steps)
         wall_s = sum(st_["wall_batch"] for st_ in steps)
@@ -302,8 +312,7 @@ def run_ours(args):
 
         lat = {}
         for name, *_ in queries:
-            d = [rep.device_seconds for n, rep, _ in all_q if n == name]
-            lat[name] = round(1e3 * statistics.median(d), 4)
+            lat[name] = round(1e3 * statistics.median(st_["lat"][name] for st_ in steps), 4)
 
         if world > 1:
             t = torch.tensor([dev_s, wall_s, dev_seq, wall_seq], dtype=torch.float64,

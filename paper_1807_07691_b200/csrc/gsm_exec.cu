@@ -127,12 +127,17 @@ __device__ __forceinline__ void export_if_last(const ExportArgs& x) {
   }
 }
 
-__device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Look-back status words are self-contained (epoch | flag | value in one
+// 64-bit word) and nothing else is published with them, so relaxed
+// gpu-scope accesses suffice: a release store would put a MEMBAR.ALL.GPU on
+// every tile's critical path (ncu: the top stall of the LUBM join kernels) and
+// an acquire load a CCTL.IVALL that drops the whole L1.
+__device__ __forceinline__ void st_status_u64(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ u64 ld_acquire_u64(const u64* p) {
+__device__ __forceinline__ u64 ld_status_u64(const u64* p) {
   u64 v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ u64 lb_word(u32 epoch, u32 flag, i64 v) {
@@ -148,10 +153,10 @@ __device__ __forceinline__ u64 lb_word(u32 epoch, u32 flag, i64 v) {
 __device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
   const int lane = threadIdx.x & 31;
   if (t == 0) {
-    if (lane == 0) st_release_u64(ts.status, lb_word(ts.epoch, 2, agg));
+    if (lane == 0) st_status_u64(ts.status, lb_word(ts.epoch, 2, agg));
     return 0;
   }
-  if (lane == 0) st_release_u64(ts.status + t, lb_word(ts.epoch, 1, agg));
+  if (lane == 0) st_status_u64(ts.status + t, lb_word(ts.epoch, 1, agg));
   i64 excl = 0;
   i64 top = (i64)t - 1;  // highest predecessor of this window
   for (;;) {
@@ -160,7 +165,7 @@ __device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
     u32 fl;
     if (j >= 0) {
       do {
-        w = ld_acquire_u64(ts.status + j);
+        w = ld_status_u64(ts.status + j);
         fl = ((u32)(w >> 42) == ts.epoch) ? (u32)(w >> 40) & 3u : 0u;
       } while (fl == 0);
     } else {
@@ -176,7 +181,7 @@ __device__ i64 lookback_warp(const TileSync& ts, u32 t, i64 agg) {
     if (pmask) break;
     top -= 32;
   }
-  if (lane == 0) st_release_u64(ts.status + t, lb_word(ts.epoch, 2, excl + agg));
+  if (lane == 0) st_status_u64(ts.status + t, lb_word(ts.epoch, 2, excl + agg));
   return excl;
 }
 
@@ -190,7 +195,7 @@ struct LBShared {
   i64 sum[TS_THREADS / 32];
 };
 __device__ __forceinline__ void lb_publish(const TileSync& ts, u32 t, i64 agg) {
-  if (threadIdx.x == 0) st_release_u64(ts.status + t, lb_word(ts.epoch, t == 0 ? 2 : 1, agg));
+  if (threadIdx.x == 0) st_status_u64(ts.status + t, lb_word(ts.epoch, t == 0 ? 2 : 1, agg));
 }
 __device__ i64 lookback_block(const TileSync& ts, u32 t, i64 agg, LBShared& sh) {
   if (t == 0) return 0;  // tile 0 published its inclusive prefix in lb_publish
@@ -204,7 +209,7 @@ __device__ i64 lookback_block(const TileSync& ts, u32 t, i64 agg, LBShared& sh) 
     u32 fl = 2;  // before tile 0: an inclusive prefix of 0
     if (j >= 0) {
       do {
-        w = ld_acquire_u64(ts.status + j);
+        w = ld_status_u64(ts.status + j);
         fl = ((u32)(w >> 42) == ts.epoch) ? (u32)(w >> 40) & 3u : 0u;
       } while (fl == 0);
     }
@@ -225,7 +230,7 @@ __device__ i64 lookback_block(const TileSync& ts, u32 t, i64 agg, LBShared& sh) 
     if (first < (1 << 30)) break;
     top -= TS_THREADS;
   }
-  if (tid == 0) st_release_u64(ts.status + t, lb_word(ts.epoch, 2, excl + agg));
+  if (tid == 0) st_status_u64(ts.status + t, lb_word(ts.epoch, 2, excl + agg));
   return excl;
 }
 
@@ -857,6 +862,45 @@ __device__ __forceinline__ bool gpost(const GroupP& p, const DTable& s, i64 r, u
   return true;
 }
 
+// Post filters on the (at most GP_BATCH) candidates of one short row, the
+// candidates side by side: every filter's lookups for all live candidates
+// are issued before any is consumed, so the row pays one dependent chain per
+// filter instead of one per (candidate, filter).  Same per-step counters as
+// evaluating gpost candidate by candidate.  Returns the survivor bit mask.
+constexpr int GP_BATCH = 4;
+static_assert(GP_BATCH >= (int)FUSE_MAX_FANOUT, "fused post filters must fit one batch");
+__device__ __forceinline__ u32 gpost_batch(const GroupP& p, const DTable& s, i64 r, u32 aux, u32 len,
+                                           i64* acc) {
+  u32 cand[GP_BATCH];
+#pragma unroll
+  for (int j = 0; j < GP_BATCH; j++) cand[j] = (u32)j < len ? __ldg(p.X.dst + aux + j) : 0u;
+  u32 alive = (1u << len) - 1u;
+  for (int i = p.npre; i < p.npre + p.npost && alive; i++) {
+    const FSpec& f = p.f[i];
+    uint2 sg[GP_BATCH];
+    u32 tgt[GP_BATCH];
+#pragma unroll
+    for (int j = 0; j < GP_BATCH; j++) {
+      sg[j] = make_uint2(0u, 0u);
+      tgt[j] = 0u;
+      if ((alive >> j) & 1u) {
+        const u32 key = vcol(s, p.a, f.kc, r, cand[j]);
+        sg[j] = seg_lookup(f.R, key);
+        tgt[j] = f.mode == F_PAIR ? vcol(s, p.a, f.tc, r, cand[j]) : f.mode == F_CONST ? f.cval : key;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < GP_BATCH; j++) {
+      if (!((alive >> j) & 1u)) continue;
+      const bool keep = sg[j].y && sorted_contains(f.R.dst + sg[j].x, sg[j].y, tgt[j]);
+      acc[2 * f.slot] += f.mode == F_PAIR ? (i64)sg[j].y : (i64)keep;
+      acc[2 * f.slot + 1] += keep;
+      if (!keep) alive &= ~(1u << j);
+    }
+  }
+  return alive;
+}
+
 __device__ __forceinline__ void gwrite(const GroupP& p, const DTable& s, i64 r, u32 cand, i64 g) {
   if (p.fz.stage) {
     if (g >= p.fz.cap) return;
@@ -924,7 +968,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
     const i64 base = (i64)t * TS_TILE;
     const i64 r = base + tid;
     // ---- count: pre-filters, expand, post-filters on short candidate lists
-    u32 cnt = 0, aux = 0, len = 0;
+    u32 cnt = 0, aux = 0, len = 0, mask = 0xffffffffu;
     bool warp_row = false;
     if (r < n) {
       bool pass = true;
@@ -944,8 +988,14 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
             cnt = p.npost ? 0u : len;
           } else if (p.npost == 0) {
             cnt = len;
-          } else {
-            for (u32 j = 0; j < len; j++) cnt += gpost(p, s_in, r, __ldg(p.X.dst + aux + j), s_acc);
+          } else if (len <= (u32)GP_BATCH) {
+            mask = gpost_batch(p, s_in, r, aux, len, s_acc);
+            cnt = __popc(mask);
+          } else {  // (the host fuses post filters only for fan-out <= GP_BATCH)
+            mask = 0;
+            for (u32 j = 0; j < len; j++)
+              if (gpost(p, s_in, r, __ldg(p.X.dst + aux + j), s_acc)) mask |= 1u << j;
+            cnt = __popc(mask);
           }
         }
       }
@@ -995,10 +1045,8 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       if (!p.has_x) {
         gwrite(p, s_in, r, 0u, pos);
       } else {
-        for (u32 j = 0; j < len; j++) {
-          const u32 cand = __ldg(p.X.dst + aux + j);
-          if (p.npost == 0 || gpost(p, s_in, r, cand, nullptr)) gwrite(p, s_in, r, cand, pos++);
-        }
+        for (u32 j = 0; j < len; j++)  // survivors recorded by the count phase
+          if ((mask >> j) & 1u) gwrite(p, s_in, r, __ldg(p.X.dst + aux + j), pos++);
       }
     }
     for (int q = warp; q < s_nlong; q += TS_THREADS / 32) {

@@ -56,6 +56,10 @@ def main():
     import paper_1807_07691_b200 as g
     from oracle import oracle as orc
 
+    import bench
+
+    peak = bench._peaks()[0].get("hbm_gbs", 6650.0)
+
     subprocess.run(["make", "-s", "-C", str(REPO / "oracle")], check=True)
     tmp = tempfile.mkdtemp(prefix="gsm_scale_")
     store_dir = args.store or f"{tmp}/{args.kind}"
@@ -107,6 +111,15 @@ def main():
                "gpu_ms": round(1e3 * statistics.median(dev), 3),
                "join_rows": sum(s.rows for s in rep.steps[1:])}
         rec["join_rows_per_s"] = round(rec["join_rows"] / statistics.median(dev), 1)
+        # HBM roofline of the whole query: algorithmic bytes of its join steps
+        # (bench._step_bytes) / device time
+        qbytes = sum(bench._step_bytes(rep.kinds[i], rep.steps[i - 1].rows, rep.arities[i - 1],
+                                       rep.steps[i].prealloc_total, rep.steps[i].rows, rep.arities[i])
+                     for i in range(1, len(rep.steps)))
+        gbps = qbytes / statistics.median(dev) / 1e9
+        rec["bytes"] = int(qbytes)
+        rec["achieved_GBps"] = round(gbps, 1)
+        rec["hbm_frac"] = round(gbps / peak, 4)
         if max(rec["step_rows"]) <= args.skip_oracle_above:
             t0 = time.perf_counter()
             rows, srows, spre = orc.run(prep, [s.pattern for s in plan.steps], q.projection,
