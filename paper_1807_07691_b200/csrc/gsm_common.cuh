@@ -89,26 +89,37 @@ __device__ __forceinline__ uint2 seg_lookup(const Orient& R, u32 key) {
   return make_uint2(0, 0);
 }
 
-// Membership of `v` in the ascending run a[0..len).  Short runs (the common
-// case: most keys have a handful of neighbours) are scanned with independent
-// loads — one memory round trip instead of log2(len) dependent ones.
+// Membership of `v` in the ascending run a[0..len).  Latency, not bytes,
+// decides here (one probe per left row or candidate, each a chain of
+// dependent loads), so the search is 9-ary: each round loads 8 pivots at
+// once and keeps the slice between the two that bracket v, until at most 8
+// entries remain, which are compared with independent loads.  A run of 20
+// costs 2 memory round trips (binary search: 5), a run of 1000 costs 4 (10).
 __device__ __forceinline__ bool sorted_contains(const u32* a, u32 len, u32 v) {
-  if (len <= 8) {
+  u32 lo = 0, hi = len;
+  while (hi - lo > 8) {
+    const u32 n = hi - lo;
+    u32 pv[8];
+#pragma unroll
+    for (u32 i = 0; i < 8; i++) pv[i] = __ldg(a + lo + (u32)(((u64)(i + 1) * n) / 9));
+    u32 c = 0;
     bool hit = false;
 #pragma unroll
-    for (u32 i = 0; i < 8; i++)
-      if (i < len) hit |= __ldg(a + i) == v;
-    return hit;
+    for (u32 i = 0; i < 8; i++) {
+      c += pv[i] < v;
+      hit |= pv[i] == v;
+    }
+    if (hit) return true;
+    const u32 nlo = c == 0 ? lo : lo + (u32)(((u64)c * n) / 9) + 1;
+    const u32 nhi = c == 8 ? hi : lo + (u32)(((u64)(c + 1) * n) / 9);
+    lo = nlo;
+    hi = nhi;
   }
-  u32 lo = 0, hi = len;
-  while (lo < hi) {
-    u32 mid = (lo + hi) >> 1;
-    u32 x = __ldg(a + mid);
-    if (x < v) lo = mid + 1;
-    else if (x > v) hi = mid;
-    else return true;
-  }
-  return false;
+  bool hit = false;
+#pragma unroll
+  for (u32 i = 0; i < 8; i++)
+    if (lo + i < hi) hit |= __ldg(a + lo + i) == v;
+  return hit;
 }
 
 // Programmatic dependent launch (PDL): a kernel launched with
