@@ -42,7 +42,8 @@ typedef enum {
                                   192-193, 237-241) or device memory exhausted           */
   GSM_ERR_CUDA = 5,            /* driver/runtime failure                                */
   GSM_ERR_UNSORTED = 6,        /* ValueError "pair list not sorted" (storage.py:44-45)  */
-  GSM_ERR_UNKNOWN_ID = 7       /* UnknownIdError: decode of an absent id (dictionary.py:84-87) */
+  GSM_ERR_UNKNOWN_ID = 7,      /* UnknownIdError: decode of an absent id (dictionary.py:84-87) */
+  GSM_ERR_PARSE = 8            /* ParseError "line N: ..." (qparser.py:80-92)            */
 } gsm_status;
 
 typedef struct gsm_store gsm_store;
@@ -290,6 +291,25 @@ gsm_status gsm_decode_rows(gsm_store* store, const uint32_t* rows, int64_t n_row
                            gsm_text** out);
 gsm_status gsm_text_data(const gsm_text* text, const char** data, int64_t* nbytes);
 gsm_status gsm_text_free(gsm_text* text);
+
+/* ---- store build from N-Triples --------------- */
+
+/* Replaces qparser.read_ntriples (qparser.py:80-111): parses an N-Triples
+ * buffer with `threads` host threads and returns the canonical (subject,
+ * predicate, object) terms of every statement, in input order, as
+ * [u32 length][bytes] x 3 per triple.  A malformed statement ->
+ * GSM_ERR_PARSE "line N: malformed N-Triples statement: '...'" (or "bad
+ * literal escape \x"), the first one in input order. */
+gsm_status gsm_ntriples_parse(const char* buf, int64_t nbytes, int32_t threads, gsm_text** out);
+
+/* Replaces `gsmat build` (cli.py:64-82: read_ntriples -> TermDictionary
+ * first-occurrence ids -> build_store -> persist, storage.py:165-177,
+ * 203-219): parses nt_path on the host threads, encodes the terms and sorts /
+ * deduplicates the per-predicate pair lists on `device`, and writes a store
+ * directory byte-identical to the reference's into out_dir (which must
+ * exist).  counts (optional) = {triples, predicates, nodes}. */
+gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t device, int32_t threads,
+                           int64_t* counts);
 
 #ifdef __cplusplus
 }

@@ -25,9 +25,12 @@ from .executor import (
 )
 from .frontend import Plan, QueryGraph, TriplePattern, bind_constants, make_plan, parse_query
 from .decode import decode_rows, format_term, result_tsv
+from .ingest import build, parse_ntriples
 from .storage import DeviceStore, StatEntry, from_store, load
 
 __all__ = [
+    "build",
+    "parse_ntriples",
     "decode_rows",
     "format_term",
     "result_tsv",

@@ -7,6 +7,7 @@ or calling it on a machine without a CUDA device, raises.
 from __future__ import annotations
 
 import ctypes as C
+import re
 import os
 import threading
 from pathlib import Path
@@ -23,6 +24,7 @@ GSM_ERR_RESOURCE = 4
 GSM_ERR_CUDA = 5
 GSM_ERR_UNSORTED = 6
 GSM_ERR_UNKNOWN_ID = 7
+GSM_ERR_PARSE = 8
 
 GSM_BUDGET_SEQUENTIAL = 0
 GSM_BUDGET_PARALLEL = 1
@@ -59,6 +61,8 @@ EXPORTS = (
     "gsm_decode_rows",
     "gsm_text_data",
     "gsm_text_free",
+    "gsm_ntriples_parse",
+    "gsm_build_store",
 )
 
 
@@ -141,6 +145,8 @@ def lib() -> C.CDLL:
             "gsm_decode_rows": (i32, [vp, vp, i64, i32, P(vp)]),
             "gsm_text_data": (i32, [vp, P(C.c_void_p), P(i64)]),
             "gsm_text_free": (i32, [vp]),
+            "gsm_ntriples_parse": (i32, [C.c_char_p, i64, i32, P(vp)]),
+            "gsm_build_store": (i32, [C.c_char_p, C.c_char_p, i32, i32, P(i64)]),
             "gsm_store_device_bytes": (i32, [vp, P(i64)]),
             "gsm_store_free": (i32, [vp]),
             "gsm_context_create": (i32, [vp, i64, P(vp)]),
@@ -200,6 +206,11 @@ def raise_status(status: int, msg: str) -> None:
         raise errors.UnknownPredicateError(pid)
     if status in (GSM_ERR_VALUE, GSM_ERR_UNSORTED):
         raise ValueError(msg)
+    if status == GSM_ERR_PARSE:
+        m = re.match(r"line (\d+): (.*)$", msg, re.S)
+        if m:
+            raise errors.ParseError(m.group(2), int(m.group(1)))
+        raise errors.ParseError(msg)
     if status == GSM_ERR_UNKNOWN_ID:
         tail = msg.rsplit(" ", 1)[-1] if msg else ""
         raise errors.UnknownIdError("node", int(tail) if tail.isdigit() else -1)

@@ -142,10 +142,6 @@ int grid_for(i64 n, int threads = 256) {
 
 using namespace gsm;
 
-struct gsm_text {
-  std::vector<char> bytes;
-};
-
 extern "C" {
 
 gsm_status gsm_store_put_dictionary(gsm_store* s, const char* buf, int64_t nbytes, const int64_t* starts,

@@ -34,6 +34,11 @@ struct gsm_store {
 
 struct gsm_context;
 
+// Host byte blob returned through the C ABI (decoded text, parsed triples).
+struct gsm_text {
+  std::vector<char> bytes;
+};
+
 struct gsm_result {
   int device = 0;
   i64 n = 0;

@@ -1,0 +1,156 @@
+"""Store build from N-Triples (gsm_ntriples_parse / gsm_build_store) against
+the reference's ``gsmat build`` (cli.py:64-82) and its N-Triples parser
+(qparser.parse_ntriples_line, qparser.py:80-104).
+
+The parse stage is host code and is checked on CPU against the installed
+reference; the build (dictionary encoding and pair sorting on the GPU) must
+reproduce the reference-built golden stores (tests/golden/ingest, made by
+make_ingest_golden.py) byte for byte.
+"""
+
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+
+import paper_1807_07691_b200 as g
+from conftest import GOLDEN, reference_available
+
+INGEST = GOLDEN / "ingest"
+
+FRAGMENTS_S = ["<http://e/s>", "<s>", "_:b1", "_:a.b", "_:x.", "<a b>", "<a\"b>", "<>", "_:", "_:-x",
+               "s", "<http://e/é>", "\"lit\""]
+FRAGMENTS_P = ["<http://e/p>", "<p>", "_:p", "<p", "p"]
+FRAGMENTS_O = ["<http://e/o>", "<o>", "_:o1", "_:o.", "_:o..", "\"v\"", "\"v\"@en", "\"v\"@en-GB",
+               "\"v\"@en-", "\"v\"@1", "\"v\"^^<http://e/dt>", "\"v\"^^<>", "\"v\"^^dt",
+               "\"a\\\"b\"", "\"a\\\\b\"", "\"tab\\t\\n\\r\\b\\f\\'\"", "\"\\u00e9\\U0001F600\"",
+               "\"bad\\q\"", "\"bad\\u12\"", "\"open", "\"\"", "\"x\"y\"", "\"é\"@fr"]
+SEPS = [" ", "\t", "  ", "", " ", "　", "\x0b", "\x1f"]
+TAILS = [" .", ".", " . ", " .# c", " . #c", " .x", "", " ..", "\t.\t"]
+
+
+def _random_line(rng):
+    if rng.random() < 0.05:
+        return rng.choice(["", "   ", "# only a comment", "\t# c", "garbage"])
+    return (rng.choice(["", " ", "\t"]) + rng.choice(FRAGMENTS_S) + rng.choice(SEPS) +
+            rng.choice(FRAGMENTS_P) + rng.choice(SEPS) + rng.choice(FRAGMENTS_O) + rng.choice(TAILS))
+
+
+def _ref_parse(line, lineno):
+    from gsmat import qparser
+    from gsmat.errors import ParseError
+
+    try:
+        return ("ok", qparser.parse_ntriples_line(line + "\n", lineno))
+    except ParseError as e:
+        return ("err", str(e))
+    except Exception:  # reference crashes (int() of a short \u escape, ...): not comparable
+        return ("skip", None)
+
+
+def _ours(line, lineno):
+    text = "\n" * (lineno - 1) + line + "\n"
+    try:
+        got = g.parse_ntriples(text, threads=1)
+        return ("ok", got[0] if got else None)
+    except g.ParseError as e:
+        return ("err", str(e))
+
+
+def test_parse_matches_reference_fuzz():
+    if not reference_available():
+        pytest.skip("reference package not installed")
+    rng = random.Random(11)
+    n_ok = n_err = 0
+    for k in range(3000):
+        line = _random_line(rng)
+        ref = _ref_parse(line, 7)
+        if ref[0] == "skip":
+            continue
+        ours = _ours(line, 7)
+        assert ours == ref, repr(line)
+        n_ok += ref[0] == "ok"
+        n_err += ref[0] == "err"
+    assert n_ok > 300 and n_err > 300
+
+
+def test_parse_files_and_line_numbers():
+    if not reference_available():
+        pytest.skip("reference package not installed")
+    from gsmat import qparser
+
+    for name in ("tricky", "random"):
+        data = (INGEST / f"{name}.nt").read_bytes()
+        with open(INGEST / f"{name}.nt", encoding="utf-8") as fh:
+            ref = list(qparser.read_ntriples(fh))
+        for threads in (1, 3, 8):
+            assert g.parse_ntriples(data, threads=threads) == ref
+    # universal newlines: \r\n and lone \r end lines too
+    assert g.parse_ntriples(b"<a> <p> <b> .\r\n<c> <p> <d> .\r<e> <p> <f> .") == [
+        ("a", "p", "b"), ("c", "p", "d"), ("e", "p", "f")]
+    # the first malformed statement in input order, with its line number
+    text = "<a> <p> <b> .\n" * 4 + "<a> <p>\n" + "<a> <p> <b> .\n" * 3000 + "bad\n"
+    for threads in (1, 4, 16):
+        with pytest.raises(g.ParseError, match="line 5") as ei:
+            g.parse_ntriples(text, threads=threads)
+        assert ei.value.line == 5
+    with pytest.raises(g.ParseError, match=r"line 2: bad literal escape \\q"):
+        g.parse_ntriples('<a> <p> "x" .\n<a> <p> "\\q" .\n')
+
+
+def _same_store(a, b):
+    names = sorted(p.name for p in a.iterdir())
+    assert names == sorted(p.name for p in b.iterdir())
+    for n in names:
+        assert (a / n).read_bytes() == (b / n).read_bytes(), n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["tricky", "tricky_crlf", "random"])
+def test_build_matches_reference_store(tmp_path, name):
+    out = tmp_path / "s"
+    counts = g.build(INGEST / f"{name}.nt", out)
+    _same_store(out, INGEST / f"{name}_store")
+    meta = (out / "meta").read_text().split()
+    assert counts == (int(meta[1]), int(meta[2]), int(meta[3]))
+
+
+@pytest.mark.gpu
+def test_build_empty_and_errors(tmp_path):
+    (tmp_path / "empty.nt").write_text("# nothing\n\n")
+    assert g.build(tmp_path / "empty.nt", tmp_path / "e") == (0, 0, 0)
+    assert (tmp_path / "e" / "meta").read_text() == "GSMAT1\n0\n0\n0\n"
+    (tmp_path / "bad.nt").write_text("<a> <p> <b> .\n" * 4 + "<a> <p>\n")
+    with pytest.raises(g.ParseError, match="line 5"):
+        g.build(tmp_path / "bad.nt", tmp_path / "b")
+
+
+@pytest.mark.gpu
+def test_build_round_trip_large(tmp_path, store_factory):
+    """A generated LUBM store written out as N-Triples and rebuilt: the same
+    set of decoded triples (ids differ: first-occurrence order of the file)."""
+    src = g.load(store_factory("lubm", univ=1, seed=0))
+    dec = src.dictionary.decode_node
+    decp = src.dictionary.decode_predicate
+    lines = []
+    for pid, m in src.matrices.items():
+        for s, o in np.asarray(m.so).tolist():
+            lines.append(f"{g.format_term(dec(s))} <{decp(pid)}> {g.format_term(dec(o))} .")
+    random.Random(5).shuffle(lines)
+    nt = tmp_path / "lubm1.nt"
+    nt.write_text("\n".join(lines) + "\n", encoding="utf-8")
+    counts = g.build(nt, tmp_path / "rebuilt")
+    assert counts[0] == src.triple_count
+    st = g.load(tmp_path / "rebuilt")
+    d2, p2 = st.dictionary.decode_node, st.dictionary.decode_predicate
+
+    def triples(store, dn, dp):
+        out = set()
+        for pid, m in store.matrices.items():
+            name = dp(pid)
+            for s, o in np.asarray(m.so).tolist():
+                out.add((dn(s), name, dn(o)))
+        return out
+    assert triples(st, d2, p2) == triples(src, dec, decp)
