@@ -121,17 +121,31 @@ __global__ void k_dedup_flags(const u32* __restrict__ p, const u64* __restrict__
 }
 
 // Pair file images (u64 LE (key, value) per pair) and per-predicate counters:
-// rows[p] += 1, heads[p] += first pair of its key run.
+// rows[p] += 1, heads[p] += first pair of its key run.  Sorted by p, a warp
+// mostly holds one predicate: one aggregated atomic per (warp, predicate).
 __global__ void k_pairs_out(const u32* __restrict__ p, const u64* __restrict__ k, u64 n,
                             u64* __restrict__ pairs, unsigned long long* __restrict__ rows,
                             unsigned long long* __restrict__ heads) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const u64 key = k[i] >> 32, val = k[i] & 0xffffffffull;
-    pairs[2 * i] = key;
-    pairs[2 * i + 1] = val;
-    atomicAdd(rows + p[i], 1ull);
-    if (i == 0 || p[i] != p[i - 1] || (k[i - 1] >> 32) != key) atomicAdd(heads + p[i], 1ull);
+  const int lane = threadIdx.x & 31;
+  for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const u64 i = base + threadIdx.x;
+    const bool live = i < n;
+    u32 pid = 0xFFFFFFFFu;
+    bool head = false;
+    if (live) {
+      const u64 key = k[i] >> 32, val = k[i] & 0xffffffffull;
+      pairs[2 * i] = key;
+      pairs[2 * i + 1] = val;
+      pid = p[i];
+      head = i == 0 || p[i - 1] != pid || (k[i - 1] >> 32) != key;
+    }
+    const u32 same = __match_any_sync(0xffffffffu, pid);
+    const u32 hm = __ballot_sync(0xffffffffu, head) & same;
+    if (live && lane == __ffs(same) - 1) {
+      atomicAdd(rows + pid, (unsigned long long)__popc(same));
+      if (hm) atomicAdd(heads + pid, (unsigned long long)__popc(hm));
+    }
   }
 }
 
