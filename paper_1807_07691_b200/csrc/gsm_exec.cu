@@ -407,14 +407,21 @@ __device__ __forceinline__ void copy_desc(DTable& dst, const DTable* src, int nc
 // finish() records the result count in the pack stat (pad = 1, or 3 when the
 // result outgrew the result buffer and the host must re-run unfused).
 struct FusedOut {
-  u32* stage = nullptr;  // device alias of the pinned staging buffer; null = not fused
+  u32* stage = nullptr;  // result rows: staging buffer (device or pinned host alias),
+                         // or the join's own arena half (dev); null = not fused
   i64 cap = 0;           // rows that fit
   int k = 0;
+  int dev = 0;           // device-resident result (larger than the staging buffer)
   int pj[GSM_MAX_VARS];
   StepStat* pst = nullptr;
   __device__ void finish(i64 total) const {
     pst->rows = total;
-    pst->pad = total <= cap ? 1 : 3;
+    if (dev) {  // like k_pack's device path: overflow -> grow the arena, re-run
+      pst->overflow = total > cap;
+      pst->pad = 0;
+    } else {
+      pst->pad = total <= cap ? 1 : 3;
+    }
   }
 };
 
@@ -1577,6 +1584,7 @@ struct gsm_context {
   bool use_defer = true;   // spread hub rows over all SMs (k_drain)
   bool use_proj_fusion = true;  // write the projected result from the last join
   bool use_batch_graph = true;  // a repeated batch replays as one graph (gsm_execute_batch)
+  size_t stage_max = (size_t)1 << 30;  // the staging buffer grows up to this (GSM_STAGE_MAX)
   // A prepared plan: the captured launch sequence plus what the host needs
   // to replay and complete it without re-planning.
   struct GraphEntry {
@@ -1825,6 +1833,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* nd = getenv("GSM_NO_DEFER")) c->use_defer = !(nd[0] == '1');
   if (const char* npf = getenv("GSM_NO_PROJ_FUSION")) c->use_proj_fusion = !(npf[0] == '1');
   if (const char* nb = getenv("GSM_NO_BATCH_GRAPH")) c->use_batch_graph = !(nb[0] == '1');
+  if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
     return st;
@@ -1851,7 +1860,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
                                 : std::min<size_t>((size_t)1 << 32, free_b / 4);
   gsm_status st = ctx_set_arena(c, want);
   if (st != GSM_OK) return fail(st);
-  st = ctx_set_stage(c, (size_t)64 << 20);
+  st = ctx_set_stage(c, std::min<size_t>((size_t)64 << 20, c->stage_max));
   if (st != GSM_OK) return fail(st);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tilescan<ExpandP>, TS_THREADS, 0);
@@ -1924,6 +1933,7 @@ struct ExecState {
   bool capture_only = false;
   char* pre_image = nullptr;  // batch capture: the d_image buffer to use
   bool zc = false;            // counters and result rows written straight to pinned host memory
+  bool big = false;           // this plan's last result outgrew the staging buffer
   gsm_context::GraphEntry meta;
   cudaStream_t sync_stream = nullptr;  // first completion waits here (batch graph)
 };
@@ -1961,8 +1971,10 @@ static std::string query_key(gsm_context* c, const QueryArgs& qa, ExecState& S) 
     while (g < lb->second) g <<= 1;
   }
   c->guess = std::min(g, c->stage_bytes);
+  S.big = lb != c->last_bytes.end() && lb->second > c->stage_bytes;
   S.plan_key = key;
   key.append(reinterpret_cast<const char*>(&c->guess), sizeof c->guess);
+  key.push_back(S.big ? 'B' : 'S');
   return key;
 }
 
@@ -2291,13 +2303,26 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   u32* const stage_rows = S.zc ? c->hd_rows : c->d_rows;
   // Fuse the projection into the last join when it is an expand/filter and
   // the result goes to the host staging buffer (no DISTINCT).
+  // Results that outgrew the staging buffer last time (S.big) are written
+  // by the last join into its own (otherwise unused) arena half instead: a
+  // device-resident result without the k_pack pass.
   bool fused = false;
-  if (allow_fuse && c->use_proj_fusion && !distinct && !launches.empty() &&
+  const Home big_home = launches.empty() ? H_NONE : ex.home[launches.back().out];
+  if (allow_fuse && c->use_proj_fusion && !distinct && !launches.empty() && n_proj > 0 &&
       (launches.back().kind == S_EXPAND || launches.back().kind == S_FILTER ||
-       launches.back().kind == S_GROUP)) {
+       launches.back().kind == S_GROUP) &&
+      (!S.big || big_home == H_A || big_home == H_B)) {
     FusedOut fz;
-    fz.stage = stage_rows;
-    fz.cap = stage_cap;
+    if (S.big) {
+      fz.stage = reinterpret_cast<u32*>(ex.buf(big_home));
+      fz.cap = (i64)(ex.half / (4 * (size_t)n_proj));
+      fz.dev = 1;
+      pack_out = fz.stage;
+      pack_cap = fz.cap;
+    } else {
+      fz.stage = stage_rows;
+      fz.cap = stage_cap;
+    }
     fz.k = n_proj;
     for (int j = 0; j < n_proj; j++) fz.pj[j] = pj_idx[j];
     fz.pst = dS + pack_stat;
@@ -2455,7 +2480,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     // kernel) and the result rows up to this plan's expected size; the host
     // fetches any remainder after the sync (rare: only when the result grew).
     if (!S.zc)
-      GSM_CUDA(cudaMemcpyAsync(c->h_stage, c->d_stage, STAGE_HEAD + (distinct ? 0 : c->guess),
+      GSM_CUDA(cudaMemcpyAsync(c->h_stage, c->d_stage, STAGE_HEAD + ((distinct || S.big) ? 0 : c->guess),
                                cudaMemcpyDeviceToHost, st));
     kernels = nk;
     return GSM_OK;
@@ -2645,7 +2670,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
       // (<= 1 GiB) for the next query.
       size_t want = (size_t)hb->stats[pack_stat].rows * 4 * (size_t)std::max(n_proj, 1);
       c->last_bytes[plan_key] = want;
-      if (want > c->stage_bytes && want <= ((size_t)1 << 30)) ctx_set_stage(c, want + want / 4);
+      if (want > c->stage_bytes && want <= c->stage_max) ctx_set_stage(c, want + want / 4);
       S.allow_fuse = false;
       continue;
     }
@@ -2780,7 +2805,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     }
     if (bytes) GSM_CUDA(cudaMemcpyAsync(r->rows, pack_out, bytes, cudaMemcpyDeviceToDevice, st));
     GSM_CUDA(cudaStreamSynchronize(st));
-    if (bytes > c->stage_bytes && bytes <= ((size_t)1 << 30)) ctx_set_stage(c, bytes + bytes / 4);
+    if (bytes > c->stage_bytes && bytes <= c->stage_max) ctx_set_stage(c, bytes + bytes / 4);
   }
   // the next D2H size guess / zero-copy choice for this plan
   if (c->last_bytes.size() > 4096) c->last_bytes.clear();

@@ -230,7 +230,8 @@ def test_execution_variants_agree(store_factory):
     deferral and projection fusion are pure optimisations: each query gives
     the same bag and the same per-step report with them switched off
     (GSM_NO_GRAPHS / GSM_NO_PDL / GSM_NO_FUSION / GSM_NO_DEFER /
-    GSM_NO_PROJ_FUSION), and repeated (replayed) executions agree."""
+    GSM_NO_PROJ_FUSION), a tiny staging buffer (GSM_STAGE_MAX) forces the
+    device-resident result paths, and repeated (replayed) executions agree."""
     import json
     import os
     import subprocess
@@ -261,12 +262,17 @@ def test_execution_variants_agree(store_factory):
         "print(json.dumps(out))\n" % (str(GOLDEN.parents[1]), str(GOLDEN.parent), str(d))
     )
     results = {}
+    # GSM_STAGE_MAX=65536: results above 64 KB outgrow the staging buffer, so
+    # the second run writes them from the last join into the arena (device
+    # result, no k_pack) and DISTINCT / sizes above the zero-copy limit take
+    # the device paths
     for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION", "GSM_NO_DEFER",
-                    "GSM_NO_PROJ_FUSION",
+                    "GSM_NO_PROJ_FUSION", "GSM_NO_BATCH_GRAPH", "GSM_STAGE_MAX=65536",
                     "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER,GSM_NO_PROJ_FUSION"):
         env = dict(os.environ)
-        for k in filter(None, variant.split(",")):
-            env[k] = "1"
+        for item in filter(None, variant.split(",")):
+            k, _, v = item.partition("=")
+            env[k] = v or "1"
         proc = subprocess.run([sys.executable, "-c", script], input=json.dumps(texts), env=env,
                               capture_output=True, text=True)
         assert proc.returncode == 0, (variant, proc.stderr[-3000:])
