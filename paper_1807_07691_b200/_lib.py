@@ -14,7 +14,7 @@ from pathlib import Path
 
 from . import errors
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgsmat_b200.so"
+LIB_PATH = Path(os.environ.get("GSM_LIB") or Path(__file__).resolve().parent / "_lib" / "libgsmat_b200.so")
 
 GSM_OK = 0
 GSM_ERR_VALUE = 1

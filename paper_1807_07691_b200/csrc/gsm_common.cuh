@@ -128,6 +128,25 @@ __device__ __forceinline__ bool sorted_contains(const u32* a, u32 len, u32 v) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
+// Phase trace (diagnostic builds only, `make trace`): thread 0 of each block
+// stamps %globaltimer and clock64 at phase boundaries of its first tiles.
+constexpr int TRACE_SLOTS = 32;  // per block: 4 tiles x 8 phases
+#ifdef GSM_TRACE
+static __device__ unsigned long long g_trace[8192 * TRACE_SLOTS * 2];
+__device__ __forceinline__ void trace_at(int tile_iter, int phase) {
+  if (threadIdx.x == 0 && tile_iter < 4 && blockIdx.x < 8192) {
+    unsigned long long g, c;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    const size_t i = ((size_t)blockIdx.x * TRACE_SLOTS + tile_iter * 8 + phase) * 2;
+    g_trace[i] = g;
+    g_trace[i + 1] = c;
+  }
+}
+#else
+__device__ __forceinline__ void trace_at(int, int) {}
+#endif
+
 }  // namespace gsm
 
 // ---- host-side error plumbing (gsm_api.cu) ----

@@ -266,8 +266,10 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   p.prepare(s_in);
   u32 wtag = 0;  // load-balanced scatter: round tag of the row-start marks
   if constexpr (P::kWindow) P::window_init();
+  trace_at(0, 0);
   __syncthreads();
   const i64 n = p.rows(s_in);
+  int it = 0;
   const i64 ntiles = (n + TS_TILE - 1) / TS_TILE;
   if (ntiles == 0 && blockIdx.x == 0 && tid == 0) p.finish(0);
   i64 e_acc = 0;
@@ -283,6 +285,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     }
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
+    trace_at(it, 1);
     const i64 base = (i64)t * TS_TILE;
 #pragma unroll
     for (int i = 0; i < TS_ITEMS; i++) {
@@ -308,6 +311,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       s_pre[rl] = c;
     }
     __syncthreads();
+    trace_at(it, 2);
     i64 v[TS_ITEMS], sum = 0;
 #pragma unroll
     for (int i = 0; i < TS_ITEMS; i++) {
@@ -333,17 +337,21 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     __syncthreads();
     const i64 total = s_pre[TS_TILE];
     lb_publish(ts, t, total);  // successors can start summing right away
+    trace_at(it, 3);
     // Tiles whose rows average < WARP_ROW candidates: load-balanced scatter
     // (does its own look-back, overlapped with its first loads).
     if constexpr (P::kWindow) {
       if (total > 0 && total <= (i64)WARP_ROW * TS_TILE && p.window_ok()) {
         const i64 gb = p.scatter_balanced(s_pre, s_aux, total, ts, t, s_lb, wtag);
         if ((i64)t == ntiles - 1 && tid == 0) p.finish(gb + total);
+        trace_at(it, 5);
+        it++;
         __syncthreads();
         continue;
       }
     }
     const i64 gbase = lookback_block(ts, t, total, s_lb);
+    trace_at(it, 4);
     // Scatter (TS_ITEMS == 1: thread tid owns tile row tid).  Rows with fewer
     // than WARP_ROW candidates are written by their own thread (consecutive
     // rows are adjacent in the output, so a warp's stores stay dense); longer
@@ -382,8 +390,11 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       }
     }
     if ((i64)t == ntiles - 1 && tid == 0) p.finish(gbase + total);
+    trace_at(it, 5);
+    it++;
     __syncthreads();
   }
+  trace_at(3, 7);
   if (P::kAccumE) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) e_acc += __shfl_xor_sync(0xffffffffu, e_acc, o);
@@ -953,9 +964,11 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
     s_nlong = 0;
   }
   copy_desc(s_in, p.L, p.a);
+  trace_at(0, 0);
   __syncthreads();
   const i64 n = s_in.n;
   const i64 ntiles = (n + TS_TILE - 1) / TS_TILE;
+  int it = 0;
   if (ntiles == 0 && blockIdx.x == 0 && tid == 0) {
     p.O->n = 0;
     if (p.fz.stage) p.fz.finish(0);
@@ -972,6 +985,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
     }
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
+    trace_at(it, 1);
     const i64 base = (i64)t * TS_TILE;
     const i64 r = base + tid;
     // ---- count: pre-filters, expand, post-filters on short candidate lists
@@ -1024,6 +1038,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       }
       __syncthreads();
     }
+    trace_at(it, 2);
     // ---- block scan of the per-row survivor counts + look-back
     const i64 mine_cnt = s_pre[tid];
     i64 x = mine_cnt;
@@ -1040,11 +1055,13 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
     if (tid == TS_THREADS - 1) s_pre[TS_TILE] = run + mine_cnt;
     __syncthreads();
     const i64 total = s_pre[TS_TILE];
+    trace_at(it, 3);
     if (warp == 0) {
       const i64 b = lookback_warp(ts, t, total);
       if (lane == 0) s_base = b;
     }
     __syncthreads();
+    trace_at(it, 4);
     const i64 gbase = s_base;
     // ---- emit: short rows by their thread, long rows by a warp
     if (!warp_row && mine_cnt > 0) {
@@ -1083,8 +1100,11 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       p.st[p.last_slot]->overflow = !p.fz.stage && tot > p.cap;
       if (p.fz.stage) p.fz.finish(tot);
     }
+    trace_at(it, 5);
+    it++;
     __syncthreads();
   }
+  trace_at(3, 7);
   // ---- publish the step counters: warp sums, one global atomic per warp
   for (int k = 0; k < p.nslots; k++) {
     i64 e = acc[2 * k], rw = acc[2 * k + 1];
@@ -2998,6 +3018,22 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
   return true;
 }
 }  // namespace
+
+#ifdef GSM_TRACE
+// Diagnostic builds only (make trace): copy / clear the phase stamps.
+gsm_status gsm_trace_dump(uint64_t* out, int64_t n_words) {
+  const size_t cap = sizeof(gsm::g_trace) / 8;
+  GSM_CUDA(cudaDeviceSynchronize());
+  GSM_CUDA(cudaMemcpyFromSymbol(out, gsm::g_trace, 8 * std::min<size_t>((size_t)n_words, cap)));
+  return GSM_OK;
+}
+gsm_status gsm_trace_reset(void) {
+  GSM_CUDA(cudaDeviceSynchronize());
+  static std::vector<unsigned long long> z(sizeof(gsm::g_trace) / 8, 0);
+  GSM_CUDA(cudaMemcpyToSymbol(gsm::g_trace, z.data(), sizeof(gsm::g_trace)));
+  return GSM_OK;
+}
+#endif
 
 gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
                              gsm_status* statuses, gsm_result** outs, float* device_ms) {
