@@ -56,6 +56,15 @@ struct TileSync {
 // tile's block: they are cut into CHUNK-output pieces and queued, and a
 // follow-up kernel (k_drain) spreads the pieces over every SM.
 constexpr int DEFER_ROW = 256;
+// With many left tiles the blocks already share rows of a few hundred
+// candidates, but a single power-law hub (10^4-10^6 candidates) written by
+// one warp outlasts the whole kernel (phase trace of chain2 on the 100M
+// power-law store: 592 blocks done at 642 us, one hub tile until 881 us):
+// such rows are always deferred, and so are all rows >= DEFER_ROW of a tile
+// whose total output is >= HEAVY_TILE (many mid-size rows pointing at large
+// runs: one tile of that store carried ~10^6 outputs).
+constexpr int DEFER_BIG = 8192;
+constexpr i64 HEAVY_TILE = 32768;
 constexpr int CHUNK = 1024;
 struct Chunk {
   i64 r;     // left row
@@ -70,6 +79,7 @@ struct ChunkQueue {
   u32* count = nullptr;    // pieces pushed (zeroed per query)
   u32* head = nullptr;     // pieces taken by k_drain (zeroed per query)
   u32 cap = 0;
+  u32 min_len = DEFER_ROW; // rows with at least this many candidates are deferred
 };
 
 // Push row r's candidates [0, c) starting at output pos as CHUNK pieces (one
@@ -373,7 +383,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       const i64 c = s_pre[r + 1] - s_pre[r];
       const i64 pos = gbase + s_pre[r];
       const u32 aux = s_aux[r];
-      if (P::kDefer && c >= DEFER_ROW && p.dq.items) {
+      if (P::kDefer && p.dq.items && c >= (total >= HEAVY_TILE ? (i64)DEFER_ROW : (i64)p.dq.min_len)) {
         defer_row(p, s_in, p.dq, base + r, aux, c, pos);
         continue;
       }
@@ -1077,7 +1087,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       const int rl = s_long[q];
       const u32 L = s_len[rl], ax = s_aux[rl];
       i64 pos = gbase + s_pre[rl];
-      if (p.npost == 0 && L >= DEFER_ROW && p.dq.items) {
+      if (p.npost == 0 && p.dq.items && L >= (total >= HEAVY_TILE ? (u32)DEFER_ROW : p.dq.min_len)) {
         defer_row(GroupEmit{p}, s_in, p.dq, base + rl, ax, L, pos);
         continue;
       }
@@ -2286,17 +2296,20 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     int slot = 0;
     for (auto& L : launches) {
       if (L.kind != S_EXPAND && L.kind != S_FILTER && L.kind != S_GROUP) continue;
-      // Only when the left table is small: with many tiles the blocks already
-      // share the hubs, and the queue round trip would only add traffic.
+      // Rows of >= DEFER_ROW candidates when the left table is small (few
+      // tiles: the hubs would serialise on a few blocks); with many tiles the
+      // blocks already share rows of that size, and only true hubs
+      // (>= DEFER_BIG) are worth the queue round trip.
       const bool small_left = ex.ub[L.left] <= (i64)c->grid_ts * TS_TILE / 4;
-      const bool hubby = c->use_defer && small_left && L.fanout >= (u32)DEFER_ROW;
+      const u32 min_len = small_left ? (u32)DEFER_ROW : (u32)DEFER_BIG;
+      const bool hubby = c->use_defer && L.fanout >= (u32)DEFER_ROW;
       if (hubby && L.kind == S_EXPAND) {
         L.ep.dq = ChunkQueue{c->d_chunks, c->d_block->qcount + slot, c->d_block->qhead + slot,
-                             c->chunk_cap};
+                             c->chunk_cap, min_len};
         L.drain = true;
       } else if (hubby && L.kind == S_GROUP && L.gp.has_x && L.gp.npost == 0) {
         L.gp.dq = ChunkQueue{c->d_chunks, c->d_block->qcount + slot, c->d_block->qhead + slot,
-                             c->chunk_cap};
+                             c->chunk_cap, min_len};
         L.drain = true;
       }
       slot++;

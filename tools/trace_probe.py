@@ -39,13 +39,23 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--query", default="takesCourse_classmates")
     ap.add_argument("--univ", type=int, default=10)
+    ap.add_argument("--powerlaw", type=int, default=0, help="power-law store of this many triples")
+    ap.add_argument("--text", default=None, help="query text (overrides --query)")
     args = ap.parse_args()
     L = _lib.lib()
     L.gsm_trace_dump.argtypes = [C.c_void_p, C.c_int64]
     L.gsm_trace_reset.argtypes = []
     with tempfile.TemporaryDirectory() as tmp:
-        store = g.load(bench._gen_store(Path(tmp), args.univ, 0), device=0)
-        text = dict(bench.PROBES).get(args.query) or dict(bench._queries())[args.query]
+        if args.powerlaw:
+            import subprocess
+            sd = Path(tmp) / "pl"
+            subprocess.run([str(REPO / "oracle/_build/gsmgen"), "powerlaw", "--triples", str(args.powerlaw),
+                            "--predicates", "40", "--seed", "0", "--out", str(sd)], check=True,
+                           stdout=subprocess.DEVNULL)
+            store = g.load(sd, device=0)
+        else:
+            store = g.load(bench._gen_store(Path(tmp), args.univ, 0), device=0)
+        text = args.text or dict(bench.PROBES).get(args.query) or dict(bench._queries())[args.query]
         q = g.bind_constants(g.parse_query(text), store.dictionary)
         plan = g.make_plan(q, store.stats)
         for _ in range(3):
