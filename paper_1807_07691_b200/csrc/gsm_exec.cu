@@ -61,8 +61,11 @@ constexpr int DEFER_ROW = 256;
 // one warp outlasts the whole kernel (phase trace of chain2 on the 100M
 // power-law store: 592 blocks done at 642 us, one hub tile until 881 us):
 // such rows are always deferred, and so are all rows >= DEFER_ROW of a tile
-// whose total output is >= HEAVY_TILE (many mid-size rows pointing at large
-// runs: one tile of that store carried ~10^6 outputs).
+// whose total output is far above the expected tile output (>= HEAVY_TILE
+// and >= 16x the orientation's average run x tile rows: one tile of that
+// store carried ~10^6 outputs, the average ~10^3).  Uniformly heavy tiles
+// (LUBM memberOf: ~500 per row everywhere) are not deferred: the queue
+// round trip would only add traffic (204 -> 384 us when they were).
 constexpr int DEFER_BIG = 8192;
 constexpr i64 HEAVY_TILE = 32768;
 constexpr int CHUNK = 1024;
@@ -80,6 +83,7 @@ struct ChunkQueue {
   u32* head = nullptr;     // pieces taken by k_drain (zeroed per query)
   u32 cap = 0;
   u32 min_len = DEFER_ROW; // rows with at least this many candidates are deferred
+  i64 heavy = (i64)1 << 62;  // ... and every row >= DEFER_ROW of a tile with this many outputs
 };
 
 // Push row r's candidates [0, c) starting at output pos as CHUNK pieces (one
@@ -253,14 +257,15 @@ __device__ i64 lookback_block(const TileSync& ts, u32 t, i64 agg, LBShared& sh) 
 //   P::finish(total)           publish the output row count
 //   P::kAccumE                 accumulate e into st->e (filters)
 // ---------------------------------------------------------------------------
-template <class P>
+template <class P, int ITEMS = 1>
 __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, ExportArgs xa) {
-  __shared__ i64 s_pre[TS_TILE + 1];
-  __shared__ u32 s_aux[TS_TILE];
+  constexpr int TILE = TS_THREADS * ITEMS;  // rows per tile
+  __shared__ i64 s_pre[TILE + 1];
+  __shared__ u32 s_aux[TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
   __shared__ LBShared s_lb;
   __shared__ u32 s_tile;
-  __shared__ int s_long[TS_TILE];
+  __shared__ int s_long[TILE];
   __shared__ int s_nlong;
   __shared__ DTable s_in;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -280,7 +285,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   __syncthreads();
   const i64 n = p.rows(s_in);
   int it = 0;
-  const i64 ntiles = (n + TS_TILE - 1) / TS_TILE;
+  const i64 ntiles = (n + TILE - 1) / TILE;
   if (ntiles == 0 && blockIdx.x == 0 && tid == 0) p.finish(0);
   i64 e_acc = 0;
   for (bool first = true; ntiles > 0; first = false) {
@@ -296,9 +301,9 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
     trace_at(it, 1);
-    const i64 base = (i64)t * TS_TILE;
+    const i64 base = (i64)t * TILE;
 #pragma unroll
-    for (int i = 0; i < TS_ITEMS; i++) {
+    for (int i = 0; i < ITEMS; i++) {
       const int rl = i * TS_THREADS + tid;
       const i64 r = base + rl;
       u32 aux = 0, c = 0;
@@ -313,7 +318,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
         if (r < n) c = p.count(s_in, r, aux, e_acc);
 #pragma unroll
         for (int cc = 0; cc < P::WIN_A; cc++)
-          if (cc < na) P::left_tile()[cc][rl] = lv[cc];
+          if (cc < na) P::template left_tile<TILE>()[cc][rl] = lv[cc];
       } else {
         if (r < n) c = p.count(s_in, r, aux, e_acc);
       }
@@ -322,10 +327,10 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     }
     __syncthreads();
     trace_at(it, 2);
-    i64 v[TS_ITEMS], sum = 0;
+    i64 v[ITEMS], sum = 0;
 #pragma unroll
-    for (int i = 0; i < TS_ITEMS; i++) {
-      v[i] = s_pre[tid * TS_ITEMS + i];
+    for (int i = 0; i < ITEMS; i++) {
+      v[i] = s_pre[tid * ITEMS + i];
       sum += v[i];
     }
     i64 x = sum;
@@ -339,20 +344,20 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     i64 run = x - sum;
     for (int w = 0; w < warp; w++) run += s_wsum[w];
 #pragma unroll
-    for (int i = 0; i < TS_ITEMS; i++) {
-      s_pre[tid * TS_ITEMS + i] = run;
+    for (int i = 0; i < ITEMS; i++) {
+      s_pre[tid * ITEMS + i] = run;
       run += v[i];
     }
-    if (tid == TS_THREADS - 1) s_pre[TS_TILE] = run;
+    if (tid == TS_THREADS - 1) s_pre[TILE] = run;
     __syncthreads();
-    const i64 total = s_pre[TS_TILE];
+    const i64 total = s_pre[TILE];
     lb_publish(ts, t, total);  // successors can start summing right away
     trace_at(it, 3);
     // Tiles whose rows average < WARP_ROW candidates: load-balanced scatter
     // (does its own look-back, overlapped with its first loads).
     if constexpr (P::kWindow) {
-      if (total > 0 && total <= (i64)WARP_ROW * TS_TILE && p.window_ok()) {
-        const i64 gb = p.scatter_balanced(s_pre, s_aux, total, ts, t, s_lb, wtag);
+      if (total > 0 && total <= (i64)WARP_ROW * TILE && p.window_ok()) {
+        const i64 gb = p.template scatter_balanced<TILE>(s_pre, s_aux, total, ts, t, s_lb, wtag);
         if ((i64)t == ntiles - 1 && tid == 0) p.finish(gb + total);
         trace_at(it, 5);
         it++;
@@ -362,19 +367,21 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     }
     const i64 gbase = lookback_block(ts, t, total, s_lb);
     trace_at(it, 4);
-    // Scatter (TS_ITEMS == 1: thread tid owns tile row tid).  Rows with fewer
+    // Scatter (thread tid owns tile rows tid, tid + TS_THREADS, ...).  Rows with fewer
     // than WARP_ROW candidates are written by their own thread (consecutive
     // rows are adjacent in the output, so a warp's stores stay dense); longer
     // rows (hubs) are queued and written warp-cooperatively, 32 consecutive
     // outputs per store instruction, unrolled for memory-level parallelism.
-    {
-      const i64 mine = s_pre[tid + 1] - s_pre[tid];
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+      const int rl = i * TS_THREADS + tid;
+      const i64 mine = s_pre[rl + 1] - s_pre[rl];
       if (mine > 0 && mine < WARP_ROW) {
-        const i64 pos = gbase + s_pre[tid];
-        const u32 aux = s_aux[tid];
-        for (i64 j = 0; j < mine; j++) p.emit(s_in, base + tid, aux, j, pos + j);
+        const i64 pos = gbase + s_pre[rl];
+        const u32 aux = s_aux[rl];
+        for (i64 j = 0; j < mine; j++) p.emit(s_in, base + rl, aux, j, pos + j);
       } else if (mine >= WARP_ROW) {
-        s_long[atomicAdd(&s_nlong, 1)] = tid;
+        s_long[atomicAdd(&s_nlong, 1)] = rl;
       }
     }
     __syncthreads();
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       const i64 c = s_pre[r + 1] - s_pre[r];
       const i64 pos = gbase + s_pre[r];
       const u32 aux = s_aux[r];
-      if (P::kDefer && p.dq.items && c >= (total >= HEAVY_TILE ? (i64)DEFER_ROW : (i64)p.dq.min_len)) {
+      if (P::kDefer && p.dq.items && c >= (total >= p.dq.heavy ? (i64)DEFER_ROW : (i64)p.dq.min_len)) {
         defer_row(p, s_in, p.dq, base + r, aux, c, pos);
         continue;
       }
@@ -624,18 +631,20 @@ struct ExpandP {
   // neighbour loads are issued before any store; the tile's look-back runs
   // while the first round's loads are in flight.  Left values come from the
   // tile's left columns staged in shared memory by the count phase.
-  static constexpr int WIN = 2048, WIN_A = 8, SLOTS = WIN / TS_THREADS, MARK_BITS = 9;
+  static constexpr int WIN = 2048, WIN_A = 8, SLOTS = WIN / TS_THREADS, MARK_BITS = 10;
   static constexpr u32 TAG_MAX = (1u << (32 - MARK_BITS)) - 1;
-  __device__ static u32 (*left_tile())[TS_TILE] {
-    __shared__ u32 lt[WIN_A][TS_TILE];
+  template <int TILE>
+  __device__ static u32 (*left_tile())[TILE] {
+    __shared__ u32 lt[WIN_A][TILE];
     return lt;
   }
   __device__ static u32 (*marks())[WIN] {
     __shared__ u32 mk[2][WIN];
     return mk;
   }
+  template <int TILE>
   __device__ static i64* row_src() {  // per row: dst index of output slot 0
-    __shared__ i64 rs[TS_TILE];
+    __shared__ i64 rs[TILE];
     return rs;
   }
   __device__ static void window_init() {  // smem is undefined at kernel start
@@ -644,23 +653,25 @@ struct ExpandP {
   }
   __device__ int staged_cols() const { return a <= WIN_A ? a : 0; }
   __device__ bool window_ok() const { return a <= WIN_A && (!fz.stage || (fz.k >= 1 && fz.k <= 4)); }
+  template <int TILE>
   __device__ static int find_row(const i64* pre, i64 slot) {
-    int lo = 0, hi = TS_TILE;  // largest lo with pre[lo] <= slot (pre[0] = 0)
+    int lo = 0, hi = TILE;  // largest lo with pre[lo] <= slot (pre[0] = 0)
 #pragma unroll
-    for (int it = 0; it < 8; it++) {
+    for (int it = 1; it < TILE; it <<= 1) {
       const int mid = (lo + hi) >> 1;
       if (pre[mid] <= slot) lo = mid; else hi = mid;
     }
     return lo;
   }
   // A = left arity for columnar output (0: runtime a); K = fused row-major width (0: columnar)
-  template <int A, int K>
+  template <int A, int K, int TILE>
   __device__ i64 balanced_rounds(const i64* pre, i64 total, const TileSync& ts, u32 t,
                                  LBShared& lb, u32& wtag) const {
-    static_assert(TS_TILE == 256, "find_row searches 2^8 rows; marks hold row+1 in 9 bits");
+    static_assert(TILE <= (1 << (MARK_BITS - 1)), "marks hold row+1 in MARK_BITS bits");
+    constexpr int ITEMS = TILE / TS_THREADS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    u32 (*lt)[TS_TILE] = left_tile();
-    const i64* rsrc = row_src();
+    u32 (*lt)[TILE] = left_tile<TILE>();
+    const i64* rsrc = row_src<TILE>();
     i64 gbase = 0;
     int q = 0;
     for (i64 w = 0; w < total; w += WIN, q++) {
@@ -672,13 +683,15 @@ struct ExpandP {
       }
       const u32 tag = ++wtag;
       u32* m = marks()[q & 1];
-      {
-        const i64 p0 = pre[tid];
-        if (pre[tid + 1] > p0 && p0 >= w && p0 < w + WIN) m[p0 - w] = (tag << MARK_BITS) | (u32)(tid + 1);
+#pragma unroll
+      for (int i = 0; i < ITEMS; i++) {
+        const int rl = i * TS_THREADS + tid;
+        const i64 p0 = pre[rl];
+        if (pre[rl + 1] > p0 && p0 >= w && p0 < w + WIN) m[p0 - w] = (tag << MARK_BITS) | (u32)(rl + 1);
       }
       __syncthreads();
       const int ws = warp * (32 * SLOTS);  // this warp's first slot in the window
-      int carry = w + ws < total ? find_row(pre, w + ws) : 0;
+      int carry = w + ws < total ? find_row<TILE>(pre, w + ws) : 0;
       int rr[SLOTS];
 #pragma unroll
       for (int i = 0; i < SLOTS; i++) {
@@ -728,23 +741,28 @@ struct ExpandP {
     }
     return gbase;
   }
+  template <int TILE>
   __device__ i64 scatter_balanced(const i64* pre, const u32* auxv, i64 total, const TileSync& ts,
                                   u32 t, LBShared& lb, u32& wtag) const {
-    row_src()[threadIdx.x] = (i64)auxv[threadIdx.x] - pre[threadIdx.x];  // read after round 0's barrier
+#pragma unroll
+    for (int i = 0; i < TILE / TS_THREADS; i++) {  // read after round 0's barrier
+      const int rl = i * TS_THREADS + threadIdx.x;
+      row_src<TILE>()[rl] = (i64)auxv[rl] - pre[rl];
+    }
     if (fz.stage) {
       switch (fz.k) {
-        case 1: return balanced_rounds<0, 1>(pre, total, ts, t, lb, wtag);
-        case 2: return balanced_rounds<0, 2>(pre, total, ts, t, lb, wtag);
-        case 3: return balanced_rounds<0, 3>(pre, total, ts, t, lb, wtag);
-        default: return balanced_rounds<0, 4>(pre, total, ts, t, lb, wtag);
+        case 1: return balanced_rounds<0, 1, TILE>(pre, total, ts, t, lb, wtag);
+        case 2: return balanced_rounds<0, 2, TILE>(pre, total, ts, t, lb, wtag);
+        case 3: return balanced_rounds<0, 3, TILE>(pre, total, ts, t, lb, wtag);
+        default: return balanced_rounds<0, 4, TILE>(pre, total, ts, t, lb, wtag);
       }
     }
     switch (a) {
-      case 1: return balanced_rounds<1, 0>(pre, total, ts, t, lb, wtag);
-      case 2: return balanced_rounds<2, 0>(pre, total, ts, t, lb, wtag);
-      case 3: return balanced_rounds<3, 0>(pre, total, ts, t, lb, wtag);
-      case 4: return balanced_rounds<4, 0>(pre, total, ts, t, lb, wtag);
-      default: return balanced_rounds<0, 0>(pre, total, ts, t, lb, wtag);
+      case 1: return balanced_rounds<1, 0, TILE>(pre, total, ts, t, lb, wtag);
+      case 2: return balanced_rounds<2, 0, TILE>(pre, total, ts, t, lb, wtag);
+      case 3: return balanced_rounds<3, 0, TILE>(pre, total, ts, t, lb, wtag);
+      case 4: return balanced_rounds<4, 0, TILE>(pre, total, ts, t, lb, wtag);
+      default: return balanced_rounds<0, 0, TILE>(pre, total, ts, t, lb, wtag);
     }
   }
   // Fused row-major output of candidates [j0, j0+32) (value nv per lane).
@@ -1087,7 +1105,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       const int rl = s_long[q];
       const u32 L = s_len[rl], ax = s_aux[rl];
       i64 pos = gbase + s_pre[rl];
-      if (p.npost == 0 && p.dq.items && L >= (total >= HEAVY_TILE ? (u32)DEFER_ROW : p.dq.min_len)) {
+      if (p.npost == 0 && p.dq.items && L >= (total >= p.dq.heavy ? (u32)DEFER_ROW : p.dq.min_len)) {
         defer_row(GroupEmit{p}, s_in, p.dq, base + rl, ax, L, pos);
         continue;
       }
@@ -1614,6 +1632,7 @@ struct gsm_context {
   bool use_defer = true;   // spread hub rows over all SMs (k_drain)
   bool use_proj_fusion = true;  // write the projected result from the last join
   bool use_batch_graph = true;  // a repeated batch replays as one graph (gsm_execute_batch)
+  int tile_items = 0;           // expand tile rows per thread: 0 = by size, 1 or 2 (GSM_TILE_ITEMS)
   size_t stage_max = (size_t)1 << 30;  // the staging buffer grows up to this (GSM_STAGE_MAX)
   // A prepared plan: the captured launch sequence plus what the host needs
   // to replay and complete it without re-planning.
@@ -1863,6 +1882,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* nd = getenv("GSM_NO_DEFER")) c->use_defer = !(nd[0] == '1');
   if (const char* npf = getenv("GSM_NO_PROJ_FUSION")) c->use_proj_fusion = !(npf[0] == '1');
   if (const char* nb = getenv("GSM_NO_BATCH_GRAPH")) c->use_batch_graph = !(nb[0] == '1');
+  if (const char* ti = getenv("GSM_TILE_ITEMS")) c->tile_items = std::min(2, std::max(0, atoi(ti)));
   if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
@@ -2090,6 +2110,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     int last_step;  // S_GROUP: the last fused step
     u32 fanout;     // S_EXPAND: longest candidate run of the orientation
     bool drain;     // hub pieces may be queued: launch k_drain after
+    int items;      // S_EXPAND: rows per thread of a tile (1 or 2)
+    i64 avg_run;    // S_EXPAND / S_GROUP: average candidate run of the expanded orientation
   };
   std::vector<Launch> launches;
   // Step fusion state: a group is [filters][expand][filters] over one input
@@ -2227,7 +2249,23 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       }
       default: break;
     }
-    L.grid = L.kind == S_CROSS ? ex.grid_for_rows(ex.ub[L.out], 256) : ex.grid_for_rows(lub, TS_TILE);
+    // Large left tables over short runs: 512-row tiles (two rows per thread)
+    // halve the number of tiles a block walks through one after another,
+    // each paying its count -> scan -> look-back latency once (power-law 100M:
+    // chain2 0.73 -> 0.56 ms, chain3 0.54 -> 0.37 ms).  Not for few tiles
+    // (fewer blocks busy) or long runs (the tile's own work dominates).
+    L.items = 1;
+    L.avg_run = 0;
+    if (L.kind == S_EXPAND) {
+      const bool on_s = jv[0] == p.s_var;
+      const HostAux& ha = on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid];
+      const i64 avg_run = ha.key.empty() ? 0 : (i64)(ha.off.back() / ha.key.size());
+      L.avg_run = avg_run;
+      L.items = c->tile_items > 0 ? c->tile_items
+                                  : (lub >= (i64)16 * c->grid_ts * TS_TILE && avg_run <= 16 ? 2 : 1);
+    }
+    L.grid = L.kind == S_CROSS ? ex.grid_for_rows(ex.ub[L.out], 256)
+                               : ex.grid_for_rows(lub, TS_TILE * L.items);
     ex.plan[s].kind = L.kind;
     ex.plan[s].schema = out_schema;
     ex.plan[s].out_table = L.out;
@@ -2271,6 +2309,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           gp.xk = L.ep.li;
           gp.xslot = slot;
           G.fanout = L.fanout;
+          G.avg_run = L.avg_run;
+          G.items = 1;
         } else {
           FSpec fs{L.fp.R, L.fp.mode, L.fp.li, L.fp.lj, L.fp.cval, slot};
           (gp.has_x ? post : pre).push_back(fs);
@@ -2302,14 +2342,15 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       // (>= DEFER_BIG) are worth the queue round trip.
       const bool small_left = ex.ub[L.left] <= (i64)c->grid_ts * TS_TILE / 4;
       const u32 min_len = small_left ? (u32)DEFER_ROW : (u32)DEFER_BIG;
+      const i64 heavy = std::max<i64>(HEAVY_TILE, 16 * L.avg_run * (i64)TS_TILE * std::max(1, L.items));
       const bool hubby = c->use_defer && L.fanout >= (u32)DEFER_ROW;
       if (hubby && L.kind == S_EXPAND) {
         L.ep.dq = ChunkQueue{c->d_chunks, c->d_block->qcount + slot, c->d_block->qhead + slot,
-                             c->chunk_cap, min_len};
+                             c->chunk_cap, min_len, heavy};
         L.drain = true;
       } else if (hubby && L.kind == S_GROUP && L.gp.has_x && L.gp.npost == 0) {
         L.gp.dq = ChunkQueue{c->d_chunks, c->d_block->qcount + slot, c->d_block->qhead + slot,
-                             c->chunk_cap, min_len};
+                             c->chunk_cap, min_len, heavy};
         L.drain = true;
       }
       slot++;
@@ -2447,7 +2488,10 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
         case S_EXPAND: {
           TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
           slot++;
-          GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP>, L.grid, TS_THREADS, st, L.ep, ts, xm));
+          if (L.items == 2)
+            GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP, 2>, L.grid, TS_THREADS, st, L.ep, ts, xm));
+          else
+            GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP>, L.grid, TS_THREADS, st, L.ep, ts, xm));
           nk++;
           if (L.drain) {
             GSM_CUDA(launch(c->use_pdl, k_drain<ExpandP>, c->grid_ts, TS_THREADS, st, L.ep, L.ep.dq, xd));
