@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     // (does its own look-back, overlapped with its first loads).
     if constexpr (P::kWindow) {
       if (total > 0 && total <= (i64)WARP_ROW * TILE && p.window_ok()) {
-        const i64 gb = p.template scatter_balanced<TILE>(s_pre, s_aux, total, ts, t, s_lb, wtag);
+        const i64 gb = p.template scatter_balanced<TILE>(s_pre, s_aux, total, ts, t, s_lb, wtag, it);
         if ((i64)t == ntiles - 1 && tid == 0) p.finish(gb + total);
         trace_at(it, 5);
         it++;
@@ -666,7 +666,7 @@ struct ExpandP {
   // A = left arity for columnar output (0: runtime a); K = fused row-major width (0: columnar)
   template <int A, int K, int TILE>
   __device__ i64 balanced_rounds(const i64* pre, i64 total, const TileSync& ts, u32 t,
-                                 LBShared& lb, u32& wtag) const {
+                                 LBShared& lb, u32& wtag, int trace_it) const {
     static_assert(TILE <= (1 << (MARK_BITS - 1)), "marks hold row+1 in MARK_BITS bits");
     constexpr int ITEMS = TILE / TS_THREADS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -711,7 +711,10 @@ struct ExpandP {
         const i64 slot = w + ws + i * 32 + lane;
         nv[i] = rr[i] >= 0 ? __ldg(R.dst + (rsrc[rr[i]] + slot)) : 0u;
       }
-      if (q == 0) gbase = lookback_block(ts, t, total, lb);  // while the loads are in flight
+      if (q == 0) {
+        gbase = lookback_block(ts, t, total, lb);  // while the loads are in flight
+        trace_at(trace_it, 6);
+      }
 #pragma unroll
       for (int i = 0; i < SLOTS; i++) {
         const i64 g = gbase + w + ws + i * 32 + lane;
@@ -738,12 +741,13 @@ struct ExpandP {
           }
         }
       }
+      if (q == 0) trace_at(trace_it, 7);
     }
     return gbase;
   }
   template <int TILE>
   __device__ i64 scatter_balanced(const i64* pre, const u32* auxv, i64 total, const TileSync& ts,
-                                  u32 t, LBShared& lb, u32& wtag) const {
+                                  u32 t, LBShared& lb, u32& wtag, int trace_it = 0) const {
 #pragma unroll
     for (int i = 0; i < TILE / TS_THREADS; i++) {  // read after round 0's barrier
       const int rl = i * TS_THREADS + threadIdx.x;
@@ -751,18 +755,18 @@ struct ExpandP {
     }
     if (fz.stage) {
       switch (fz.k) {
-        case 1: return balanced_rounds<0, 1, TILE>(pre, total, ts, t, lb, wtag);
-        case 2: return balanced_rounds<0, 2, TILE>(pre, total, ts, t, lb, wtag);
-        case 3: return balanced_rounds<0, 3, TILE>(pre, total, ts, t, lb, wtag);
-        default: return balanced_rounds<0, 4, TILE>(pre, total, ts, t, lb, wtag);
+        case 1: return balanced_rounds<0, 1, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+        case 2: return balanced_rounds<0, 2, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+        case 3: return balanced_rounds<0, 3, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+        default: return balanced_rounds<0, 4, TILE>(pre, total, ts, t, lb, wtag, trace_it);
       }
     }
     switch (a) {
-      case 1: return balanced_rounds<1, 0, TILE>(pre, total, ts, t, lb, wtag);
-      case 2: return balanced_rounds<2, 0, TILE>(pre, total, ts, t, lb, wtag);
-      case 3: return balanced_rounds<3, 0, TILE>(pre, total, ts, t, lb, wtag);
-      case 4: return balanced_rounds<4, 0, TILE>(pre, total, ts, t, lb, wtag);
-      default: return balanced_rounds<0, 0, TILE>(pre, total, ts, t, lb, wtag);
+      case 1: return balanced_rounds<1, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+      case 2: return balanced_rounds<2, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+      case 3: return balanced_rounds<3, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+      case 4: return balanced_rounds<4, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+      default: return balanced_rounds<0, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
     }
   }
   // Fused row-major output of candidates [j0, j0+32) (value nv per lane).

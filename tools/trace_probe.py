@@ -6,7 +6,8 @@ trace -> libgsmat_b200_trace.so), runs one query on the LUBM store and reads
 the %globaltimer stamps thread 0 of every block wrote at the phase
 boundaries of its first tiles (gsm_common.cuh trace_at):
   0 prologue done, 1 tile grabbed, 2 count done, 3 scan + publish done,
-  4 look-back done (non-window path), 5 tile done; (3,7) = block end.
+  4 look-back done (non-window path), 5 tile done, 6 window look-back done
+  (round 0's loads in flight), 7 window round 0 stored; (3,7) = block end.
 Usage: python tools/trace_probe.py [--query takesCourse_classmates|qNN] [--univ 10]
 """
 from __future__ import annotations
@@ -93,7 +94,8 @@ def main():
     tiles = [sum(1 for it in range(4) if it * 8 + 1 in st) for st in blocks]
     print("tiles per block:", {k: tiles.count(k) for k in sorted(set(tiles))})
     names = {(1, 2): "count", (2, 3): "scan+publish", (3, 4): "look-back",
-             (4, 5): "scatter", (3, 5): "look-back+scatter", (1, 5): "tile"}
+             (4, 5): "scatter", (3, 6): "window look-back", (6, 7): "window round 0",
+             (7, 5): "window rounds 1+", (3, 5): "look-back+scatter", (1, 5): "tile"}
     for it in range(3):
         rows = []
         for (a, b), nm in names.items():
