@@ -22,6 +22,7 @@
 // power-law tail (>= 256) as 1024-output pieces drained by k_drain on every SM.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <utility>
 #include <cstdio>
 #include <cstdlib>
@@ -3096,8 +3097,27 @@ gsm_status gsm_trace_reset(void) {
 }
 #endif
 
+// Host-side phase times of gsm_execute_batch (GSM_HOST_TIMING=1: summary on
+// stderr at exit) — the e2e path's host overhead, phase by phase.
+namespace {
+struct HostTimes {
+  double launch = 0, wait = 0, complete = 0;
+  long calls = 0;
+  bool on = getenv("GSM_HOST_TIMING") && getenv("GSM_HOST_TIMING")[0] == '1';
+  ~HostTimes() {
+    if (on && calls)
+      fprintf(stderr, "gsm host timing: %ld batches, per batch: launch %.1f us, wait %.1f us, complete %.1f us\n",
+              calls, 1e6 * launch / calls, 1e6 * wait / calls, 1e6 * complete / calls);
+  }
+} g_host_times;
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
 gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
                              gsm_status* statuses, gsm_result** outs, float* device_ms) {
+  const double t_begin = g_host_times.on ? now_s() : 0.0;
   if (n_queries < 0 || (n_queries > 0 && (!ctxs || !queries || !outs)))
     return set_error(GSM_ERR_VALUE, "bad batch arguments");
   for (int i = 0; i < n_queries; i++) {
@@ -3138,6 +3158,12 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
     }
   }
   // Complete in order (budget checks, retries, result hand-off).
+  double t_launched = 0, t_waited = 0;
+  if (g_host_times.on) {
+    t_launched = now_s();
+    if (n_queries > 0) cudaStreamSynchronize(as_graph ? ctxs[0]->stream : ctxs[n_queries - 1]->stream);
+    t_waited = now_s();
+  }
   gsm_status first = GSM_OK;
   std::string first_msg;
   for (int i = 0; i < n_queries; i++) {
@@ -3154,6 +3180,13 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
   if (timed && cudaEventElapsedTime(device_ms, ctxs[0]->ev_b0, ctxs[0]->ev_b1) != cudaSuccess) {
     *device_ms = -1.f;
     cudaGetLastError();
+  }
+  if (g_host_times.on) {
+    const double t_end = now_s();
+    g_host_times.launch += t_launched - t_begin;
+    g_host_times.wait += t_waited - t_launched;
+    g_host_times.complete += t_end - t_waited;
+    g_host_times.calls++;
   }
   if (first != GSM_OK) set_error(first, first_msg);
   return first;
