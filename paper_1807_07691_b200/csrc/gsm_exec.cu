@@ -1991,6 +1991,7 @@ struct ExecState {
   bool big = false;           // this plan's last result outgrew the staging buffer
   gsm_context::GraphEntry meta;
   cudaStream_t sync_stream = nullptr;  // first completion waits here (batch graph)
+  bool synced = false;                 // ... or the caller already waited for it
 };
 
 // Restore a prepared plan into the context: query-block image with fresh
@@ -2704,7 +2705,8 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
       gsm_status stt = launch_query(c, qa, S);
       if (stt != GSM_OK) return stt;
     }
-    GSM_CUDA(cudaStreamSynchronize(attempt == 0 && S.sync_stream ? S.sync_stream : c->stream));
+    if (!(attempt == 0 && S.synced))
+      GSM_CUDA(cudaStreamSynchronize(attempt == 0 && S.sync_stream ? S.sync_stream : c->stream));
     memcpy(c->h_block->stats, c->h_stage, sizeof(StepStat) * (size_t)(n + 1));
     const QueryBlock* hb = c->h_block;
     // Budget checks in plan order (executor.py:158-163, 192-193, 237-241).
@@ -2944,6 +2946,8 @@ gsm_status gsm_execute_seeded(gsm_context* c, const uint32_t* seed_rows, int64_t
 }
 
 namespace {
+double g_graph_launch_s = 0;  // host time inside cudaGraphLaunch (GSM_HOST_TIMING)
+void note_graph_launch(double s) { g_graph_launch_s += s; }
 // Make sure the next `need` epochs of a context need no status re-zeroing
 // (reserve_epochs' wrap enqueues a memset on the context's own stream, which a
 // batch graph launched on another stream would not be ordered after).
@@ -3071,10 +3075,12 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     }
   }
   if (timed && cudaEventRecord(c0->ev_b0, s0) != cudaSuccess) return false;
+  const auto tg0 = std::chrono::steady_clock::now();
   if (cudaGraphLaunch(it->second.exec, s0) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
+  note_graph_launch(std::chrono::duration<double>(std::chrono::steady_clock::now() - tg0).count());
   if (timed) cudaEventRecord(c0->ev_b1, s0);
   for (int i = 0; i < n; i++) S[i].sync_stream = s0;
   return true;
@@ -3101,13 +3107,16 @@ gsm_status gsm_trace_reset(void) {
 // stderr at exit) — the e2e path's host overhead, phase by phase.
 namespace {
 struct HostTimes {
-  double launch = 0, wait = 0, complete = 0;
+  double launch = 0, wait = 0, complete = 0, graph_launch = 0;
   long calls = 0;
   bool on = getenv("GSM_HOST_TIMING") && getenv("GSM_HOST_TIMING")[0] == '1';
   ~HostTimes() {
     if (on && calls)
-      fprintf(stderr, "gsm host timing: %ld batches, per batch: launch %.1f us, wait %.1f us, complete %.1f us\n",
-              calls, 1e6 * launch / calls, 1e6 * wait / calls, 1e6 * complete / calls);
+      fprintf(stderr,
+              "gsm host timing: %ld batches, per batch: launch %.1f us (cudaGraphLaunch %.1f us), "
+              "wait %.1f us, complete %.1f us\n",
+              calls, 1e6 * launch / calls, 1e6 * graph_launch / calls, 1e6 * wait / calls,
+              1e6 * complete / calls);
   }
 } g_host_times;
 double now_s() {
@@ -3164,6 +3173,10 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
     if (n_queries > 0) cudaStreamSynchronize(as_graph ? ctxs[0]->stream : ctxs[n_queries - 1]->stream);
     t_waited = now_s();
   }
+  if (as_graph && n_queries > 0) {  // one wait for the whole batch graph
+    GSM_CUDA(cudaStreamSynchronize(ctxs[0]->stream));
+    for (int i = 0; i < n_queries; i++) S[i].synced = true;
+  }
   gsm_status first = GSM_OK;
   std::string first_msg;
   for (int i = 0; i < n_queries; i++) {
@@ -3186,6 +3199,7 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
     g_host_times.launch += t_launched - t_begin;
     g_host_times.wait += t_waited - t_launched;
     g_host_times.complete += t_end - t_waited;
+    g_host_times.graph_launch = g_graph_launch_s;
     g_host_times.calls++;
   }
   if (first != GSM_OK) set_error(first, first_msg);
