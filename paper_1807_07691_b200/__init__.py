@@ -24,7 +24,7 @@ from .executor import (
     execute_batch,
 )
 from .frontend import Plan, QueryGraph, TriplePattern, bind_constants, make_plan, parse_query
-from .decode import decode_rows, format_term, result_tsv
+from .decode import decode_rows, format_term, result_tsv, write_tsv
 from .ingest import build, parse_ntriples
 from .storage import DeviceStore, StatEntry, from_store, load
 
@@ -34,6 +34,7 @@ __all__ = [
     "decode_rows",
     "format_term",
     "result_tsv",
+    "write_tsv",
     "BindingTable",
     "DEFAULT_ROW_BUDGET",
     "DeviceStore",

@@ -83,6 +83,16 @@ def decode_rows(store, rows: np.ndarray) -> bytes:
         L.gsm_text_free(txt)
 
 
+def write_tsv(result, store, fh) -> int:
+    """Write what ``gsmat query`` prints (cli.py:101-105) to a binary file
+    object without building a Python str; returns the bytes written."""
+    head = ("\t".join(result.schema) + "\n").encode("utf-8")
+    body = decode_rows(store, result.array)
+    fh.write(head)
+    fh.write(body)
+    return len(head) + len(body)
+
+
 def result_tsv(result, store) -> str:
     """What ``gsmat query`` prints for a result (cli.py:101-105): the schema
     line, then one decoded line per row."""

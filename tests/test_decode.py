@@ -69,6 +69,10 @@ def test_decode_worked_example():
     q = g.bind_constants(g.parse_query(text), store.dictionary)
     res = g.execute(q, g.make_plan(q, store.stats), store)
     assert g.result_tsv(res, store).splitlines() == ["?x\t?y\t?z\t?w", "<A>\t<B>\t<C>\t<I2>"]
+    import io
+    buf = io.BytesIO()
+    assert g.write_tsv(res, store, buf) == len(buf.getvalue())
+    assert buf.getvalue().decode("utf-8") == g.result_tsv(res, store)
 
 
 @pytest.mark.gpu

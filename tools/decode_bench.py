@@ -40,10 +40,11 @@ def main():
         for name, text in QUERIES.items():
             q = g.bind_constants(g.parse_query(text), st.dictionary)
             res = g.execute(q, g.make_plan(q, st.stats), st, row_budget=1 << 62)
-            g.result_tsv(res, st)  # dictionary upload + warm-up
+            g.decode_rows(st, res.array[:10])  # dictionary upload + warm-up
             t0 = time.perf_counter()
-            out = g.result_tsv(res, st)
+            body = g.decode_rows(st, res.array)  # the TSV body as bytes
             ours = time.perf_counter() - t0
+            out = ("\t".join(res.schema) + "\n").encode() + body
             arr = res.array
             n = len(arr)
             sample = min(n, 200_000)
@@ -51,6 +52,7 @@ def main():
             ref = "\t".join(res.schema) + "\n" + "".join(
                 "\t".join(g.format_term(dec(int(v))) for v in row) + "\n" for row in arr[:sample].tolist())
             loop = time.perf_counter() - t0
+            ref = ref.encode("utf-8")
             head = out[: len(ref)]
             print(json.dumps({"query": name, "rows": n, "bytes": len(out), "ours_s": round(ours, 4),
                               "ours_rows_per_s": round(n / ours, 1),
