@@ -558,34 +558,43 @@ struct ExpandP {
   template <int K>
   __device__ void row_warp_fused(const DTable& s, i64 r, u32 aux, i64 c, i64 pos) const {
     // row-major, K words per row: lane l of a 32-row chunk writes words
-    // l, l+32, ..., (K-1)*32+l of the chunk; word w is column w % K of row w / K
+    // l, l+32, ..., (K-1)*32+l of the chunk; word w is column w % K of row
+    // w / K.  The lane's (row, column, value) per word do not depend on the
+    // chunk, so they are set up once; U chunks of candidates are loaded
+    // before any is stored (as in row_warp_cols: the chunk loop would
+    // otherwise wait one memory round trip per 32 candidates).
+    constexpr int U = 4;
     const int lane = threadIdx.x & 31;
-    u32 cv[K];      // value of each projected column when it is a left column
-    bool isnew[K];  // projected column is the expanded one
+    int rr[K];
+    u32 val[K];
+    bool nw[K];
 #pragma unroll
     for (int x = 0; x < K; x++) {
-      const int src = fz.pj[x];
-      isnew[x] = src >= a;
-      cv[x] = src < a ? __ldg(s.col[src] + r) : 0u;
+      const int w = x * 32 + lane;
+      rr[x] = w / K;
+      const int src = fz.pj[w - rr[x] * K];
+      nw[x] = src >= a;
+      val[x] = src < a ? __ldg(s.col[src] + r) : 0u;
     }
     const u32* dsrc = R.dst + aux;
-    for (i64 j0 = 0; j0 < c; j0 += 32) {
-      const i64 j = j0 + lane;
-      const u32 nv = j < c ? __ldg(dsrc + j) : 0u;
-      const i64 base = pos + j0;
-      const int rows = (int)min((i64)32, c - j0);
+    for (i64 j0 = 0; j0 < c; j0 += 32 * U) {
+      u32 nv[U];
 #pragma unroll
-      for (int x = 0; x < K; x++) {
-        const int w = x * 32 + lane;
-        const int rr = w / K, cc = w - rr * K;
-        u32 val = cv[0];
+      for (int u = 0; u < U; u++) {
+        const i64 j = j0 + 32 * u + lane;
+        nv[u] = j < c ? __ldg(dsrc + j) : 0u;
+      }
 #pragma unroll
-        for (int y = 1; y < K; y++) val = cc == y ? cv[y] : val;
-        bool nw = isnew[0];
+      for (int u = 0; u < U; u++) {
+        const i64 jb = j0 + 32 * u;
+        if (jb >= c) break;
+        const i64 base = pos + jb;
+        const int rows = (int)min((i64)32, c - jb);
 #pragma unroll
-        for (int y = 1; y < K; y++) nw = cc == y ? isnew[y] : nw;
-        const u32 nvr = __shfl_sync(0xffffffffu, nv, rr);
-        if (rr < rows && base + rr < fz.cap) fz.stage[base * K + w] = nw ? nvr : val;
+        for (int x = 0; x < K; x++) {
+          const u32 nvr = __shfl_sync(0xffffffffu, nv[u], rr[x]);
+          if (rr[x] < rows && base + rr[x] < fz.cap) fz.stage[base * K + x * 32 + lane] = nw[x] ? nvr : val[x];
+        }
       }
     }
   }
