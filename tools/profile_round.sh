@@ -19,7 +19,7 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
 # skip the first launches of each probe (the first execution may overflow the
 # arena and re-run): capture a steady-state launch
 for p in memberOf_coworkers takesCourse_classmates; do
-  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:ExpandP -s 3 -c 1 \
+  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_tilescan.*ExpandP" -s 3 -c 1 \
       -o $out/prof_probe_$p python bench.py --only-probe --probe $p > $out/ncu_probe_$p.log 2>&1
 done
 echo done
