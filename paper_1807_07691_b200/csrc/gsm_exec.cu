@@ -3031,7 +3031,9 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       return false;
     }
     bool ok = cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
-    for (int i = 1; i < n && ok; i++) ok = cudaStreamWaitEvent(ctxs[i]->stream, c0->ev_fork, 0) == cudaSuccess;
+    int forked = 1;  // streams joined to the capture (ctxs[0]'s is the origin)
+    for (; forked < n && ok; forked++) ok = cudaStreamWaitEvent(ctxs[forked]->stream, c0->ev_fork, 0) == cudaSuccess;
+    if (!ok) forked--;
     // No programmatic dependent launch inside a batch: early-launched
     // dependents sit on SMs waiting for their predecessor and take the slots
     // the other queries' kernels need (measured: batch 0.096 -> 0.086 ms on
@@ -3045,9 +3047,14 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       S[i].capture_only = false;
       ctxs[i]->use_pdl = pdl;
     }
-    for (int i = 1; i < n && ok; i++)
-      ok = cudaEventRecord(ctxs[i]->ev_done, ctxs[i]->stream) == cudaSuccess &&
-           cudaStreamWaitEvent(s0, ctxs[i]->ev_done, 0) == cudaSuccess;
+    // Join every forked stream back, also after a failed plan (a planning
+    // error returns before issuing anything): an unjoined stream would leave
+    // the capture in an invalid state for the fallback path.
+    for (int i = 1; i < forked; i++) {
+      const bool j = cudaEventRecord(ctxs[i]->ev_done, ctxs[i]->stream) == cudaSuccess &&
+                     cudaStreamWaitEvent(s0, ctxs[i]->ev_done, 0) == cudaSuccess;
+      ok = ok && j;
+    }
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(s0, &g);
     cudaGraphExec_t ge = nullptr;

@@ -322,3 +322,48 @@ def test_execute_batch_matches_sequential(store_factory):
     bad = items[:3] + [_plan(store, q9)]
     with pytest.raises(g.ResourceLimitError, match="pre-allocated join region"):
         g.execute_batch(bad, store, row_budget=5)
+
+
+def test_batch_planning_error_falls_back(store_factory):
+    """A query of a batch that fails while its launch sequence is being
+    captured (here: a projection naming a variable the plan never binds,
+    built through the C ABI) reports its own error; the other queries of the
+    batch still complete, and the contexts keep working afterwards."""
+    import ctypes as C
+
+    from paper_1807_07691_b200 import _lib
+    from paper_1807_07691_b200.executor import compile_plan
+
+    store = g.load(store_factory("lubm", univ=1, seed=0))
+    items = [_plan(store, text) for _, text in lubm_queries()[:4]]
+    good = g.execute_batch(items, store)
+    good = g.execute_batch(items, store)  # replayed batch graph
+    n = len(items)
+    L = _lib.lib()
+    ctxs = store.context_pool(n)
+    qarr = (_lib.Query * n)()
+    keep = []
+    for i, (q, p) in enumerate(items):
+        steps, arr, proj_arr, nproj = compile_plan(q, p)
+        keep.append((arr, proj_arr))
+        rec = qarr[i]
+        rec.steps, rec.n_steps, rec.proj, rec.n_proj = arr, len(steps), proj_arr, nproj
+        rec.distinct, rec.part_index, rec.part_count = 0, 0, 1
+        rec.row_budget, rec.budget_mode = 1 << 40, _lib.GSM_BUDGET_PARALLEL
+        rec.report = None
+    bad = (C.c_int32 * 1)(30)
+    qarr[2].proj, qarr[2].n_proj = bad, 1
+    outs = (C.c_void_p * n)()
+    statuses = (C.c_int32 * n)()
+    st = L.gsm_execute_batch((C.c_void_p * n)(*[c.value for c in ctxs]), n, qarr, statuses, outs, None)
+    assert st == _lib.GSM_ERR_VALUE
+    assert "not bound" in _lib.last_error()
+    assert [statuses[i] for i in range(n)] == [0, 0, _lib.GSM_ERR_VALUE, 0]
+    nrows = (C.c_int64 * n)()
+    ncols = (C.c_int32 * n)()
+    L.gsm_results_shape(outs, n, nrows, ncols)
+    assert [int(nrows[i]) for i in (0, 1, 3)] == [len(good[i]) for i in (0, 1, 3)]
+    L.gsm_results_copy(outs, n, None, 1)
+    again = g.execute_batch(items, store)
+    for a, b in zip(again, good):
+        assert orc.fingerprint_array(a.array) == orc.fingerprint_array(b.array)
