@@ -311,6 +311,16 @@ gsm_status gsm_ntriples_parse(const char* buf, int64_t nbytes, int32_t threads, 
 gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t device, int32_t threads,
                            int64_t* counts);
 
+/* Replaces storage.build_store's partition / set / sort (storage.py:165-177)
+ * for encoded triples (s[i], p[i], o[i]), p[i] <= max_pid: duplicates are
+ * dropped and both orders sorted on the device.  so_pairs / os_pairs get the
+ * pair-file images (u64 LE pairs) of every predicate in pid order; counts
+ * (3 x (max_pid + 1) entries) = per pid (pairs, distinct subjects, distinct
+ * objects). */
+gsm_status gsm_sort_triples(int32_t device, const uint32_t* s, const uint32_t* p, const uint32_t* o,
+                            int64_t n, int32_t max_pid, gsm_text** so_pairs, gsm_text** os_pairs,
+                            int64_t* counts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,7 @@ EXPORTS = (
     "gsm_text_free",
     "gsm_ntriples_parse",
     "gsm_build_store",
+    "gsm_sort_triples",
 )
 
 
@@ -147,6 +148,7 @@ def lib() -> C.CDLL:
             "gsm_text_free": (i32, [vp]),
             "gsm_ntriples_parse": (i32, [C.c_char_p, i64, i32, P(vp)]),
             "gsm_build_store": (i32, [C.c_char_p, C.c_char_p, i32, i32, P(i64)]),
+            "gsm_sort_triples": (i32, [i32, vp, vp, vp, i64, i32, P(vp), P(vp), P(i64)]),
             "gsm_store_device_bytes": (i32, [vp, P(i64)]),
             "gsm_store_free": (i32, [vp]),
             "gsm_context_create": (i32, [vp, i64, P(vp)]),

@@ -370,6 +370,50 @@ gsm_status gsm_ntriples_parse(const char* buf, int64_t nbytes, int32_t threads, 
   return GSM_OK;
 }
 
+// storage.build_store's partition / deduplicate / sort (storage.py:165-177)
+// for already encoded triples: the (p, s, o) and (p, o, s) orders on the
+// device.  so_pairs / os_pairs receive the pair-file images (u64 LE (key,
+// value) pairs) of all predicates in pid order; counts[3 * pid + {0, 1, 2}]
+// = (pairs, distinct subjects, distinct objects) for pid in [0, max_pid].
+gsm_status gsm_sort_triples(int32_t device, const uint32_t* s, const uint32_t* p, const uint32_t* o,
+                            int64_t n, int32_t max_pid, gsm_text** so_pairs, gsm_text** os_pairs,
+                            int64_t* counts) {
+  *so_pairs = *os_pairs = nullptr;
+  if (n < 0 || max_pid < 0 || (n > 0 && (!s || !p || !o)) || !counts)
+    return set_error(GSM_ERR_VALUE, "bad arguments");
+  for (int64_t i = 0; i < n; i++)
+    if ((int64_t)p[i] > max_pid) return set_error(GSM_ERR_VALUE, "predicate id above max_pid");
+  GSM_CUDA(cudaSetDevice(device));
+  cudaStream_t cs;
+  GSM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{cs};
+  std::vector<u64> kso((size_t)n), kos((size_t)n);
+  std::vector<u32> pid(p, p + n);
+  for (int64_t i = 0; i < n; i++) {
+    kso[(size_t)i] = ((u64)s[i] << 32) | o[i];
+    kos[(size_t)i] = ((u64)o[i] << 32) | s[i];
+  }
+  std::vector<u64> sp, op, so_rows, so_heads, os_rows, os_heads;
+  gsm_status st = build_orientation(kso, pid, (u32)max_pid, cs, sp, so_rows, so_heads);
+  if (st != GSM_OK) return st;
+  if ((st = build_orientation(kos, pid, (u32)max_pid, cs, op, os_rows, os_heads)) != GSM_OK) return st;
+  gsm_text* a = new gsm_text();
+  gsm_text* b = new gsm_text();
+  a->bytes.assign(reinterpret_cast<const char*>(sp.data()), reinterpret_cast<const char*>(sp.data() + sp.size()));
+  b->bytes.assign(reinterpret_cast<const char*>(op.data()), reinterpret_cast<const char*>(op.data() + op.size()));
+  for (int32_t q = 0; q <= max_pid; q++) {
+    counts[3 * q] = q < (int32_t)so_rows.size() ? (int64_t)so_rows[q] : 0;
+    counts[3 * q + 1] = q < (int32_t)so_heads.size() ? (int64_t)so_heads[q] : 0;
+    counts[3 * q + 2] = q < (int32_t)os_heads.size() ? (int64_t)os_heads[q] : 0;
+  }
+  *so_pairs = a;
+  *os_pairs = b;
+  return GSM_OK;
+}
+
 gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t device, int32_t threads,
                            int64_t* counts) {
   if (!nt_path || !out_dir) return set_error(GSM_ERR_VALUE, "null path");

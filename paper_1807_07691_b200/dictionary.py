@@ -117,3 +117,86 @@ class StoreDictionary:
         if not 1 <= id_ <= self._preds.count:
             raise UnknownIdError("predicate", id_)
         return self._preds.term(id_)
+
+    def save(self, directory: Path | str) -> None:
+        """TermDictionary.save (dictionary.py:95-104): the files as read."""
+        directory = Path(directory)
+        for name, tf in ((NODES_FILE, self._nodes), (PREDS_FILE, self._preds)):
+            data = tf.buf
+            if data and not data.endswith(b"\n"):
+                data += b"\n"
+            (directory / name).write_bytes(data)
+
+
+class TermDictionary:
+    """dictionary.TermDictionary (dictionary.py:46-125): two first-occurrence
+    ordered bijections (nodes, predicates), dense 1-based ids, the reference's
+    one-term-per-line persistence.  Host-side state of the build path
+    (:func:`paper_1807_07691_b200.storage.build_store`)."""
+
+    def __init__(self) -> None:
+        self.node_terms: list[str] = []
+        self.pred_terms: list[str] = []
+        self.node_index: dict[str, int] = {}
+        self.pred_index: dict[str, int] = {}
+
+    def encode_node(self, term: str) -> int:
+        nid = self.node_index.get(term)
+        if nid is None:
+            self.node_terms.append(term)
+            nid = len(self.node_terms)
+            self.node_index[term] = nid
+        return nid
+
+    def encode_predicate(self, term: str) -> int:
+        pid = self.pred_index.get(term)
+        if pid is None:
+            self.pred_terms.append(term)
+            pid = len(self.pred_terms)
+            self.pred_index[term] = pid
+        return pid
+
+    def lookup_node(self, term: str) -> int | None:
+        return self.node_index.get(term)
+
+    def lookup_predicate(self, term: str) -> int | None:
+        return self.pred_index.get(term)
+
+    def decode_node(self, id_: int) -> str:
+        if not 1 <= id_ <= len(self.node_terms):
+            raise UnknownIdError("node", id_)
+        return self.node_terms[id_ - 1]
+
+    def decode_predicate(self, id_: int) -> str:
+        if not 1 <= id_ <= len(self.pred_terms):
+            raise UnknownIdError("predicate", id_)
+        return self.pred_terms[id_ - 1]
+
+    @property
+    def node_count(self) -> int:
+        return len(self.node_terms)
+
+    @property
+    def predicate_count(self) -> int:
+        return len(self.pred_terms)
+
+    def save(self, directory: Path | str) -> None:
+        directory = Path(directory)
+        for name, terms in ((NODES_FILE, self.node_terms), (PREDS_FILE, self.pred_terms)):
+            with open(directory / name, "w", encoding="utf-8", newline="\n") as fh:
+                for term in terms:
+                    fh.write(escape_term(term))
+                    fh.write("\n")
+
+    @classmethod
+    def load(cls, directory: Path | str) -> "TermDictionary":
+        directory = Path(directory)
+        d = cls()
+        for name, encode in ((NODES_FILE, d.encode_node), (PREDS_FILE, d.encode_predicate)):
+            path = directory / name
+            if not path.exists():
+                raise StoreFormatError(f"missing dictionary file {path}")
+            with open(path, encoding="utf-8", newline="\n") as fh:
+                for raw in fh:
+                    encode(unescape_term(raw.rstrip("\n")))
+        return d

@@ -288,3 +288,83 @@ def from_store(store, device: int = 0) -> DeviceStore:
     except TypeError:  # not weak-referenceable: no caching
         pass
     return dev
+
+
+# -- build / persist (storage.py:165-219) -----------------------------------
+
+class EncodedTriple(NamedTuple):
+    """storage.EncodedTriple: one triple of dictionary ids."""
+
+    s: int
+    p: int
+    o: int
+
+
+# The reference's names for the store and its per-predicate matrices.
+Store = DeviceStore
+PredicateMatrix = PairMatrix
+
+
+def build_store(dictionary, triples, device: int = 0) -> DeviceStore:
+    """storage.build_store (storage.py:165-177): partition encoded triples by
+    predicate, drop duplicates, sort both orientations and index them — the
+    deduplication and sorting on the device (``gsm_sort_triples``); the
+    result is already resident on ``device``."""
+    rows = [tuple(t) for t in triples]
+    arr = np.asarray(rows, dtype=np.uint64).reshape(-1, 3)
+    if arr.size and int(arr.max()) >= 1 << 32:
+        raise ValueError("ids must be < 2^32")
+    s_ = np.ascontiguousarray(arr[:, 0], dtype=np.uint32)
+    p_ = np.ascontiguousarray(arr[:, 1], dtype=np.uint32)
+    o_ = np.ascontiguousarray(arr[:, 2], dtype=np.uint32)
+    n = arr.shape[0]
+    max_pid = int(p_.max()) if n else 0
+    counts = (C.c_int64 * (3 * (max_pid + 1)))()
+    L = _lib.lib()
+    t_so, t_os = C.c_void_p(), C.c_void_p()
+    _lib.check(L.gsm_sort_triples(int(device), s_.ctypes.data if n else None, p_.ctypes.data if n else None,
+                                  o_.ctypes.data if n else None, n, max_pid, C.byref(t_so), C.byref(t_os),
+                                  counts))
+
+    def take(t) -> np.ndarray:
+        try:
+            ptr, nb = C.c_void_p(), C.c_int64()
+            _lib.check(L.gsm_text_data(t, C.byref(ptr), C.byref(nb)))
+            raw = C.string_at(ptr, nb.value) if nb.value else b""
+        finally:
+            L.gsm_text_free(t)
+        return np.frombuffer(raw, dtype="<u8").reshape(-1, 2)
+
+    so_all, os_all = take(t_so), take(t_os)
+    matrices: dict[int, PairMatrix] = {}
+    stats: dict[int, StatEntry] = {}
+    off = 0
+    for pid in range(max_pid + 1):
+        card, ds, do = (int(counts[3 * pid + k]) for k in range(3))
+        if card == 0:
+            continue
+        matrices[pid] = PairMatrix(pid, so_all[off:off + card], os_all[off:off + card])
+        stats[pid] = StatEntry(card, ds, do)
+        off += card
+    node_count = max(int(dictionary.node_count), int(arr[:, [0, 2]].max()) if n else 0)
+    return DeviceStore(dictionary, matrices, stats, node_count, device=device)
+
+
+def persist(store, directory: Path | str) -> None:
+    """storage.persist (storage.py:203-219): the reference's store directory
+    (dictionary files, meta, stats.tsv, p<ID>.so / p<ID>.os u64 LE pairs)."""
+    directory = Path(directory)
+    directory.mkdir(parents=True, exist_ok=True)
+    store.dictionary.save(directory)
+    matrices = store.matrices
+    triple_count = sum(int(np.asarray(m.so).shape[0]) for m in matrices.values())
+    with open(directory / META_FILE, "w", encoding="ascii", newline="\n") as fh:
+        fh.write(f"{MAGIC}\n{triple_count}\n{len(matrices)}\n{store.dictionary.node_count}\n")
+    with open(directory / STATS_FILE, "w", encoding="ascii", newline="\n") as fh:
+        for pid in sorted(store.stats):
+            st = store.stats[pid]
+            fh.write(f"{pid}\t{st.cardinality}\t{st.distinct_subjects}\t{st.distinct_objects}\n")
+    for pid in sorted(matrices):
+        m = matrices[pid]
+        (directory / f"p{pid}.so").write_bytes(np.ascontiguousarray(m.so, dtype="<u8").tobytes())
+        (directory / f"p{pid}.os").write_bytes(np.ascontiguousarray(m.os, dtype="<u8").tobytes())

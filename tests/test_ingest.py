@@ -154,3 +154,70 @@ def test_build_round_trip_large(tmp_path, store_factory):
                 out.add((dn(s), name, dn(o)))
         return out
     assert triples(st, d2, p2) == triples(src, dec, decp)
+
+
+def test_delta_bounds_and_dictionary_match_reference(tmp_path):
+    """planner.delta_bounds and dictionary.TermDictionary restated."""
+    if not reference_available():
+        pytest.skip("reference package not installed")
+    from gsmat import dictionary as rdict
+    from gsmat import planner
+
+    rng = random.Random(4)
+    for _ in range(200):
+        cards = [rng.choice([0, 1, 7, 10**6, 10**12, 2**62]) for _ in range(rng.randint(1, 6))]
+        a, b = g.delta_bounds(cards), planner.delta_bounds(cards)
+        assert (a.lower, a.upper) == (b.lower, b.upper)
+    with pytest.raises(ValueError):
+        g.delta_bounds([])
+    ours, ref = g.TermDictionary(), rdict.TermDictionary()
+    terms = ["a", "b\\tc", "line\nbreak", "a", '"lit"@en', "back\\slash"]
+    assert [ours.encode_node(t) for t in terms] == [ref.encode_node(t) for t in terms]
+    assert ours.encode_predicate("p") == ref.encode_predicate("p")
+    (tmp_path / "o").mkdir()
+    (tmp_path / "r").mkdir()
+    ours.save(tmp_path / "o")
+    ref.save(tmp_path / "r")
+    for f in ("nodes.dict", "preds.dict"):
+        assert (tmp_path / "o" / f).read_bytes() == (tmp_path / "r" / f).read_bytes()
+    back = g.TermDictionary.load(tmp_path / "o")
+    assert back.node_terms == ref.node_terms
+    with pytest.raises(g.UnknownIdError):
+        back.decode_node(99)
+
+
+@pytest.mark.gpu
+def test_build_store_and_persist_match_reference(tmp_path):
+    """storage.build_store + persist on encoded triples (duplicates, sparse
+    predicate ids): the device build persists byte-identical stores."""
+    if not reference_available():
+        pytest.skip("reference package not installed")
+    from gsmat import dictionary as rdict
+    from gsmat import storage as rstorage
+
+    rng = random.Random(9)
+    ours_d, ref_d = g.TermDictionary(), rdict.TermDictionary()
+    triples = []
+    for _ in range(6000):
+        s, p, o = f"n{rng.randrange(700)}", f"p{rng.choice([1, 2, 3, 5, 8])}", f"n{rng.randrange(900)}"
+        t1 = (ours_d.encode_node(s), ours_d.encode_predicate(p), ours_d.encode_node(o))
+        t2 = (ref_d.encode_node(s), ref_d.encode_predicate(p), ref_d.encode_node(o))
+        assert t1 == t2
+        triples.append(g.EncodedTriple(*t1))
+    triples += triples[:500]  # duplicates
+    ours = g.build_store(ours_d, triples)
+    ref = rstorage.build_store(ref_d, [rstorage.EncodedTriple(*t) for t in triples])
+    assert ours.stats == {k: g.StatEntry(*v) for k, v in ref.stats.items()}
+    g.persist(ours, tmp_path / "o")
+    rstorage.persist(ref, tmp_path / "r")
+    _same_store(tmp_path / "o", tmp_path / "r")
+    # the built store answers queries like a loaded one
+    back = g.load(tmp_path / "o")
+    text = "SELECT * WHERE { ?x <p1> ?y . ?y <p2> ?z . }"
+    q1 = g.bind_constants(g.parse_query(text), ours.dictionary)
+    q2 = g.bind_constants(g.parse_query(text), back.dictionary)
+    a = g.execute(q1, g.make_plan(q1, ours.stats), ours).array
+    b = g.execute(q2, g.make_plan(q2, back.stats), back).array
+    assert len(a) > 0
+    from oracle import oracle as orc
+    assert orc.fingerprint_array(a) == orc.fingerprint_array(b)
