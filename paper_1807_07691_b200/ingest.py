@@ -39,6 +39,28 @@ def parse_ntriples(data: str | bytes, threads: int = 0) -> list[tuple[str, str, 
     return [tuple(terms[k:k + 3]) for k in range(0, len(terms), 3)]
 
 
+def parse_ntriples_line(line: str, lineno: int | None = None):
+    """qparser.parse_ntriples_line (qparser.py:80-104): the canonical triple
+    of one statement, None for a blank or comment line."""
+    text = ("\n" * ((lineno or 1) - 1)) + line.rstrip("\n") + "\n"
+    try:
+        got = parse_ntriples(text, threads=1)
+    except Exception as e:  # keep the reference's "line N" only when a number was given
+        from .errors import ParseError
+
+        if isinstance(e, ParseError) and lineno is None:
+            raise ParseError(str(e).split(": ", 1)[1] if ": " in str(e) else str(e)) from None
+        raise
+    return got[0] if got else None
+
+
+def read_ntriples(lines):
+    """qparser.read_ntriples (qparser.py:107-111) over an iterable of lines
+    (e.g. an open text file): all statements parsed in one call."""
+    text = "".join(line if line.endswith("\n") else line + "\n" for line in lines)
+    yield from parse_ntriples(text)
+
+
 def build(input_path: Path | str, out_dir: Path | str, device: int = 0,
           threads: int = 0) -> tuple[int, int, int]:
     """``gsmat build`` (cli._cmd_build): returns (triples, predicates, nodes),

@@ -87,6 +87,8 @@ def test_parse_files_and_line_numbers():
             ref = list(qparser.read_ntriples(fh))
         for threads in (1, 3, 8):
             assert g.parse_ntriples(data, threads=threads) == ref
+        if name == "tricky":
+            ref_tricky = ref
     # universal newlines: \r\n and lone \r end lines too
     assert g.parse_ntriples(b"<a> <p> <b> .\r\n<c> <p> <d> .\r<e> <p> <f> .") == [
         ("a", "p", "b"), ("c", "p", "d"), ("e", "p", "f")]
@@ -98,6 +100,14 @@ def test_parse_files_and_line_numbers():
         assert ei.value.line == 5
     with pytest.raises(g.ParseError, match=r"line 2: bad literal escape \\q"):
         g.parse_ntriples('<a> <p> "x" .\n<a> <p> "\\q" .\n')
+    # the reference's per-line and iterator entry points
+    from paper_1807_07691_b200.ingest import parse_ntriples_line, read_ntriples
+    with open(INGEST / "tricky.nt", encoding="utf-8") as fh:
+        assert list(read_ntriples(fh)) == ref_tricky
+    assert parse_ntriples_line("<a> <b> <c> .") == ("a", "b", "c")
+    assert parse_ntriples_line("# comment") is None
+    with pytest.raises(g.ParseError, match="line 3"):
+        parse_ntriples_line("<a> <b>", lineno=3)
 
 
 def _same_store(a, b):
