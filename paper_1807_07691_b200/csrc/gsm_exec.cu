@@ -4,12 +4,17 @@
 // cross_product / preallocate (/root/reference/pkg/src/gsmat/executor.py:94-368).
 //
 // One query = one stream-ordered launch sequence with no host round trip
-// between plan steps:
-//   resolve   constant-endpoint scans (R2/R3/R5) -> device table descriptors
-//   per step  J1 expand | J2/J3 filter | J0 cross | gate  (one kernel each)
-//   pack      projection into a row-major u32 result
+// between plan steps, captured once per plan as a CUDA graph and replayed:
+//   k_init    install the query block from its device image, take look-back
+//             epochs, resolve constant-endpoint scans (R2/R3/R5)
+//   per step  J1 expand | J2/J3 filter | fused [filter][expand][filter] group |
+//             J0 cross | gate  (one kernel each; hub pieces drained by k_drain)
+//   pack      projection into a row-major u32 result (or fused into the last
+//             join), written to pinned host memory when small (zero-copy)
 // followed by one sync that returns the per-step counters (the report and the
-// budget checks), then optional DISTINCT and the result hand-off.
+// budget checks), then optional DISTINCT and the result hand-off.  A batch of
+// independent queries (gsm_execute_batch) is captured as ONE graph forking
+// over the queries' contexts.
 //
 // Every join kernel is a single pass of "count -> scan -> scatter" (the
 // paper's Alg. 4 N/P pre-allocation, executor.py:197-215) fused into one
