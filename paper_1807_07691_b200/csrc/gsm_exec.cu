@@ -49,6 +49,7 @@ constexpr u64 LB_MASK = (1ull << 40) - 1;
 constexpr int WARP_ROW = 32;  // rows with >= this many candidates are written by a warp
 constexpr u32 EPOCH_MAX = (1u << 22) - 1;
 constexpr size_t ZC_BYTES = (size_t)16 << 10;  // results up to this size are written to host memory directly
+constexpr size_t ZC_PACK_BYTES = (size_t)1 << 20;  // ... when k_pack writes them (scan-only plans)
 
 struct TileSync {
   u64* status;            // one word per tile: epoch:22 | flag:2 | value:40
@@ -2391,8 +2392,13 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // Zero-copy results: when this plan's last result was small, the last
   // kernel writes the step counters and the projected rows straight into the
   // pinned staging buffer (no device->host copy in the launch sequence).
-  S.zc = c->guess <= ZC_BYTES;
-  const size_t stage_lim = S.zc ? std::min<size_t>(c->stage_bytes, ZC_BYTES) : c->stage_bytes;
+  // Results packed by k_pack (plans ending in a scan) are written row after
+  // row with coalesced stores, so they stay zero-copy up to ZC_PACK_BYTES;
+  // the joins' fused projections scatter, so their limit is ZC_BYTES.
+  const bool packs = launches.empty() && !distinct && n_proj >= 1 && n_proj <= 2;
+  const size_t zc_lim = packs ? ZC_PACK_BYTES : ZC_BYTES;
+  S.zc = c->guess <= zc_lim;
+  const size_t stage_lim = S.zc ? std::min<size_t>(c->stage_bytes, zc_lim) : c->stage_bytes;
   const i64 stage_cap = n_proj ? (i64)(stage_lim / (4 * (size_t)n_proj)) : ((i64)1 << 62);
   u32* const stage_rows = S.zc ? c->hd_rows : c->d_rows;
   // Fuse the projection into the last join when it is an expand/filter and
