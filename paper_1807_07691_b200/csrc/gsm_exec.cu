@@ -2395,7 +2395,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // Results packed by k_pack (plans ending in a scan) are written row after
   // row with coalesced stores, so they stay zero-copy up to ZC_PACK_BYTES;
   // the joins' fused projections scatter, so their limit is ZC_BYTES.
-  const bool packs = launches.empty() && !distinct && n_proj >= 1 && n_proj <= 2;
+  const bool packs = launches.empty() && !distinct && qa.seed_k < 0 && n_proj >= 1 && n_proj <= 2;
   const size_t zc_lim = packs ? ZC_PACK_BYTES : ZC_BYTES;
   S.zc = c->guess <= zc_lim;
   const size_t stage_lim = S.zc ? std::min<size_t>(c->stage_bytes, zc_lim) : c->stage_bytes;
