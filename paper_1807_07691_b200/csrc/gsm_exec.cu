@@ -1653,6 +1653,9 @@ struct gsm_context {
   bool use_proj_fusion = true;  // write the projected result from the last join
   bool use_batch_graph = true;  // a repeated batch replays as one graph (gsm_execute_batch)
   int tile_items = 0;           // expand tile rows per thread: 0 = by size, 1 or 2 (GSM_TILE_ITEMS)
+  // post filters also fuse into an expand whose output bound is at least
+  // this many rows, whatever its fan-out (GSM_FUSE_HUGE)
+  i64 fuse_huge = (i64)1 << 28;
   size_t stage_max = (size_t)1 << 30;  // the staging buffer grows up to this (GSM_STAGE_MAX)
   // A prepared plan: the captured launch sequence plus what the host needs
   // to replay and complete it without re-planning.
@@ -1902,6 +1905,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* nd = getenv("GSM_NO_DEFER")) c->use_defer = !(nd[0] == '1');
   if (const char* npf = getenv("GSM_NO_PROJ_FUSION")) c->use_proj_fusion = !(npf[0] == '1');
   if (const char* nb = getenv("GSM_NO_BATCH_GRAPH")) c->use_batch_graph = !(nb[0] == '1');
+  if (const char* fh = getenv("GSM_FUSE_HUGE")) c->fuse_huge = std::max<i64>(1, atoll(fh));
   if (const char* ti = getenv("GSM_TILE_ITEMS")) c->tile_items = std::min(2, std::max(0, atoi(ti)));
   if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
   auto fail = [&](gsm_status st) {
@@ -2191,7 +2195,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       bool join = false;
       if (c->use_fusion && g_open) {
         if (is_expand) join = !g_has_x;
-        else if (g_has_x) join = g_npost < MAXF && g_x_fanout <= FUSE_MAX_FANOUT;
+        else if (g_has_x)  // short runs, or an intermediate too large to materialise well
+          join = g_npost < MAXF && (g_x_fanout <= FUSE_MAX_FANOUT || ex.ub[cur] >= c->fuse_huge);
         else join = g_npre < MAXF;
       }
       if (!join) {

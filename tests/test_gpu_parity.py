@@ -267,7 +267,7 @@ def test_execution_variants_agree(store_factory):
     # result, no k_pack) and DISTINCT / sizes above the zero-copy limit take
     # the device paths
     for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION", "GSM_NO_DEFER",
-                    "GSM_NO_PROJ_FUSION", "GSM_NO_BATCH_GRAPH", "GSM_STAGE_MAX=65536", "GSM_TILE_ITEMS=2",
+                    "GSM_NO_PROJ_FUSION", "GSM_NO_BATCH_GRAPH", "GSM_STAGE_MAX=65536", "GSM_TILE_ITEMS=2", "GSM_FUSE_HUGE=1",
                     "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER,GSM_NO_PROJ_FUSION"):
         env = dict(os.environ)
         for item in filter(None, variant.split(",")):
