@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--skip-oracle-above", type=int, default=400_000_000,
                     help="skip the oracle when a step materialises more rows (host RAM guard)")
     ap.add_argument("--store", default=None, help="reuse an existing store directory")
+    ap.add_argument("--only", default=None, help="comma-separated query names to run")
     args = ap.parse_args()
 
     import numpy as np
@@ -89,6 +90,9 @@ def main():
     else:
         qfiles = sorted((REPO / f"datagen/queries/{args.kind}").glob("*.rq"))
     summary = {"gpu_ms": 0.0, "cpu_s": 0.0, "join_rows": 0, "parity_ok": 0, "parity_checked": 0}
+    if args.only:
+        keep = set(args.only.split(","))
+        qfiles = [f for f in qfiles if f.stem in keep]
     for qf in qfiles:
         q = g.bind_constants(g.parse_query(qf.read_text()), store.dictionary)
         plan = g.make_plan(q, store.stats)
