@@ -1653,9 +1653,11 @@ struct gsm_context {
   bool use_proj_fusion = true;  // write the projected result from the last join
   bool use_batch_graph = true;  // a repeated batch replays as one graph (gsm_execute_batch)
   int tile_items = 0;           // expand tile rows per thread: 0 = by size, 1 or 2 (GSM_TILE_ITEMS)
-  // post filters also fuse into an expand whose output bound is at least
-  // this many rows, whatever its fan-out (GSM_FUSE_HUGE)
-  i64 fuse_huge = (i64)1 << 28;
+  // post filters also fuse into an expand expected to output at least this
+  // many rows (left rows x average run), whatever its fan-out, unless its
+  // runs are skewed (longest > 64 x average: hub rows would serialise in the
+  // fused kernel) (GSM_FUSE_HUGE)
+  i64 fuse_huge = (i64)1 << 25;
   size_t stage_max = (size_t)1 << 30;  // the staging buffer grows up to this (GSM_STAGE_MAX)
   // A prepared plan: the captured launch sequence plus what the host needs
   // to replay and complete it without re-planning.
@@ -2145,6 +2147,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   bool g_open = false, g_has_x = false;
   int g_npre = 0, g_npost = 0;
   u32 g_x_fanout = 0;  // longest candidate list of the group's expand
+  i64 g_x_avg = 0, g_x_est = 0;  // its average run, expected output rows
   Home g_in_home = H_NONE;
   std::vector<int> group_id(n, -1);
   int n_groups = 0;
@@ -2196,7 +2199,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       if (c->use_fusion && g_open) {
         if (is_expand) join = !g_has_x;
         else if (g_has_x)  // short runs, or an intermediate too large to materialise well
-          join = g_npost < MAXF && (g_x_fanout <= FUSE_MAX_FANOUT || ex.ub[cur] >= c->fuse_huge);
+          join = g_npost < MAXF && (g_x_fanout <= FUSE_MAX_FANOUT ||
+                                    (g_x_est >= c->fuse_huge && g_x_fanout <= 64 * std::max<i64>(1, g_x_avg)));
         else join = g_npre < MAXF;
       }
       if (!join) {
@@ -2209,7 +2213,11 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       if (is_expand) {
         g_has_x = true;
         const bool on_s = jv[0] == p.s_var;
-        g_x_fanout = (on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid]).max_run;
+        const HostAux& gha = on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid];
+        g_x_fanout = gha.max_run;
+        // expected expand output: left rows x the orientation's average run
+        g_x_avg = gha.key.empty() ? 0 : (i64)(gha.off.back() / gha.key.size());
+        g_x_est = Exec::sat_mul(ex.ub[cur], std::max<i64>(1, g_x_avg));
       } else if (g_has_x) g_npost++;
       else g_npre++;
       group_id[s] = n_groups - 1;
