@@ -376,7 +376,7 @@ def run_ours(args):
             except Exception:
                 probe["expand_kernel_columnar"] = {"error": out.stderr[-400:]}
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 measurement
             cpu = cpu_baseline_port(store, queries, args.cpu_seconds)
 
         value = rows_all / dev_s if dev_s > 0 else 0.0
