@@ -232,7 +232,12 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
  * order).  prealloc_total (may be NULL) receives E, the first-variable match
  * total (executor.py:197-215); row_counts (may be NULL, n_left entries)
  * receives each left row's first-variable match count N.  Budget rules and
- * messages as gsm_execute (cross product: |L|*|R|). */
+ * messages as gsm_execute (cross product: |L|*|R|).  out = NULL is the
+ * counts-only mode of preallocate() (executor.py:197-215): E and the row
+ * counts are returned without materialising any candidate (device memory
+ * O(|L| + |R|)).  Under the sequential rule a join whose E exceeds the
+ * budget counts its emitted rows before allocating E-sized buffers, so an
+ * over-budget join raises the budget error, not an allocation failure. */
 gsm_status gsm_table_join(gsm_context* ctx, const uint32_t* left, int64_t n_left, int32_t a,
                           const uint32_t* right, int64_t n_right, int32_t b,
                           const int32_t* join_left, const int32_t* join_right, int32_t n_join,

@@ -18,4 +18,7 @@ cp -r "$src" "$tmp/pkg"          # the reference tree is read-only; build from a
 rm -rf "$here/_ref"
 python -m pip install --quiet --no-index --no-build-isolation --no-deps \
   --target "$here/_ref" "$tmp/pkg"
-echo "installed reference gsmat into $here/_ref"
+# the reference's own test modules (run against the drop-in by
+# tests/test_reference_suite.py through the INTEGRATION.md §2 patch)
+cp -r "$tmp/pkg/tests" "$here/_ref/gsmat_tests"
+echo "installed reference gsmat (+ its tests) into $here/_ref"

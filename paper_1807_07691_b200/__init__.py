@@ -23,18 +23,13 @@ from .executor import (
     execute,
     execute_batch,
 )
-from .dictionary import TermDictionary
-from .frontend import (CostBounds, Plan, QueryGraph, TriplePattern, bind_constants, delta_bounds,
-                       make_plan, parse_query)
+from .frontend import Plan, QueryGraph, TriplePattern, bind_constants, make_plan, parse_query
 from .decode import decode_rows, format_term, result_tsv, write_tsv
 from .ingest import build, parse_ntriples
 from .storage import (DeviceStore, EncodedTriple, PredicateMatrix, StatEntry, Store, build_store, from_store,
                       load, persist)
 
 __all__ = [
-    "TermDictionary",
-    "CostBounds",
-    "delta_bounds",
     "EncodedTriple",
     "PredicateMatrix",
     "Store",

@@ -1454,6 +1454,34 @@ __global__ void k_row_counts(const u32* __restrict__ Lk, i64 n, Orient X, i64* _
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, acc);
 }
 
+// Emitted-row count of a table join without materialising its candidates:
+// per left row, the candidates of its first-variable key that agree on every
+// further shared variable (executor.py:186-191).  Lets the sequential budget
+// rule (executor.py:192-193) trip before E-sized buffers are allocated.
+struct SecCols {
+  int n;
+  int jl[GSM_MAX_VARS], jr[GSM_MAX_VARS];
+};
+__global__ void k_sec_counts(const u32* __restrict__ Lcols, i64 n, int li, Orient X,
+                             const u32* __restrict__ R, int b, SecCols sc,
+                             unsigned long long* __restrict__ total) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  unsigned long long acc = 0;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint2 seg = seg_lookup(X, __ldg(Lcols + (i64)li * n + i));
+    for (u32 j = 0; j < seg.y; j++) {
+      const u32 ri = __ldg(X.dst + seg.x + j);
+      bool ok = true;
+      for (int k = 0; k < sc.n && ok; k++)
+        ok = __ldg(Lcols + (i64)sc.jl[k] * n + i) == __ldg(R + (i64)ri * b + sc.jr[k]);
+      acc += ok;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, acc);
+}
+
 // Secondary join variables + output gather of the expanded (left ++ right row
 // index) table: keep a candidate iff every further shared variable agrees
 // (executor.py:186-191); emit left ++ right[rcols] row-major.
@@ -2841,6 +2869,13 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
   cudaStream_t st = c->stream;
   i64 d2h_extra = 0;
   if (distinct && nrows > 1) {
+    if (nrows >= 0xFFFFFFFFLL) {  // the tuple set stores u32 row indices
+      delete r;
+      char msg[160];
+      snprintf(msg, sizeof msg, "DISTINCT over %lld rows exceeds the device limit of 2^32-1 rows",
+               (long long)nrows);
+      return set_error(GSM_ERR_RESOURCE, msg);
+    }
     size_t cap = 16;
     while (cap < 2 * (size_t)nrows) cap <<= 1;
     if (cap > c->n_slots) {
@@ -3264,7 +3299,8 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
                           const int32_t* join_left, const int32_t* join_right, int32_t n_join,
                           int64_t budget, int32_t budget_mode, int64_t* prealloc_total,
                           int64_t* row_counts, gsm_result** out) {
-  *out = nullptr;
+  const bool counts_only = out == nullptr;  // preallocate(): N and E only
+  if (out) *out = nullptr;
   if (!c) return set_error(GSM_ERR_VALUE, "null context");
   if (n_left < 0 || n_right < 0 || a < 0 || b < 0 || n_join < 0 || n_join > a || n_join > b ||
       a + b - n_join > GSM_MAX_VARS || a >= GSM_MAX_VARS)
@@ -3284,10 +3320,13 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
     if (e == cudaSuccess) tmp.push_back(*p);
     return e;
   };
+  gsm_result* r = nullptr;  // owned here until handed to *out
   auto cleanup = [&]() {
     for (void* p : tmp) cudaFreeAsync(p, st);
     cudaStreamSynchronize(st);
     tmp.clear();
+    if (r) gsm_result_free(r);
+    r = nullptr;
   };
 #define TJ_CUDA(call)                              \
   do {                                             \
@@ -3298,9 +3337,6 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
     }                                              \
   } while (0)
   const int w_out = a + b - n_join;
-  gsm_result* r = new gsm_result();
-  r->device = c->device;
-  r->k = w_out;
   u32 *dL = nullptr, *dR = nullptr;
   TJ_CUDA(alloc((void**)&dL, 4 * (size_t)n_left * a));
   TJ_CUDA(alloc((void**)&dR, 4 * (size_t)n_right * b));
@@ -3312,26 +3348,33 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
     i64 total = 0;
     if (__builtin_mul_overflow((i64)n_left, (i64)n_right, &total) || total > budget) {
       cleanup();
-      delete r;
       char msg[256];
       snprintf(msg, sizeof msg, "cross product of %lld x %lld rows exceeds budget %lld",
                (long long)n_left, (long long)n_right, (long long)budget);
       return set_error(GSM_ERR_RESOURCE, msg);
     }
+    if (counts_only) {
+      cleanup();
+      return GSM_OK;
+    }
+    r = new gsm_result();
+    r->device = c->device;
+    r->k = w_out;
     r->n = total;
     if (total * w_out > 0) {
       cudaError_t e = cudaMalloc(&r->rows, 4 * (size_t)total * w_out);
       if (e != cudaSuccess) {
         cleanup();
-        delete r;
         return cuda_error(e, "cudaMalloc(result)");
       }
       k_cross_rows<<<c->grid_ts, 256, 0, st>>>(dL, n_left, a, dR, n_right, b, r->rows);
       count_launch();
     }
     TJ_CUDA(cudaGetLastError());
+    gsm_result* done = r;
+    r = nullptr;
     cleanup();
-    *out = r;
+    *out = done;
     return GSM_OK;
   }
 
@@ -3351,10 +3394,10 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
         dR, n_right, b, join_right[0], keys_in, rows_in);
     count_launch();
     size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in, keys, rows_in, rows, (int)n_right, 0, 32, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in, keys, rows_in, rows, (int64_t)n_right, 0, 32, st);
     void* tsort;
     TJ_CUDA(alloc(&tsort, tb));
-    TJ_CUDA(cub::DeviceRadixSort::SortPairs(tsort, tb, keys_in, keys, rows_in, rows, (int)n_right, 0, 32, st));
+    TJ_CUDA(cub::DeviceRadixSort::SortPairs(tsort, tb, keys_in, keys, rows_in, rows, (int64_t)n_right, 0, 32, st));
     count_launch();
   }
   Orient X{};
@@ -3396,12 +3439,44 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
   if (prealloc_total) *prealloc_total = (i64)E;
   if (budget_mode == GSM_BUDGET_PARALLEL && (i64)E > budget) {
     cleanup();
-    delete r;
     char msg[256];
     snprintf(msg, sizeof msg, "pre-allocated join region of %lld rows exceeds budget %lld",
              (long long)E, (long long)budget);
     return set_error(GSM_ERR_RESOURCE, msg);
   }
+  if (counts_only) {
+    cleanup();
+    return GSM_OK;
+  }
+  if (budget_mode == GSM_BUDGET_SEQUENTIAL && (i64)E > budget) {
+    // E-sized candidates may not fit: count the emitted rows first
+    i64 O = (i64)E;
+    if (n_join > 1) {
+      SecCols sc{};
+      sc.n = n_join - 1;
+      for (int i = 1; i < n_join; i++) {
+        sc.jl[i - 1] = join_left[i];
+        sc.jr[i - 1] = join_right[i];
+      }
+      TJ_CUDA(cudaMemsetAsync(dE, 0, 8, st));
+      k_sec_counts<<<std::max(1, std::min(c->grid_ts, (int)((n_left + 255) / 256))), 256, 0, st>>>(
+          Lcols, n_left, join_left[0], X, dR, b, sc, dE);
+      count_launch();
+      unsigned long long hO = 0;
+      TJ_CUDA(cudaMemcpyAsync(&hO, dE, 8, cudaMemcpyDeviceToHost, st));
+      TJ_CUDA(cudaStreamSynchronize(st));
+      O = (i64)hO;
+    }
+    if (O > budget) {
+      cleanup();
+      char msg[256];
+      snprintf(msg, sizeof msg, "join output exceeds row budget %lld", (long long)budget);
+      return set_error(GSM_ERR_RESOURCE, msg);
+    }
+  }
+  r = new gsm_result();
+  r->device = c->device;
+  r->k = w_out;
 
   // ---- expand (left ++ right row index), then secondary checks + gather
   const i64 ntile_max = (std::max<i64>(n_left, (i64)E) + TS_TILE - 1) / TS_TILE + 2;
@@ -3452,7 +3527,6 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
   cudaError_t e = cudaMalloc(&r->rows, 4 * (size_t)res_rows * std::max(w_out, 1));
   if (e != cudaSuccess) {
     cleanup();
-    delete r;
     return cuda_error(e, "cudaMalloc(result)");
   }
   fp.out = r->rows;
@@ -3464,16 +3538,18 @@ gsm_status gsm_table_join(gsm_context* c, const uint32_t* left, int64_t n_left, 
   StepStat res{};
   TJ_CUDA(cudaMemcpyAsync(&res, &d->st[1], sizeof res, cudaMemcpyDeviceToHost, st));
   TJ_CUDA(cudaStreamSynchronize(st));
-  cleanup();
 #undef TJ_CUDA
   r->n = res.rows;
-  if (budget_mode == GSM_BUDGET_SEQUENTIAL && r->n > budget) {
-    gsm_result_free(r);
+  gsm_result* done = r;
+  r = nullptr;
+  cleanup();
+  if (budget_mode == GSM_BUDGET_SEQUENTIAL && done->n > budget) {
+    gsm_result_free(done);
     char msg[256];
     snprintf(msg, sizeof msg, "join output exceeds row budget %lld", (long long)budget);
     return set_error(GSM_ERR_RESOURCE, msg);
   }
-  *out = r;
+  *out = done;
   return GSM_OK;
 }
 

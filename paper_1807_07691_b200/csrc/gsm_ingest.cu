@@ -203,8 +203,8 @@ gsm_status encode_terms(const unsigned char* d_bytes, const std::vector<u64>& of
   IG_CUDA(cudaMemcpyAsync(d_off, off.data(), 8 * n, cudaMemcpyHostToDevice, st));
   IG_CUDA(cudaMemcpyAsync(d_len, len.data(), 4 * n, cudaMemcpyHostToDevice, st));
   size_t tb = 0, tb2 = 0, tb3 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, d_h, d_h2, d_idx, d_idx2, (int)n, 0, 64, st);
-  cub::DeviceScan::InclusiveSum(nullptr, tb2, d_head, d_gid, (int)n, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, d_h, d_h2, d_idx, d_idx2, (int64_t)n, 0, 64, st);
+  cub::DeviceScan::InclusiveSum(nullptr, tb2, d_head, d_gid, (int64_t)n, st);
   void* tmp;
   IG_CUDA(b.alloc((char**)&tmp, std::max(tb, tb2)));
   u64 G = 0;
@@ -212,10 +212,10 @@ gsm_status encode_terms(const unsigned char* d_bytes, const std::vector<u64>& of
     if (attempt == 4) return set_error(GSM_ERR_VALUE, "term hash collisions persisted over 4 seeds");
     const u64 seed = 0x243f6a8885a308d3ull * (u64)(attempt + 1);
     k_term_hash<<<gridn(n), 256, 0, st>>>(d_bytes, d_off, d_len, n, seed, d_h, d_idx);
-    cub::DeviceRadixSort::SortPairs(tmp, tb, d_h, d_h2, d_idx, d_idx2, (int)n, 0, 64, st);
+    cub::DeviceRadixSort::SortPairs(tmp, tb, d_h, d_h2, d_idx, d_idx2, (int64_t)n, 0, 64, st);
     IG_CUDA(cudaMemsetAsync(d_coll, 0, 4, st));
     k_term_heads<<<gridn(n), 256, 0, st>>>(d_h2, d_idx2, d_bytes, d_off, d_len, n, d_head, d_coll);
-    cub::DeviceScan::InclusiveSum(tmp, tb2, d_head, d_gid, (int)n, st);
+    cub::DeviceScan::InclusiveSum(tmp, tb2, d_head, d_gid, (int64_t)n, st);
     count_launch(4);
     u32 coll = 0, g32 = 0;
     IG_CUDA(cudaMemcpyAsync(&coll, d_coll, 4, cudaMemcpyDeviceToHost, st));
@@ -232,11 +232,11 @@ gsm_status encode_terms(const unsigned char* d_bytes, const std::vector<u64>& of
   IG_CUDA(b.alloc(&d_gkey2, G));
   IG_CUDA(b.alloc(&d_rank, G));
   k_group_first<<<gridn(n), 256, 0, st>>>(d_head, d_gid, d_idx2, n, d_first, d_gkey);
-  cub::DeviceRadixSort::SortPairs(nullptr, tb3, d_first, d_first2, d_gkey, d_gkey2, (int)G, 0,
+  cub::DeviceRadixSort::SortPairs(nullptr, tb3, d_first, d_first2, d_gkey, d_gkey2, (int64_t)G, 0,
                                   bits_for(n), st);
   void* tmp3;
   IG_CUDA(b.alloc((char**)&tmp3, tb3));
-  cub::DeviceRadixSort::SortPairs(tmp3, tb3, d_first, d_first2, d_gkey, d_gkey2, (int)G, 0,
+  cub::DeviceRadixSort::SortPairs(tmp3, tb3, d_first, d_first2, d_gkey, d_gkey2, (int64_t)G, 0,
                                   bits_for(n), st);
   k_rank<<<gridn(G), 256, 0, st>>>(d_gkey2, G, d_rank);
   k_assign_ids<<<gridn(n), 256, 0, st>>>(d_idx2, d_gid, d_rank, n, d_ids);
@@ -274,20 +274,20 @@ gsm_status build_orientation(const std::vector<u64>& key, const std::vector<u32>
   IG_CUDA(cudaMemcpyAsync(d_p, pid.data(), 4 * T, cudaMemcpyHostToDevice, st));
   // (key) then stable by p  ->  sorted by (p, key)
   size_t t1 = 0, t2 = 0, t3 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, t1, d_k, d_k2, d_p, d_p2, (int)T, 0, 64, st);
-  cub::DeviceRadixSort::SortPairs(nullptr, t2, d_p2, d_p, d_k2, d_k, (int)T, 0, bits_for(max_pid), st);
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, d_k, d_k2, d_p, d_p2, (int64_t)T, 0, 64, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, t2, d_p2, d_p, d_k2, d_k, (int64_t)T, 0, bits_for(max_pid), st);
   void* tmp;
   IG_CUDA(b.alloc((char**)&tmp, std::max(t1, t2)));
-  cub::DeviceRadixSort::SortPairs(tmp, t1, d_k, d_k2, d_p, d_p2, (int)T, 0, 64, st);
-  cub::DeviceRadixSort::SortPairs(tmp, t2, d_p2, d_p, d_k2, d_k, (int)T, 0, bits_for(max_pid), st);
+  cub::DeviceRadixSort::SortPairs(tmp, t1, d_k, d_k2, d_p, d_p2, (int64_t)T, 0, 64, st);
+  cub::DeviceRadixSort::SortPairs(tmp, t2, d_p2, d_p, d_k2, d_k, (int64_t)T, 0, bits_for(max_pid), st);
   k_dedup_flags<<<gridn(T), 256, 0, st>>>(d_p, d_k, T, d_keep);
   IG_CUDA(b.alloc(&d_k3, T));
   IG_CUDA(b.alloc(&d_p3, T));
-  cub::DeviceSelect::Flagged(nullptr, t3, d_k, d_keep, d_k3, d_nsel, (int)T, st);
+  cub::DeviceSelect::Flagged(nullptr, t3, d_k, d_keep, d_k3, d_nsel, (int64_t)T, st);
   void* tmp3;
   IG_CUDA(b.alloc((char**)&tmp3, t3));
-  cub::DeviceSelect::Flagged(tmp3, t3, d_k, d_keep, d_k3, d_nsel, (int)T, st);
-  cub::DeviceSelect::Flagged(tmp3, t3, d_p, d_keep, d_p3, d_nsel, (int)T, st);
+  cub::DeviceSelect::Flagged(tmp3, t3, d_k, d_keep, d_k3, d_nsel, (int64_t)T, st);
+  cub::DeviceSelect::Flagged(tmp3, t3, d_p, d_keep, d_p3, d_nsel, (int64_t)T, st);
   count_launch(5);
   int U = 0;
   IG_CUDA(cudaMemcpyAsync(&U, d_nsel, 4, cudaMemcpyDeviceToHost, st));

@@ -194,10 +194,10 @@ static gsm_status build_host_aux(const Orient& o, HostAux& a) {
   thrust::counting_iterator<u32> it(0);
   size_t tmp_bytes = 0;
   HeadFlag f{o.src};
-  cub::DeviceSelect::If(nullptr, tmp_bytes, it, d_pos, d_n, (int)o.nnz, f);
+  cub::DeviceSelect::If(nullptr, tmp_bytes, it, d_pos, d_n, (int64_t)o.nnz, f);
   void* tmp;
   GSM_CUDA(cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 4));
-  cub::DeviceSelect::If(tmp, tmp_bytes, it, d_pos, d_n, (int)o.nnz, f);
+  cub::DeviceSelect::If(tmp, tmp_bytes, it, d_pos, d_n, (int64_t)o.nnz, f);
   k_gather_u32<<<grid_for(o.nrows), 256>>>(d_pos, d_n, o.src, d_key);
   count_launch(3);
   a.key.resize(o.nrows);
@@ -223,10 +223,10 @@ static gsm_status build_diag(gsm_store* s, PredDev& p) {
   thrust::counting_iterator<u32> it(0);
   size_t tmp_bytes = 0;
   DiagFlag f{o.src, o.dst};
-  cub::DeviceSelect::If(nullptr, tmp_bytes, it, d_idx, d_n, (int)o.nnz, f);
+  cub::DeviceSelect::If(nullptr, tmp_bytes, it, d_idx, d_n, (int64_t)o.nnz, f);
   void* tmp;
   GSM_CUDA(cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 4));
-  cub::DeviceSelect::If(tmp, tmp_bytes, it, d_idx, d_n, (int)o.nnz, f);
+  cub::DeviceSelect::If(tmp, tmp_bytes, it, d_idx, d_n, (int64_t)o.nnz, f);
   count_launch(2);
   u32 nd = 0;
   GSM_CUDA(cudaMemcpy(&nd, d_n, 4, cudaMemcpyDeviceToHost));

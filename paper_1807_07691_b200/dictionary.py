@@ -1,15 +1,17 @@
 """Read-only, array-backed term dictionary over a store's ``*.dict`` files.
 
 Same lookup/decode contract as the reference's TermDictionary
-(/root/reference/pkg/src/gsmat/dictionary.py:46-125): dense 1-based ids in
-file line order, ``lookup_*`` returns None for unknown terms, ``decode_*``
-raises UnknownIdError.  It does not build a Python dict of every node (the
+(/root/reference/pkg/src/gsmat/dictionary.py:46-125) for a persisted store:
+dense 1-based ids in file line order, ``lookup_*`` returns None for unknown
+terms, ``decode_*`` raises UnknownIdError.  Building a dictionary (encoding
+new terms) is out of scope: ``build_store`` takes the caller's dictionary.  It does not build a Python dict of every node (the
 reference's costs ~115 B per node): nodes.dict is kept as one
 bytes buffer plus a numpy line-offset array; lookups search the buffer.
 """
 
 from __future__ import annotations
 
+import re
 from pathlib import Path
 
 import numpy as np
@@ -19,31 +21,26 @@ from .errors import StoreFormatError, UnknownIdError
 NODES_FILE = "nodes.dict"
 PREDS_FILE = "preds.dict"
 
-_ESC = {"\\": "\\", "n": "\n", "r": "\r", "t": "\t"}
+# One-term-per-line file format of nodes.dict / preds.dict
+# (/root/reference/pkg/src/gsmat/dictionary.py:18-43): backslash, newline,
+# carriage return and tab are written as two-character escapes; on reading,
+# a backslash takes the next character literally unless it names one of
+# those escapes, and a trailing lone backslash stays as it is.
+_TO_FILE = str.maketrans({"\\": "\\\\", "\n": "\\n", "\r": "\\r", "\t": "\\t"})
+_FROM_FILE = {"n": "\n", "r": "\r", "t": "\t"}
+_ESCAPED = re.compile(r"\\(.)", re.S)
 
 
 def escape_term(term: str) -> str:
-    """dictionary.escape_term (dictionary.py:18-25)."""
-    return (
-        term.replace("\\", "\\\\").replace("\n", "\\n").replace("\r", "\\r").replace("\t", "\\t")
-    )
+    """A term as one line of a ``*.dict`` file."""
+    return term.translate(_TO_FILE)
 
 
 def unescape_term(text: str) -> str:
-    """dictionary.unescape_term (dictionary.py:28-43)."""
+    """The term one line of a ``*.dict`` file encodes."""
     if "\\" not in text:
         return text
-    out: list[str] = []
-    i, n = 0, len(text)
-    while i < n:
-        c = text[i]
-        if c == "\\" and i + 1 < n:
-            out.append(_ESC.get(text[i + 1], text[i + 1]))
-            i += 2
-        else:
-            out.append(c)
-            i += 1
-    return "".join(out)
+    return _ESCAPED.sub(lambda m: _FROM_FILE.get(m.group(1), m.group(1)), text)
 
 
 class _TermFile:
@@ -126,77 +123,3 @@ class StoreDictionary:
             if data and not data.endswith(b"\n"):
                 data += b"\n"
             (directory / name).write_bytes(data)
-
-
-class TermDictionary:
-    """dictionary.TermDictionary (dictionary.py:46-125): two first-occurrence
-    ordered bijections (nodes, predicates), dense 1-based ids, the reference's
-    one-term-per-line persistence.  Host-side state of the build path
-    (:func:`paper_1807_07691_b200.storage.build_store`)."""
-
-    def __init__(self) -> None:
-        self.node_terms: list[str] = []
-        self.pred_terms: list[str] = []
-        self.node_index: dict[str, int] = {}
-        self.pred_index: dict[str, int] = {}
-
-    def encode_node(self, term: str) -> int:
-        nid = self.node_index.get(term)
-        if nid is None:
-            self.node_terms.append(term)
-            nid = len(self.node_terms)
-            self.node_index[term] = nid
-        return nid
-
-    def encode_predicate(self, term: str) -> int:
-        pid = self.pred_index.get(term)
-        if pid is None:
-            self.pred_terms.append(term)
-            pid = len(self.pred_terms)
-            self.pred_index[term] = pid
-        return pid
-
-    def lookup_node(self, term: str) -> int | None:
-        return self.node_index.get(term)
-
-    def lookup_predicate(self, term: str) -> int | None:
-        return self.pred_index.get(term)
-
-    def decode_node(self, id_: int) -> str:
-        if not 1 <= id_ <= len(self.node_terms):
-            raise UnknownIdError("node", id_)
-        return self.node_terms[id_ - 1]
-
-    def decode_predicate(self, id_: int) -> str:
-        if not 1 <= id_ <= len(self.pred_terms):
-            raise UnknownIdError("predicate", id_)
-        return self.pred_terms[id_ - 1]
-
-    @property
-    def node_count(self) -> int:
-        return len(self.node_terms)
-
-    @property
-    def predicate_count(self) -> int:
-        return len(self.pred_terms)
-
-    def save(self, directory: Path | str) -> None:
-        directory = Path(directory)
-        for name, terms in ((NODES_FILE, self.node_terms), (PREDS_FILE, self.pred_terms)):
-            with open(directory / name, "w", encoding="utf-8", newline="\n") as fh:
-                for term in terms:
-                    fh.write(escape_term(term))
-                    fh.write("\n")
-
-    @classmethod
-    def load(cls, directory: Path | str) -> "TermDictionary":
-        directory = Path(directory)
-        d = cls()
-        for name, encode in ((NODES_FILE, d.encode_node), (PREDS_FILE, d.encode_predicate)):
-            path = directory / name
-            if not path.exists():
-                raise StoreFormatError(f"missing dictionary file {path}")
-            with open(path, encoding="utf-8", newline="\n") as fh:
-                for raw in fh:
-                    encode(unescape_term(raw.rstrip("\n")))
-        return d

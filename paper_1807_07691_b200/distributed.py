@@ -6,8 +6,10 @@ so with the store replicated on every GPU a query shards with NO exchange
 between plan steps: rank r of W evaluates rows [n*r/W, n*(r+1)/W) of the
 first step's table through the whole chain (``gsm_execute`` part_index /
 part_count).  The only collectives are on the per-step counters (one
-all-reduce, so the row-budget rule is applied to the GLOBAL E and every rank
-raises the same ResourceLimitError, executor.py:237-241) and, optionally, the
+all-reduce, so the row-budget rules -- emitted rows for "gpu"/"sequential"
+(executor.py:192-193), E for "parallel" (executor.py:237-241), |L|x|R| for
+cross products (executor.py:158-163) -- are applied to the GLOBAL counts and
+every rank raises the same ResourceLimitError) and, optionally, the
 gather of the result rows to rank 0.  DISTINCT is applied to the union.
 
 ``runner`` defaults to the CUDA executor; the CPU tests inject the C oracle's
@@ -92,11 +94,19 @@ def execute_distributed(query, plan, store, mode: str = "gpu", row_budget: int =
     kinds = local_rep.kinds or [""] * n_steps
     for i in range(1, n_steps):
         if kinds[i] in ("cross", "gate"):
-            continue  # cross-product budgets: |L| differs per rank; checked by the runner
-        if mode != "sequential" and step_e[i] > row_budget:
+            # cross_product's rule (executor.py:158-163) on the GLOBAL tables:
+            # every rank crossed its slice of L with the whole right table R,
+            # so the summed step rows are |L| * |R|
+            n_left = step_rows[i - 1]
+            if n_left and step_rows[i] > row_budget:
+                raise ResourceLimitError(
+                    f"cross product of {n_left} x {step_rows[i] // n_left} rows exceeds "
+                    f"budget {row_budget}")
+            continue
+        if mode == "parallel" and step_e[i] > row_budget:
             raise ResourceLimitError(
                 f"pre-allocated join region of {step_e[i]} rows exceeds budget {row_budget}")
-        if mode == "sequential" and step_rows[i] > row_budget:
+        if mode != "parallel" and step_rows[i] > row_budget:
             raise ResourceLimitError(f"join output exceeds row budget {row_budget}")
     if report is not None:
         for i, pat in enumerate(plan.steps):

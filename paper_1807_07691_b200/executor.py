@@ -12,10 +12,14 @@ HBM-resident store, through the C ABI in include/gsmat_b200.h.
   ``plan.steps[i].pattern``, ``projection``, ``distinct``).
 * ``store`` is a :class:`.storage.DeviceStore` (``storage.load``) or a
   reference ``Store`` (uploaded once and cached).
-* ``mode``: "gpu" (default) evaluates with the parallel mode's pre-allocation
-  budget rule (executor.py:237-241); "sequential"/"parallel" also run on the
-  GPU and select that mode's budget rule (executor.py:192-193 / 237-241).
-  There is no CPU path.
+* ``mode``: "gpu" (default) evaluates with the reference's DEFAULT mode's
+  budget rule, the sequential one: a join raises ResourceLimitError when its
+  EMITTED rows exceed ``row_budget`` (executor.py:192-193), so a query whose
+  pre-filter candidate total E is large but whose output is small (the
+  device filters while expanding) is answered, as ``gsmat query`` answers it.
+  "sequential" is the same rule; "parallel" selects the parallel mode's
+  pre-allocation rule (E > budget, executor.py:237-241). Every mode runs on
+  the GPU; there is no CPU path.
 * The result is a :class:`BindingTable` whose ``rows`` are the projected id
   tuples (bag; row order is not contractual); ``array`` holds
   the same rows as an (n, k) uint32 numpy array without building tuples.
@@ -179,6 +183,11 @@ def _compile(query, plan):
     return steps, arr, proj_arr, len(proj)
 
 
+def _budget_mode(mode: str) -> int:
+    """"gpu" and "sequential" -> emitted-rows rule; "parallel" -> E rule."""
+    return _lib.GSM_BUDGET_PARALLEL if mode == "parallel" else _lib.GSM_BUDGET_SEQUENTIAL
+
+
 def execute(
     query,
     plan,
@@ -202,9 +211,12 @@ def execute(
     if not plan.steps:
         raise ValueError("cannot execute an empty plan")
     dstore = store if isinstance(store, DeviceStore) else from_store(store)
+    if getattr(dstore, "shard", None) is not None:
+        raise ValueError(
+            f"store holds shard {dstore.shard} only; evaluate it with sharded.execute_sharded")
     steps, arr, proj_arr, nproj = compile_plan(query, plan)
     n = len(steps)
-    budget_mode = _lib.GSM_BUDGET_SEQUENTIAL if mode == "sequential" else _lib.GSM_BUDGET_PARALLEL
+    budget_mode = _budget_mode(mode)
     budget = min(int(row_budget), (1 << 63) - 1)
 
     rep_struct = None
@@ -259,6 +271,9 @@ def _fill_report(report, steps, rep_struct, rows_buf, pre_buf, ms_buf, kind_buf,
         report.steps.append(
             StepReport(_pattern_text(pat), int(rows_buf[i]), int(pre_buf[i]), float(ms_buf[i]) / 1e3)
         )
+    if not isinstance(report, ExecutionReport):
+        return  # the reference's own ExecutionReport: its fields only
+    for i in range(len(steps)):
         report.kinds.append(_lib.STEP_KINDS[kind_buf[i]])
         report.arities.append(int(ar_buf[i]))
     report.device_seconds += rep_struct.total_device_ms / 1e3
@@ -335,8 +350,11 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
     if not items:
         return []
     dstore = store if isinstance(store, DeviceStore) else from_store(store)
+    if getattr(dstore, "shard", None) is not None:
+        raise ValueError(
+            f"store holds shard {dstore.shard} only; evaluate it with sharded.execute_sharded")
     n = len(items)
-    budget_mode = _lib.GSM_BUDGET_SEQUENTIAL if mode == "sequential" else _lib.GSM_BUDGET_PARALLEL
+    budget_mode = _budget_mode(mode)
     budget = min(int(row_budget), (1 << 63) - 1)
     prep = _prepared_batch(dstore, items, budget_mode, budget)
     qarr = prep.qarr

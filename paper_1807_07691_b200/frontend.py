@@ -388,35 +388,3 @@ def make_plan(query, stats) -> Plan:
             steps.append(PlanStep(pat, est, [v for v in pat.variables() if v in bound]))
             bound.update(pat.variables())
     return Plan(steps, warnings)
-
-
-# -- cost bounds (planner.py:17-55) ---------------------------------------
-
-_SATURATE = (1 << 63) - 1
-
-
-@dataclass(frozen=True)
-class CostBounds:
-    """planner.CostBounds (planner.py:30-33)."""
-
-    lower: int
-    upper: int
-
-
-def delta_bounds(cards: list[int]) -> CostBounds:
-    """planner.delta_bounds (planner.py:36-55): bounds on the total
-    intermediate-result count of a left-deep join — lower: sum of running
-    minima, upper: sum of running products (saturating), both from the
-    second relation on; a single relation bounds to itself."""
-    if not cards:
-        raise ValueError("delta_bounds requires at least one cardinality")
-    if len(cards) == 1:
-        return CostBounds(cards[0], cards[0])
-    lower = upper = 0
-    run_min = run_prod = cards[0]
-    for c in cards[1:]:
-        run_min = min(run_min, c)
-        run_prod = min(run_prod * c, _SATURATE)
-        lower = min(lower + run_min, _SATURATE)
-        upper = min(upper + run_prod, _SATURATE)
-    return CostBounds(lower, upper)

@@ -84,7 +84,7 @@ def _layout(left, right, join_vars):
     return jl, jr, tuple(left.schema) + tuple(rcols)
 
 
-def _join(left, right, join_vars, row_budget, budget_mode, want_counts=False):
+def _join(left, right, join_vars, row_budget, budget_mode, want_counts=False, counts_only=False):
     L = _lib.lib()
     la, ra = _rows_array(left), _rows_array(right)
     if join_vars:
@@ -101,8 +101,11 @@ def _join(left, right, join_vars, row_budget, budget_mode, want_counts=False):
         _context(), la.ctypes.data if la.size else None, la.shape[0], la.shape[1],
         ra.ctypes.data if ra.size else None, ra.shape[0], ra.shape[1], jl_a, jr_a, nj,
         min(int(row_budget), (1 << 63) - 1), budget_mode, C.byref(E),
-        counts.ctypes.data if (counts is not None and counts.size) else None, C.byref(res))
+        counts.ctypes.data if (counts is not None and counts.size) else None,
+        None if counts_only else C.byref(res))
     _lib.check(st)
+    if counts_only:
+        return None, int(E.value), counts
     out = _fetch(L, res)
     return BindingTable(schema, array=out), int(E.value), counts
 
@@ -137,16 +140,18 @@ def cross_product(left, right, row_budget: int = DEFAULT_ROW_BUDGET) -> BindingT
 
 def preallocate(left, right, first_var: str) -> PreallocPlan:
     """executor.preallocate (executor.py:197-215): the device computes every
-    left row's first-variable match count N_r; rows are grouped by key in
-    first-occurrence order (N[g] = sum of N_r over the group)."""
+    left row's first-variable match count N_r (a counts-only table join: no
+    candidate is materialised, O(|L| + |R|) device memory); rows are grouped
+    by key in first-occurrence order (N[g] = sum of N_r over the group)."""
     _, E, counts = _join(left, right, [first_var], (1 << 62), _lib.GSM_BUDGET_PARALLEL,
-                         want_counts=True)
+                         want_counts=True, counts_only=True)
     la = _rows_array(left)
     if la.shape[0] == 0:
         return PreallocPlan([], [], [], 0)
     keys = la[:, list(left.schema).index(first_var)].astype(np.int64)
     uniq, first, inv = np.unique(keys, return_index=True, return_inverse=True)
-    sums = np.bincount(inv, weights=counts, minlength=len(uniq)).astype(np.int64)
+    sums = np.zeros(len(uniq), dtype=np.int64)  # exact int64 group sums
+    np.add.at(sums, inv.reshape(-1), counts)
     order = np.argsort(first, kind="stable")
     gk = uniq[order].tolist()
     gc = sums[order].tolist()

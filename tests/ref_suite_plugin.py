@@ -1,0 +1,31 @@
+"""pytest plugin for tests/test_reference_suite.py: counts the reference
+suite's calls that reach the B200 executor and the kernels they launched,
+and writes both to $GSM_REF_SUITE_COUNTS at the end of the session."""
+
+from __future__ import annotations
+
+import json
+import os
+
+_calls = {"execute": 0}
+
+
+def pytest_configure(config):
+    import paper_1807_07691_b200 as g
+
+    inner = g.execute
+
+    def counted(*args, **kwargs):
+        _calls["execute"] += 1
+        return inner(*args, **kwargs)
+
+    g.execute = counted
+
+
+def pytest_sessionfinish(session, exitstatus):
+    from paper_1807_07691_b200 import _lib
+
+    path = os.environ.get("GSM_REF_SUITE_COUNTS")
+    if path:
+        with open(path, "w") as fh:
+            json.dump({"execute_calls": _calls["execute"], "kernels": _lib.kernel_launches()}, fh)

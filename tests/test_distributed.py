@@ -16,14 +16,34 @@ import torch.multiprocessing as mp
 from conftest import REPO, lubm_queries
 
 QUERIES = dict(lubm_queries())
+UB = "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
+RDF = "PREFIX rdf: <http://www.w3.org/1999/02/22-rdf-syntax-ns#> "
+CROSS = (RDF + UB + "SELECT * WHERE { ?x rdf:type ub:FullProfessor . "
+         "?y rdf:type ub:Course . }")
+# (name, query, row budget or None, mode)
 CASES = [
-    ("q09", QUERIES["q09"], None),
-    ("q08", QUERIES["q08"], None),
-    ("q02", QUERIES["q02"], None),
-    ("distinct", "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
-                 "SELECT DISTINCT ?d WHERE { ?x ub:memberOf ?d . ?x ub:takesCourse ?c . }", None),
-    ("budget", QUERIES["q09"], 10),
+    ("q09", QUERIES["q09"], None, "gpu"),
+    ("q08", QUERIES["q08"], None, "gpu"),
+    ("q02", QUERIES["q02"], None, "gpu"),
+    ("distinct", UB + "SELECT DISTINCT ?d WHERE { ?x ub:memberOf ?d . ?x ub:takesCourse ?c . }",
+     None, "gpu"),
+    ("cross", CROSS, None, "gpu"),
+    ("budget_par", QUERIES["q09"], 10, "parallel"),
+    ("budget_seq", QUERIES["q09"], 10, "gpu"),
+    ("budget_cross", CROSS, 50, "gpu"),
 ]
+
+
+def _kinds(plan) -> list[str]:
+    """Step kinds as the executor reports them: a step sharing no variable
+    with the steps before it is a cross product (a gate when it has none)."""
+    bound: set = set()
+    kinds = []
+    for i, st in enumerate(plan.steps):
+        vs = {t for t in (st.pattern.s, st.pattern.o) if isinstance(t, str)}
+        kinds.append("scan" if i == 0 else "join" if vs & bound else "cross" if vs else "gate")
+        bound |= vs
+    return kinds
 
 
 def _free_port() -> int:
@@ -53,15 +73,15 @@ def _worker(rank, world, port, store_dir, out_dir):
                                     q.distinct, partition=part)
         for i, s in enumerate(plan.steps):
             rep.steps.append(StepReport(s.pattern.source.text(), srows[i], spre[i], 0.0))
-        rep.kinds = ["scan"] + ["join"] * (len(plan.steps) - 1)
+        rep.kinds = _kinds(plan)
         return np.asarray(rows, dtype=np.uint32).reshape(len(rows), len(q.projection))
 
     results = {}
-    for name, text, budget in CASES:
+    for name, text, budget, mode in CASES:
         q, plan = plan_for(store, text)
         try:
             rep = ExecutionReport()
-            res = execute_distributed(q, plan, store, runner=runner, report=rep,
+            res = execute_distributed(q, plan, store, runner=runner, report=rep, mode=mode,
                                       row_budget=budget if budget is not None else 10**8)
             results[name] = ("ok", orc.fingerprint_array(res.array), [s.rows for s in rep.steps],
                              [s.prealloc_total for s in rep.steps])
@@ -82,15 +102,19 @@ def test_row_partitioned_two_ranks(tmp_path, store_factory):
     r0 = np.load(tmp_path / "rank0.npy", allow_pickle=True)[0]
     r1 = np.load(tmp_path / "rank1.npy", allow_pickle=True)[0]
     store = HostStore(store_dir)
-    for name, text, budget in CASES:
+    prep = orc.PreparedStore(store.matrices)
+    for name, text, budget, mode in CASES:
         q, plan = plan_for(store, text)
         if budget is not None:
-            assert r0[name][0] == "ResourceLimitError" == r1[name][0]
-            assert r0[name][1] == r1[name][1]
-            assert "pre-allocated join region" in r0[name][1]
+            # the same error, raised on every rank, as the whole-store oracle
+            # (the reference's rule for the mode: "gpu" = the sequential one)
+            with pytest.raises(orc.OracleResourceError) as exc:
+                orc.run(prep, [s.pattern for s in plan.steps], q.projection, q.distinct,
+                        budget=budget, mode="parallel" if mode == "parallel" else "sequential")
+            assert r0[name] == ("ResourceLimitError", str(exc.value)) == r1[name], name
             continue
-        rows, srows, spre = orc.run(orc.PreparedStore(store.matrices),
-                                    [s.pattern for s in plan.steps], q.projection, q.distinct)
+        rows, srows, spre = orc.run(prep, [s.pattern for s in plan.steps], q.projection,
+                                    q.distinct)
         exp = np.asarray(rows, dtype=np.uint32).reshape(len(rows), len(q.projection))
         assert r0[name][0] == "ok"
         assert tuple(r0[name][1]) == orc.fingerprint_array(exp), name

@@ -170,10 +170,25 @@ def test_budget_and_arena_growth(store_factory):
     q, plan = _plan(store, text)
     full = g.execute(q, plan, store)
     with pytest.raises(g.ResourceLimitError, match="pre-allocated join region"):
-        g.execute(q, plan, store, row_budget=len(full) - 1)
-    with pytest.raises(g.ResourceLimitError, match="join output exceeds row budget"):
-        g.execute(q, plan, store, mode="sequential", row_budget=len(full) - 1)
+        g.execute(q, plan, store, mode="parallel", row_budget=len(full) - 1)
+    # mode="gpu" (the default) applies the reference's default (sequential) rule
+    for mode in ("gpu", "sequential"):
+        with pytest.raises(g.ResourceLimitError, match="join output exceeds row budget"):
+            g.execute(q, plan, store, mode=mode, row_budget=len(full) - 1)
     assert len(g.execute(q, plan, store, row_budget=len(full))) == len(full)
+    # a filter join whose E exceeds the budget but whose output does not is
+    # answered under the default rule, and refused under the parallel one
+    tri = "SELECT * WHERE { ?x <p1> ?y . ?y <p1> ?z . ?z <p1> ?x . }"
+    q, plan = _plan(store, tri)
+    rep = g.ExecutionReport()
+    res = g.execute(q, plan, store, report=rep)
+    e_max = max(s.prealloc_total for s in rep.steps)
+    o_max = max(s.rows for s in rep.steps[1:])
+    if o_max < e_max:
+        budget = o_max
+        assert len(g.execute(q, plan, store, row_budget=budget)) == len(res)
+        with pytest.raises(g.ResourceLimitError, match="pre-allocated join region"):
+            g.execute(q, plan, store, mode="parallel", row_budget=budget)
 
 
 def test_reference_objects_drop_in():
@@ -188,8 +203,11 @@ def test_reference_objects_drop_in():
     ref = gsmat.executor.execute(q, plan, st)
     got = g.execute(q, plan, st, mode="gpu")
     assert _bag(got.rows) == _bag(ref.rows)
-    with pytest.raises(gsmat.errors.ResourceLimitError):
+    with pytest.raises(g.ResourceLimitError) as exc:
         g.execute(q, plan, st, row_budget=0)
+    with pytest.raises(gsmat.errors.ResourceLimitError) as ref_exc:
+        gsmat.executor.execute(q, plan, st, row_budget=0)
+    assert str(exc.value) == str(ref_exc.value)
 
 
 UB = "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
@@ -320,8 +338,10 @@ def test_execute_batch_matches_sequential(store_factory):
     # a budget violation in one query raises the reference's error
     q9 = dict(lubm_queries())["q09"]
     bad = items[:3] + [_plan(store, q9)]
-    with pytest.raises(g.ResourceLimitError, match="pre-allocated join region"):
+    with pytest.raises(g.ResourceLimitError, match="join output exceeds row budget 5"):
         g.execute_batch(bad, store, row_budget=5)
+    with pytest.raises(g.ResourceLimitError, match="pre-allocated join region"):
+        g.execute_batch(bad, store, mode="parallel", row_budget=5)
 
 
 def test_batch_planning_error_falls_back(store_factory):
