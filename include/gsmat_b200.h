@@ -82,6 +82,8 @@ typedef struct {
   int64_t h2d_bytes;       /* out: host->device bytes copied for this query          */
   int64_t d2h_bytes;       /* out: device->host bytes of the query incl. result rows */
   int64_t kernels;         /* out: kernels launched for this query                   */
+  int32_t* fused;          /* 1 = the step ran inside the previous step's kernel
+                              (k_group): its input table was never materialised    */
 } gsm_report;
 
 /* Step kinds reported in gsm_report.kind (SURVEY.md §8 join taxonomy). */

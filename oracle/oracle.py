@@ -102,11 +102,12 @@ class PreparedStore:
 
 
 def run(store, patterns, projection, distinct=False, budget=(1 << 62), mode="sequential",
-        partition=(0, 1)):
+        partition=(0, 1), as_array=False):
     """Returns (rows: list[tuple], step_rows: list[int], step_prealloc: list[int]).
 
     ``partition=(i, k)`` keeps only the i-th of k contiguous slices of the
-    first step's rows (the executor's multi-GPU row partitioning)."""
+    first step's rows (the executor's multi-GPU row partitioning).  With
+    ``as_array`` the rows come back as an (n, k) int64 array (no tuples)."""
     if not isinstance(store, PreparedStore):
         store = PreparedStore(store)
     n = len(patterns)
@@ -142,7 +143,10 @@ def run(store, patterns, projection, distinct=False, budget=(1 << 62), mode="seq
     try:
         k = len(proj)
         cnt = int(nout.value)
-        if cnt and k:
+        if as_array:
+            rows = (np.ctypeslib.as_array(out, shape=(cnt * k,)).reshape(cnt, k).copy()
+                    if cnt and k else np.zeros((cnt, k), dtype=np.int64))
+        elif cnt and k:
             flat = np.ctypeslib.as_array(out, shape=(cnt * k,)).copy()
             rows = [tuple(r) for r in flat.reshape(cnt, k).tolist()]
         else:

@@ -93,6 +93,7 @@ class Report(C.Structure):
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
         ("kernels", C.c_int64),
+        ("fused", C.POINTER(C.c_int32)),
     ]
 
 

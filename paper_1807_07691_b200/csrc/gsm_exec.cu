@@ -1324,25 +1324,30 @@ __global__ void k_init(const uint4* __restrict__ src, uint4* __restrict__ dst, i
                        u32* epochs, int n_epochs, ResolveArgs res, DTable* tables, StepStat* stats) {
   pdl_wait();
   pdl_trigger();
+  // The three parts are independent chains of (cold, after an L2 flush)
+  // loads; all of them are issued before the block synchronises, so the
+  // kernel costs the longest chain, not their sum.  Only the stores into the
+  // block wait for the image copy.
+  const int i = threadIdx.x;
+  u32 base = 0;
+  if (i == 0 && n_epochs > 0) base = *ctr;
+  uint2 sg = make_uint2(0, 0);
+  i64 n = 0;
+  if (i < res.njobs) {
+    const ResolveJob& jb = res.job[i];
+    sg = seg_lookup(jb.R, jb.k1);
+    n = jb.kind == J_SEG ? (i64)sg.y : (sg.y && sorted_contains(jb.R.dst + sg.x, sg.y, jb.k2)) ? 1 : 0;
+  }
   if (src)
-    for (int i = threadIdx.x; i < words16; i += blockDim.x) dst[i] = src[i];
+    for (int w = i; w < words16; w += blockDim.x) dst[w] = src[w];
   __syncthreads();
-  if (threadIdx.x == 0 && n_epochs > 0) {
-    const u32 base = *ctr;
-    for (int i = 0; i < n_epochs; i++) epochs[i] = base + 1 + (u32)i;
+  if (i == 0 && n_epochs > 0) {
+    for (int e = 0; e < n_epochs; e++) epochs[e] = base + 1 + (u32)e;
     *ctr = base + (u32)n_epochs;
   }
-  const int i = threadIdx.x;
   if (i >= res.njobs) return;
   const ResolveJob& jb = res.job[i];
-  const uint2 sg = seg_lookup(jb.R, jb.k1);
-  i64 n;
-  if (jb.kind == J_SEG) {
-    n = sg.y;
-    tables[jb.table].col[0] = const_cast<u32*>(jb.R.dst) + sg.x;
-  } else {
-    n = (sg.y && sorted_contains(jb.R.dst + sg.x, sg.y, jb.k2)) ? 1 : 0;
-  }
+  if (jb.kind == J_SEG) tables[jb.table].col[0] = const_cast<u32*>(jb.R.dst) + sg.x;
   tables[jb.table].n = n;
   if (jb.stat >= 0) stats[jb.stat].rows = n;
 }
@@ -1701,7 +1706,7 @@ struct gsm_context {
     i64 h2d = 0;
     bool zc = false;
     char* d_image = nullptr;  // device copy of `image` (k_init's source)
-    std::vector<int> kinds, arities;
+    std::vector<int> kinds, arities, fused_in;
   };
   std::unordered_map<std::string, GraphEntry> graphs;
   // A prepared batch (gsm_execute_batch with this context first): the launch
@@ -1787,6 +1792,9 @@ gsm_status ctx_set_stage(gsm_context* c, size_t bytes) {
   bytes = (bytes + 4095) & ~(size_t)4095;
   GSM_CUDA(cudaMallocHost(&c->h_stage, bytes + STAGE_HEAD));
   GSM_CUDA(cudaMalloc(&c->d_stage, bytes + STAGE_HEAD));
+  // the launch sequence copies a size GUESS of this buffer to the host
+  // (valid rows + a tail the host ignores): defined bytes, once
+  GSM_CUDA(cudaMemset(c->d_stage, 0, bytes + STAGE_HEAD));
   c->h_rows = c->h_stage + STAGE_HEAD / 4;
   c->d_rows = c->d_stage + STAGE_HEAD / 4;
   GSM_CUDA(cudaHostGetDevicePointer((void**)&c->hd_stage, c->h_stage, 0));
@@ -2032,6 +2040,7 @@ struct ExecState {
   bool timing = false;
   std::string plan_key;
   std::vector<int> kinds, arities;  // per step (report, budget checks)
+  std::vector<int> fused_in;        // per step: 1 = ran inside the previous step's kernel
   // Batch capture: the caller holds c->stream inside a stream capture; only
   // issue the launch sequence into it and describe it in `meta`.
   bool capture_only = false;
@@ -2056,6 +2065,7 @@ static void apply_entry(gsm_context* c, const gsm_context::GraphEntry& P, ExecSt
   S.h2d = P.h2d;
   S.kinds = P.kinds;
   S.arities = P.arities;
+  S.fused_in = P.fused_in;
 }
 
 // Plan key: everything a query's launch sequence derives from, including the
@@ -2392,6 +2402,10 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     }
     launches.swap(fl);
   }
+  S.fused_in.assign(n, 0);
+  for (const Launch& L : launches)
+    if (L.kind == S_GROUP)
+      for (int q = L.step + 1; q <= L.last_step; q++) S.fused_in[q] = 1;
 
   // ---- hub deferral for expands whose orientation has long runs ----
   {
@@ -2654,6 +2668,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     P.d_image = d_image;
     P.kinds = S.kinds;
     P.arities = S.arities;
+    P.fused_in = S.fused_in;
     return GSM_OK;
   }
   if (graphs) {
@@ -2691,6 +2706,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       P.d_image = d_image;
       P.kinds = S.kinds;
       P.arities = S.arities;
+      P.fused_in = S.fused_in;
       c->graphs.emplace(key, std::move(P));
     }
     GSM_CUDA(cudaGraphLaunch(ge, st));
@@ -2844,6 +2860,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
       StepKind k = (StepKind)S.kinds[s];
       if (rep->kind) rep->kind[s] = (int32_t)k;
       if (rep->arity) rep->arity[s] = (int32_t)S.arities[s];
+      if (rep->fused) rep->fused[s] = s < (int)S.fused_in.size() ? S.fused_in[s] : 0;
       if (rep->rows) rep->rows[s] = hb->stats[s].rows;
       if (rep->prealloc_total)
         rep->prealloc_total[s] = (k == S_EXPAND || k == S_FILTER) ? hb->stats[s].e : 0;

@@ -99,8 +99,9 @@ class StepReport:
 class ExecutionReport:
     """executor.ExecutionReport (executor.py:74-91); seconds are device time.
 
-    Extra device-side fields (not in the reference): per-step ``kinds`` and
-    ``arities``, the whole-query ``device_seconds``, the bytes copied each way
+    Extra device-side fields (not in the reference): per-step ``kinds``,
+    ``arities`` and ``fused`` (1 = the step ran inside the previous step's
+    kernel, so its input table was never materialised), the whole-query ``device_seconds``, the bytes copied each way
     (``h2d_bytes``, ``d2h_bytes``, result rows included) and ``kernels``.
     """
 
@@ -109,6 +110,7 @@ class ExecutionReport:
     uses: int = 0
     kinds: list[str] = field(default_factory=list)
     arities: list[int] = field(default_factory=list)
+    fused: list[int] = field(default_factory=list)
     device_seconds: float = 0.0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
@@ -211,7 +213,7 @@ def execute(
     if not plan.steps:
         raise ValueError("cannot execute an empty plan")
     dstore = store if isinstance(store, DeviceStore) else from_store(store)
-    if getattr(dstore, "shard", None) is not None:
+    if getattr(dstore, "shard", None) is not None and dstore.shard[1] > 1:
         raise ValueError(
             f"store holds shard {dstore.shard} only; evaluate it with sharded.execute_sharded")
     steps, arr, proj_arr, nproj = compile_plan(query, plan)
@@ -220,9 +222,9 @@ def execute(
     budget = min(int(row_budget), (1 << 63) - 1)
 
     rep_struct = None
-    rows_buf = pre_buf = ms_buf = kind_buf = ar_buf = None
+    bufs = None
     if report is not None:
-        rep_struct, (rows_buf, pre_buf, ms_buf, kind_buf, ar_buf) = _new_report(n)
+        rep_struct, bufs = _new_report(n)
 
     L = _lib.lib()
     res = C.c_void_p()
@@ -235,7 +237,7 @@ def execute(
     _lib.check(st)
     out = _fetch(L, res)
     if report is not None:
-        _fill_report(report, steps, rep_struct, rows_buf, pre_buf, ms_buf, kind_buf, ar_buf)
+        _fill_report(report, steps, rep_struct, *bufs)
     return BindingTable(tuple(query.projection), array=out)
 
 
@@ -255,11 +257,14 @@ def _fetch(L, res) -> np.ndarray:
 
 def _new_report(n: int):
     bufs = ((C.c_int64 * n)(), (C.c_int64 * n)(), (C.c_float * n)(), (C.c_int32 * n)(),
-            (C.c_int32 * n)())
-    return _lib.Report(*bufs), bufs
+            (C.c_int32 * n)(), (C.c_int32 * n)())
+    rep = _lib.Report(*bufs[:5])
+    rep.fused = bufs[5]
+    return rep, bufs
 
 
-def _fill_report(report, steps, rep_struct, rows_buf, pre_buf, ms_buf, kind_buf, ar_buf) -> None:
+def _fill_report(report, steps, rep_struct, rows_buf, pre_buf, ms_buf, kind_buf, ar_buf,
+                 fused_buf) -> None:
     # matrix_of(): one preparation per distinct pid, one use per step (executor.py:315-325)
     seen: set[int] = set()
     for pat in steps:
@@ -276,6 +281,7 @@ def _fill_report(report, steps, rep_struct, rows_buf, pre_buf, ms_buf, kind_buf,
     for i in range(len(steps)):
         report.kinds.append(_lib.STEP_KINDS[kind_buf[i]])
         report.arities.append(int(ar_buf[i]))
+        report.fused.append(int(fused_buf[i]))
     report.device_seconds += rep_struct.total_device_ms / 1e3
     report.h2d_bytes += int(rep_struct.h2d_bytes)
     report.d2h_bytes += int(rep_struct.d2h_bytes)
@@ -350,7 +356,7 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
     if not items:
         return []
     dstore = store if isinstance(store, DeviceStore) else from_store(store)
-    if getattr(dstore, "shard", None) is not None:
+    if getattr(dstore, "shard", None) is not None and dstore.shard[1] > 1:
         raise ValueError(
             f"store holds shard {dstore.shard} only; evaluate it with sharded.execute_sharded")
     n = len(items)

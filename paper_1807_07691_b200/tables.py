@@ -22,6 +22,7 @@ reference's (sequential: emitted rows; parallel: the pre-allocated total E).
 from __future__ import annotations
 
 import ctypes as C
+import atexit
 import threading
 from collections import Counter
 from dataclasses import dataclass
@@ -58,7 +59,18 @@ def _context(device: int = 0):
             ctx = C.c_void_p()
             _lib.check(L.gsm_context_create(store, 1 << 20, C.byref(ctx)))
             hit = _ctx[device] = (store, ctx)
+            if len(_ctx) == 1:
+                atexit.register(_free_contexts)
         return hit[1]
+
+
+def _free_contexts() -> None:
+    L = _lib.lib()
+    with _ctx_lock:
+        for store, ctx in _ctx.values():
+            L.gsm_context_free(ctx)
+            L.gsm_store_free(store)
+        _ctx.clear()
 
 
 def _rows_array(table) -> np.ndarray:

@@ -25,3 +25,14 @@ def test_reference_arm_json_line():
         assert k in line, k
     assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    # both of the reference's modes were timed; value is the faster one
+    assert set(line["modes"]) == {"sequential", "parallel"}
+    assert line["value"] == max(m["value"] for m in line["modes"].values())
+    assert line["cpu_baseline"]["cpu_model"]
+    # the same workload description as the GPU arm
+    sys.path.insert(0, str(REPO))
+    import bench
+
+    class A:
+        univ, seed = 1, 0
+    assert line["config"] == bench._config(A, line["config"]["triples"])

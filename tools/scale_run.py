@@ -117,9 +117,8 @@ def main():
         rec["join_rows_per_s"] = round(rec["join_rows"] / statistics.median(dev), 1)
         # HBM roofline of the whole query: algorithmic bytes of its join steps
         # (bench._step_bytes) / device time
-        qbytes = sum(bench._step_bytes(rep.kinds[i], rep.steps[i - 1].rows, rep.arities[i - 1],
-                                       rep.steps[i].prealloc_total, rep.steps[i].rows, rep.arities[i])
-                     for i in range(1, len(rep.steps)))
+        # (fused intermediates are not billed: bench.query_bytes)
+        qbytes = bench.query_bytes(rep, len(q.projection))
         gbps = qbytes / statistics.median(dev) / 1e9
         rec["bytes"] = int(qbytes)
         rec["achieved_GBps"] = round(gbps, 1)
