@@ -63,6 +63,20 @@ def _args():
     ap.add_argument("--no-probe", action="store_true")
     ap.add_argument("--only-probe", action="store_true", help="run only the kernel probe (ncu)")
     ap.add_argument("--probe", default=None, help="with --only-probe: run just this probe")
+    ap.add_argument("--mode", choices=["replica", "partition", "sharded"], default="replica",
+                    help="N>1: replica = every rank serves its own copy of the query stream "
+                         "(default); partition = every query's first table split across the ranks "
+                         "by equal E over replicated stores (distributed.py); sharded = subject/"
+                         "object id-range shards with all-to-all exchanges (sharded.py)")
+    ap.add_argument("--workload", choices=["lubm", "watdiv", "powerlaw"], default="lubm",
+                    help="store/queries of --mode partition|sharded (configs[1]-[4])")
+    ap.add_argument("--scale", type=int, default=1000, help="watdiv scale (1000 ~ 100M triples)")
+    ap.add_argument("--triples", type=int, default=100_000_000, help="powerlaw triples")
+    ap.add_argument("--predicates", type=int, default=40, help="powerlaw predicates")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="every rank on cuda:0 (multi-rank tests on a one-GPU box; needs gloo)")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--scale-univ", type=int, default=1000,
                     help="configs[2]: LUBM-style scale run in the same invocation (N=1); 0 = skip")
     ap.add_argument("--scale-reps", type=int, default=3)
@@ -736,11 +750,240 @@ def run_reference(args):
         }), flush=True)
 
 
+WORKLOAD_QDIRS = {"lubm": ("lubm", "lubm_complex"), "watdiv": ("watdiv",), "powerlaw": ("powerlaw",)}
+
+
+def _gen_args(args) -> list[str]:
+    if args.workload == "lubm":
+        return ["lubm", "--univ", str(args.univ), "--seed", str(args.seed)]
+    if args.workload == "watdiv":
+        return ["watdiv", "--scale", str(args.scale), "--seed", str(args.seed)]
+    return ["powerlaw", "--triples", str(args.triples), "--predicates", str(args.predicates),
+            "--seed", str(args.seed)]
+
+
+def run_distributed(args):
+    """--mode partition|sharded: every query of the workload evaluated by ALL
+    ranks together, one process per GPU.
+
+    * partition: replicated store; the first table of every query is split
+      by equal E (the first join's candidate counts, k_slice_sums /
+      k_slice_pick), no exchange between steps; per-step counters all-reduced.
+    * sharded: rank r loads only id range r of every pair file (one byte
+      range each) and rows are re-keyed by all-to-all between steps.
+    One step = the workload's queries once.  Device time of a query = the
+    span between CUDA events on the executing stream, max over ranks;
+    ``e2e`` = host wall clock incl. the gather of the result rows to rank 0.
+    Parity: rank 0 checks every query's gathered bag (and the global step
+    counters) against the C oracle on the whole store."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = _dist()
+    dev = 0 if args.share_gpu else local
+    torch.cuda.set_device(dev)
+    dist.init_process_group(args.backend)
+    import paper_1807_07691_b200 as g
+    from paper_1807_07691_b200 import _lib
+    from paper_1807_07691_b200.distributed import execute_distributed
+    from paper_1807_07691_b200.sharded import execute_sharded
+
+    holder = [None]
+    if rank == 0:
+        tmp = tempfile.mkdtemp(prefix="gsm_bench_")
+        t0 = time.perf_counter()
+        subprocess.run([str(REPO / "oracle" / "_build" / "gsmgen"), *_gen_args(args), "--out",
+                        f"{tmp}/store"], check=True, stdout=subprocess.DEVNULL)
+        holder[0] = (f"{tmp}/store", time.perf_counter() - t0)
+    dist.broadcast_object_list(holder, src=0)
+    store_dir, t_gen = holder[0]
+    t0 = time.perf_counter()
+    store = g.load(store_dir, device=dev, shard=(rank, world) if args.mode == "sharded" else None)
+    t_load = time.perf_counter() - t0
+    qs = []
+    for d in WORKLOAD_QDIRS[args.workload]:
+        for f in sorted((REPO / "datagen" / "queries" / d).glob("*.rq")):
+            q = g.bind_constants(g.parse_query(f.read_text()), store.dictionary)
+            qs.append((f.stem, q, g.make_plan(q, store.stats)))
+    ctx = store.context()
+    sp = C_u64()
+    _lib.check(_lib.lib().gsm_context_stream(ctx, sp.ref()))
+    stream = torch.cuda.ExternalStream(sp.value, device=torch.device("cuda", dev))
+    budget = 1 << 62
+
+    def run(q, plan, rep):
+        if args.mode == "sharded":
+            return execute_sharded(q, plan, store, row_budget=budget, report=rep)
+        with torch.cuda.stream(stream):
+            return execute_distributed(q, plan, store, row_budget=budget, report=rep)
+
+    def one(q, plan):
+        rep = g.ExecutionReport()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tw = time.perf_counter()
+        e0.record(stream)
+        res = run(q, plan, rep)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - tw
+        return res, rep, e0.elapsed_time(e1) / 1e3, wall
+
+    skipped = {}
+    for name, q, plan in list(qs):  # warm-up (plans, graphs, arenas); drop infeasible queries
+        try:
+            for _ in range(max(1, args.warmup)):
+                one(q, plan)
+        except g.ResourceLimitError as e:
+            skipped[name] = str(e)
+    qs = [x for x in qs if x[0] not in skipped]
+    launches0 = _lib.kernel_launches()
+    per = {name: {"dev": [], "wall": []} for name, *_ in qs}
+    reps, results = {}, {}
+    for _ in range(args.steps):
+        for name, q, plan in qs:
+            res, rep, d, w = one(q, plan)
+            per[name]["dev"].append(d)
+            per[name]["wall"].append(w)
+            reps[name], results[name] = rep, res
+    launches = _lib.kernel_launches() - launches0
+    # max over ranks of every per-query device / wall time, sums of sent bytes
+    names = [n for n, *_ in qs]
+    t = torch.tensor([x for n in names for x in (sum(per[n]["dev"]), sum(per[n]["wall"]))],
+                     dtype=torch.float64)
+    b = torch.tensor([reps[n].exchanged_bytes for n in names], dtype=torch.float64)
+    if args.backend == "nccl":
+        t, b = t.cuda(), b.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(b)
+    t, b = t.cpu().tolist(), b.cpu().tolist()
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    peaks, peak_kind = _peaks()
+    out_q = {}
+    tot_dev = tot_wall = 0.0
+    tot_rows = tot_bytes = 0
+    for i, (name, q, plan) in enumerate(qs):
+        rep = reps[name]
+        dev_s, wall_s = t[2 * i] / args.steps, t[2 * i + 1] / args.steps
+        jr = _join_rows(rep.steps)
+        if len(rep.arities) != len(rep.steps):
+            rep.arities = _arities(plan, q)
+        qb = query_bytes(rep, len(q.projection))
+        out_q[name] = {"ms": round(1e3 * dev_s, 4), "e2e_ms": round(1e3 * wall_s, 4),
+                       "result_rows": len(results[name]), "join_rows": jr,
+                       "join_rows_per_s": round(jr / dev_s, 1) if dev_s else 0.0,
+                       "exchanged_bytes": int(b[i]) // max(1, args.steps),
+                       "per_gpu_GBps": round(qb / world / dev_s / 1e9, 2) if dev_s else 0.0}
+        tot_dev += dev_s
+        tot_wall += wall_s
+        tot_rows += jr
+        tot_bytes += qb
+    parity = None
+    if not args.no_parity:
+        parity = _distributed_parity(store_dir, qs, reps, results, args)
+        for name, ok in parity["per_query"].items():
+            out_q[name]["parity"] = ok
+    gbs = tot_bytes / world / tot_dev / 1e9 if tot_dev else 0.0
+    line = {
+        "metric": f"{args.workload} join output rows/sec, {args.mode} over {world} GPU(s)",
+        "value": round(tot_rows / tot_dev, 1) if tot_dev else 0.0, "unit": "rows/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * tot_dev, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": f"synthetic (datagen/gsmgen {' '.join(_gen_args(args))})",
+        "config": {"workload": f"{args.workload} ({store.triple_count} triples), "
+                               f"{len(qs)} queries, one step = every query once",
+                   "mode": args.mode, "backend": args.backend, "share_gpu": args.share_gpu,
+                   "parallelism": f"{args.mode} x{world}",
+                   "l2": "store larger than L2" if store.triple_count > 20_000_000 else
+                         "not flushed (small store; latency-bound)"},
+        "e2e": {"value": round(tot_rows / tot_wall, 1) if tot_wall else 0.0, "unit": "rows/s",
+                "ms_per_step": round(1e3 * tot_wall, 4), "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(sum(len(r) * max(1, len(r.schema)) * 4
+                                              for r in results.values()))},
+        "roofline_per_gpu": {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"],
+                             "peak_source": peak_kind, "unit": "GB/s",
+                             "frac": round(gbs / peaks["hbm_gbs"], 5),
+                             "note": "query_bytes (fused intermediates not billed) / world / "
+                                     "device time (max over ranks)"},
+        "exchanged_bytes_per_step": int(sum(b)) // max(1, args.steps),
+        "gen_s": round(t_gen, 1), "load_s_rank0": round(t_load, 2),
+        "queries": out_q, "skipped": skipped, "parity": parity,
+        "gpu_launches": int(launches),
+    }
+    print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    subprocess.run(["rm", "-rf", str(Path(store_dir).parent)])
+
+
+class C_u64:
+    def __init__(self):
+        import ctypes
+
+        self._v = ctypes.c_uint64(0)
+
+    def ref(self):
+        import ctypes
+
+        return ctypes.byref(self._v)
+
+    @property
+    def value(self) -> int:
+        return int(self._v.value)
+
+
+def _arities(plan, q) -> list[int]:
+    """Arity of the binding table after each step (the sharded report does
+    not carry them): first-appearance variables in plan order."""
+    seen: list[str] = []
+    out = []
+    for st in plan.steps:
+        for t in (st.pattern.s, st.pattern.o):
+            if isinstance(t, str) and t not in seen:
+                seen.append(t)
+        out.append(len(seen))
+    return out
+
+
+def _distributed_parity(store_dir, qs, reps, results, args):
+    """Rank 0: the gathered bag of every query (and its global per-step
+    counters when the oracle ran the plan's order) vs the C oracle."""
+    import numpy as np
+
+    sys.path.insert(0, str(REPO / "tests"))
+    from hoststore import HostStore
+    from oracle import oracle as orc
+
+    st = HostStore(store_dir)
+    prep = orc.PreparedStore(st.matrices)
+    per = {}
+    for name, q, plan in qs:
+        fp, srows, spre, how = _oracle_check(orc, prep, plan, q, args.oracle_guard, reps[name].steps)
+        if fp is None:
+            per[name] = how
+            continue
+        got = np.asarray(results[name].array, dtype=np.uint64)
+        ok = tuple(fp) == tuple(orc.fingerprint_array(got))
+        if srows is not None:
+            ok = ok and srows == [s.rows for s in reps[name].steps] and \
+                spre == [s.prealloc_total for s in reps[name].steps]
+        per[name] = bool(ok)
+    return {"per_query": per, "ok": sum(v is True for v in per.values()), "queries": len(per),
+            "oracle": "C restatement (oracle/gsm_oracle.c) on the whole store, rank 0"}
+
+
 def main():
     args = _args()
     _ensure_built()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode != "replica":
+        run_distributed(args)
     else:
         run_ours(args)
 

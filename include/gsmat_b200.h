@@ -149,6 +149,12 @@ gsm_status gsm_store_free(gsm_store* store);
 gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context** out);
 gsm_status gsm_context_free(gsm_context* ctx);
 
+/* The context's CUDA stream (cudaStream_t as an integer): every launch of
+ * the context is stream-ordered on it, so a caller can enqueue its own work
+ * (e.g. NCCL collectives in the sharded mode) on the same stream and skip
+ * host synchronisation between the library's launches and its own. */
+gsm_status gsm_context_stream(gsm_context* ctx, uint64_t* stream);
+
 /* Replaces executor.execute (executor.py:296-368) for mode="gpu":
  * evaluates `n_steps` patterns in plan order as a left-deep chain of SM-based
  * joins on the device, then projects onto `proj` (variable indices, n_proj of

@@ -43,6 +43,7 @@ EXPORTS = (
     "gsm_store_free",
     "gsm_context_create",
     "gsm_context_free",
+    "gsm_context_stream",
     "gsm_execute",
     "gsm_execute_batch",
     "gsm_execute_seeded",
@@ -154,6 +155,7 @@ def lib() -> C.CDLL:
             "gsm_store_free": (i32, [vp]),
             "gsm_context_create": (i32, [vp, i64, P(vp)]),
             "gsm_context_free": (i32, [vp]),
+            "gsm_context_stream": (i32, [vp, P(C.c_uint64)]),
             "gsm_execute": (
                 i32,
                 [vp, P(Pattern), i32, P(i32), i32, i32, i64, i32, i64, i64, P(Report), P(vp)],

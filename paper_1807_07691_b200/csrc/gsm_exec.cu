@@ -1367,6 +1367,93 @@ __global__ void k_slice(DTable* T, int a, i64 part, i64 parts, StepStat* st) {
   }
 }
 
+// Equal-E row partitioning of the first table ("balanced by
+// the count pass's prefix (equal E, not equal L)").  The first table is cut
+// into SLICE_CHUNKS contiguous chunks; k_slice_sums adds up the first join's
+// per-row candidate counts N_i (its segment lengths) per chunk, k_slice_pick
+// scans the chunk sums and gives rank `part` the chunks whose exclusive
+// prefix falls in [E*part/parts, E*(part+1)/parts).  Any split is correct
+// (the ranks' slices tile the table); this one balances E to within one
+// chunk.  E = 0 falls back to equal rows.
+constexpr int SLICE_CHUNKS = 4096;
+__global__ void k_slice_sums(const DTable* T, int key, Orient R, u64* __restrict__ sums) {
+  pdl_wait();
+  pdl_trigger();
+  const i64 n = T->n;
+  const i64 nch = n < SLICE_CHUNKS ? n : SLICE_CHUNKS;
+  const u32* kc = T->col[key];
+  const int lane = threadIdx.x & 31;
+  const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 ch = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nch; ch += nw) {
+    const i64 lo = (i64)((__int128)n * ch / nch), hi = (i64)((__int128)n * (ch + 1) / nch);
+    u64 acc = 0;
+    for (i64 r = lo + lane; r < hi; r += 32) acc += seg_lookup(R, __ldg(kc + r)).y;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sums[ch] = acc;
+  }
+}
+__global__ void __launch_bounds__(1024) k_slice_pick(DTable* T, int a, i64 part, i64 parts,
+                                                     StepStat* st, const u64* __restrict__ sums) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int PER = SLICE_CHUNKS / 1024;
+  __shared__ u64 s_w[32];
+  __shared__ unsigned long long s_lo, s_hi;
+  const i64 n = T->n;
+  const int nch = (int)(n < SLICE_CHUNKS ? n : SLICE_CHUNKS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  u64 v[PER], tot = 0;
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int ch = tid * PER + i;
+    v[i] = ch < nch ? sums[ch] : 0;
+    tot += v[i];
+  }
+  u64 x = tot;  // inclusive warp scan of the per-thread totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  if (tid == 0) s_lo = s_hi = 0;
+  __syncthreads();
+  u64 before = x - tot, E = 0;
+  for (int w = 0; w < 32; w++) {
+    if (w < warp) before += s_w[w];
+    E += s_w[w];
+  }
+  unsigned long long c_lo = 0, c_hi = 0;  // chunks owned by ranks < part / <= part
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int ch = tid * PER + i;
+    if (ch < nch && E > 0) {
+      i64 own = (i64)((unsigned __int128)before * (u64)parts / E);
+      if (own > parts - 1) own = parts - 1;
+      c_lo += own < part;
+      c_hi += own <= part;
+    }
+    before += v[i];
+  }
+  if (c_lo) atomicAdd(&s_lo, c_lo);
+  if (c_hi) atomicAdd(&s_hi, c_hi);
+  __syncthreads();
+  if (tid == 0) {
+    i64 lo, hi;
+    if (E > 0) {
+      lo = (i64)((__int128)n * (i64)s_lo / nch);
+      hi = (i64)((__int128)n * (i64)s_hi / nch);
+    } else {
+      lo = (i64)((__int128)n * part / parts);
+      hi = (i64)((__int128)n * (part + 1) / parts);
+    }
+    for (int c = 0; c < a; c++) T->col[c] += lo;
+    T->n = hi - lo;
+    st->rows = hi - lo;
+  }
+}
+
 struct ProjArgs {
   int col[GSM_MAX_VARS];
 };
@@ -1669,6 +1756,8 @@ struct gsm_context {
   cudaEvent_t ev_b0 = nullptr, ev_b1 = nullptr, ev_done = nullptr;  // batch timing
   // Result staging: [step counters (STAGE_HEAD bytes) | projected rows].
   u32* d_ctr = nullptr;     // device epoch counter (mirrored by `epoch`)
+  u64* d_slice = nullptr;   // equal-E partition: per-chunk candidate sums (SLICE_CHUNKS)
+  bool use_equal_e = true;  // GSM_EQUAL_ROWS=1: partition the first table by rows
   u32* hd_stage = nullptr;  // device alias of h_stage (zero-copy results)
   u32* hd_rows = nullptr;   // = hd_stage + STAGE_HEAD
   u32* h_stage = nullptr;  // pinned host copy
@@ -1954,6 +2043,9 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(cuda_error(e, "cudaStreamCreate"));
   if ((e = cudaMalloc(&c->d_ctr, 16)) != cudaSuccess) return fail(cuda_error(e, "cudaMalloc(epoch counter)"));
+  if ((e = cudaMalloc(&c->d_slice, sizeof(u64) * SLICE_CHUNKS)) != cudaSuccess)
+    return fail(cuda_error(e, "cudaMalloc(slice sums)"));
+  c->use_equal_e = !getenv("GSM_EQUAL_ROWS");
   if ((e = cudaMemset(c->d_ctr, 0, 16)) != cudaSuccess) return fail(cuda_error(e, "cudaMemset"));
   if ((e = cudaMalloc(&c->d_block, sizeof(QueryBlock))) != cudaSuccess)
     return fail(cuda_error(e, "cudaMalloc(query block)"));
@@ -1983,6 +2075,12 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   return GSM_OK;
 }
 
+gsm_status gsm_context_stream(gsm_context* c, uint64_t* stream) {
+  if (!c || !stream) return set_error(GSM_ERR_VALUE, "null context or output");
+  *stream = (uint64_t)(uintptr_t)c->stream;
+  return GSM_OK;
+}
+
 gsm_status gsm_context_free(gsm_context* c) {
   if (!c) return GSM_OK;
   cudaSetDevice(c->device);
@@ -1992,6 +2090,7 @@ gsm_status gsm_context_free(gsm_context* c) {
   if (c->d_status) cudaFree(c->d_status);
   if (c->d_block) cudaFree(c->d_block);
   if (c->d_ctr) cudaFree(c->d_ctr);
+  if (c->d_slice) cudaFree(c->d_slice);
   if (c->h_block) cudaFreeHost(c->h_block);
   if (c->d_slots) cudaFree(c->d_slots);
   if (c->d_chunks) cudaFree(c->d_chunks);
@@ -2189,6 +2288,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   Home g_in_home = H_NONE;
   std::vector<int> group_id(n, -1);
   int n_groups = 0;
+  Orient slice_R{};  // the first join's orientation / left key column: equal-E partition
+  int slice_key = -1;
   for (int s = 1; s < n; s++) {
     const gsm_pattern& p = steps[s];
     std::vector<int> rs = pattern_schema(p);
@@ -2274,6 +2375,10 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
         e.O = dT + L.out;
         e.st = dS + s;
         L.fanout = (on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid]).max_run;
+        if (s == 1) {
+          slice_R = e.R;
+          slice_key = e.li;
+        }
       } else {
         L.kind = S_FILTER;
         L.out = ex.new_table(a, oh);
@@ -2292,6 +2397,10 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           bool on_s = jv[0] == p.s_var;
           f.R = on_s ? m->so : m->os;
           f.lj = index_of(schema, on_s ? p.o_var : p.s_var);
+          if (s == 1) {
+            slice_R = f.R;
+            slice_key = f.li;
+          }
         } else if (sv && ov) {  // R4 (?x p ?x)
           f.mode = F_SELF;
           f.R = m->so;
@@ -2542,7 +2651,14 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       GSM_CUDA(cudaGetLastError());
       nk++;
     }
-    if (parts > 1) {
+    if (parts > 1 && slice_key >= 0 && c->d_slice && c->use_equal_e) {
+      const i64 nch = std::min<i64>(ex.ub[ex.plan[0].out_table], SLICE_CHUNKS);
+      GSM_CUDA(launch(c->use_pdl, k_slice_sums, (int)std::max<i64>(1, std::min<i64>(c->grid_ts, (nch + 7) / 8)),
+                      256, st, (const DTable*)(dT + ex.plan[0].out_table), slice_key, slice_R, c->d_slice));
+      GSM_CUDA(launch(c->use_pdl, k_slice_pick, 1, 1024, st, dT + ex.plan[0].out_table,
+                      (int)ex.plan[0].schema.size(), part, parts, dS + 0, (const u64*)c->d_slice));
+      nk += 2;
+    } else if (parts > 1) {
       GSM_CUDA(launch(c->use_pdl, k_slice, 1, 64, st, dT + ex.plan[0].out_table,
                       (int)ex.plan[0].schema.size(), part, parts, dS + 0));
       nk++;

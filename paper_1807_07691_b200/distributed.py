@@ -115,6 +115,9 @@ def execute_distributed(query, plan, store, mode: str = "gpu", row_budget: int =
             secs = local_rep.steps[i].seconds if i < len(local_rep.steps) else 0.0
             report.steps.append(StepReport(text, int(step_rows[i]), int(step_e[i]), secs))
         report.kinds = list(kinds)
+        if isinstance(report, ExecutionReport):
+            report.fused = list(local_rep.fused)
+            report.arities = list(local_rep.arities)
 
     if not gather:
         return BindingTable(tuple(query.projection), array=rows)

@@ -115,6 +115,9 @@ class ExecutionReport:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     kernels: int = 0
+    exchanged_bytes: int = 0  # multi-GPU: bytes this rank sent to its peers
+    collectives: int = 0
+    host_syncs: int = 0
 
     @property
     def intermediate_total(self) -> int:

@@ -196,12 +196,51 @@ def shard_owner(ids: np.ndarray, node_count: int, shards: int) -> np.ndarray:
     return np.minimum(o, shards - 1).astype(np.int64)
 
 
+def shard_id_range(index: int, shards: int, node_count: int) -> tuple[int, int]:
+    """The ids [lo, hi) that shard ``index`` owns (the inverse of
+    :func:`shard_owner`: owner(id) >= i  <=>  id - 1 >= ceil(i * N / n))."""
+    lo = 0 if index == 0 else -(-index * node_count // shards) + 1
+    hi = (1 << 64) - 1 if index == shards - 1 else -(-(index + 1) * node_count // shards) + 1
+    return lo, hi
+
+
+def _key_bound(pairs: np.ndarray, key: int) -> int:
+    """First row whose key column is >= key, by binary search on the mapped
+    file itself (a few page reads; np.searchsorted would copy the strided
+    key column, i.e. read the whole file)."""
+    lo, hi = 0, pairs.shape[0]
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if int(pairs[mid, 0]) < key:
+            lo = mid + 1
+        else:
+            hi = mid
+    return lo
+
+
+def _read_shard(path: Path, lo: int, hi: int) -> np.ndarray:
+    """The rows of a key-sorted pair file whose key lies in [lo, hi): one
+    contiguous byte range, read with a single pread."""
+    mm = _read_pairs(path, lazy=True)
+    a, b = _key_bound(mm, lo), _key_bound(mm, hi)
+    out = np.empty((b - a, 2), dtype=np.uint64)
+    if b > a:
+        with open(path, "rb") as fh:
+            fh.seek(16 * a)
+            got = fh.readinto(memoryview(out).cast("B"))
+        if got != 16 * (b - a):
+            raise StoreFormatError(f"short read of {path}")
+        out = out.astype("<u8", copy=False)
+    return out
+
+
 def load(directory: Path | str, device: int = 0, shard: tuple[int, int] | None = None) -> DeviceStore:
     """storage.load (storage.py:222-271) into device memory.
 
     ``shard=(i, n)`` keeps only shard i of n (SURVEY.md §8(e) sharded mode):
     the CSR rows of subjects and the CSC rows of objects whose ids fall in
-    range i (:func:`shard_owner`).  Validation and ``stats`` are global, so
+    range i (:func:`shard_owner`), read as one byte range per pair file
+    (:func:`_read_shard`), so a rank reads ~1/n of the store.  Validation and ``stats`` are global, so
     every shard plans a query identically."""
     if shard is not None and not (0 <= shard[0] < shard[1]):
         raise ValueError(f"bad shard {shard}")
@@ -241,8 +280,8 @@ def load(directory: Path | str, device: int = 0, shard: tuple[int, int] | None =
         if not so_path.exists() or not os_path.exists():
             raise StoreFormatError(f"missing pair files for predicate {pid}")
         files[pid] = (so_path, os_path)
-        so = _read_pairs(so_path, lazy=shard is None)
-        os_ = _read_pairs(os_path, lazy=shard is None)
+        so = _read_pairs(so_path, lazy=True)
+        os_ = _read_pairs(os_path, lazy=True)
         if so.shape[0] != stats[pid].cardinality:
             raise StoreFormatError(
                 f"{so_path}: {so.shape[0]} pairs but stats declares {stats[pid].cardinality}"
@@ -251,8 +290,11 @@ def load(directory: Path | str, device: int = 0, shard: tuple[int, int] | None =
             raise StoreFormatError(f"{os_path}: {os_.shape[0]} pairs but {so_path} has {so.shape[0]}")
         total += so.shape[0]
         if shard is not None:
-            so = so[shard_owner(so[:, 0], node_count, shard[1]) == shard[0]]
-            os_ = os_[shard_owner(os_[:, 0], node_count, shard[1]) == shard[0]]
+            # the files are sorted by key, so a shard's rows are ONE byte
+            # range of each file: only that range is read
+            lo, hi = shard_id_range(shard[0], shard[1], node_count)
+            so = _read_shard(so_path, lo, hi)
+            os_ = _read_shard(os_path, lo, hi)
         matrices[pid] = PairMatrix(pid, so, os_)
     if total != triple_count:
         raise StoreFormatError(f"meta declares {triple_count} triples but store holds {total}")
