@@ -921,6 +921,37 @@ __device__ __forceinline__ bool gfilter(const FSpec& f, const DTable& s, int a, 
   return keep;
 }
 
+// A post filter whose lookup key is a LEFT column (kc < a) searches the same
+// segment for every candidate of the row: with the target being the
+// candidate (F_PAIR, tc == a) the filter is a sorted-run INTERSECTION of the
+// expand's run and that segment.  The long-row path looks such segments up
+// once per row (HOIST of them, in shared memory) instead of per candidate.
+constexpr int HOIST = 2;
+__device__ __forceinline__ bool gpost_h(const GroupP& p, const DTable& s, i64 r, u32 cand,
+                                        const uint2* rsg, i64* acc) {
+  for (int i = p.npre; i < p.npre + p.npost; i++) {
+    const FSpec& f = p.f[i];
+    const int h = i - p.npre;
+    uint2 sg;
+    u32 key = 0;
+    if (h < HOIST && f.kc < p.a) {
+      sg = rsg[h];
+    } else {
+      key = vcol(s, p.a, f.kc, r, cand);
+      sg = seg_lookup(f.R, key);
+    }
+    if (f.mode == F_SELF && f.kc < p.a) key = __ldg(s.col[f.kc] + r);
+    const u32 target = f.mode == F_PAIR ? vcol(s, p.a, f.tc, r, cand) : f.mode == F_CONST ? f.cval : key;
+    const bool keep = sg.y && sorted_contains(f.R.dst + sg.x, sg.y, target);
+    if (acc) {
+      acc[2 * f.slot] += f.mode == F_PAIR ? (i64)sg.y : (i64)keep;
+      acc[2 * f.slot + 1] += keep;
+    }
+    if (!keep) return false;
+  }
+  return true;
+}
+
 __device__ __forceinline__ bool gpost(const GroupP& p, const DTable& s, i64 r, u32 cand,
                                       i64* acc) {
   for (int i = p.npre; i < p.npre + p.npost; i++)
@@ -934,6 +965,7 @@ __device__ __forceinline__ bool gpost(const GroupP& p, const DTable& s, i64 r, u
 // filter instead of one per (candidate, filter).  Same per-step counters as
 // evaluating gpost candidate by candidate.  Returns the survivor bit mask.
 constexpr int GP_BATCH = 4;
+constexpr int GSURV = 1024;  // survivors of a tile's long rows kept from the count pass
 static_assert(GP_BATCH >= (int)FUSE_MAX_FANOUT, "fused post filters must fit one batch");
 __device__ __forceinline__ u32 gpost_batch(const GroupP& p, const DTable& s, i64 r, u32 aux, u32 len,
                                            i64* acc) {
@@ -999,6 +1031,13 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
   __shared__ int s_long[TS_TILE];
   __shared__ int s_nlong;
   __shared__ DTable s_in;
+  // long rows with post filters: flattened candidate prefix, hoisted
+  // segments, survivor counts, and the survivors themselves (when they fit)
+  __shared__ u32 s_lpre[TS_TILE + 1];
+  __shared__ uint2 s_rsg[TS_TILE][HOIST];
+  __shared__ u32 s_lcnt[TS_TILE];
+  __shared__ uint2 s_surv[GSURV];
+  __shared__ u32 s_nsurv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   i64 acc[2 * MAXGS];  // this thread's (E, rows) contribution to each fused step
   for (int k = 0; k < 2 * MAXGS; k++) acc[k] = 0;
@@ -1052,8 +1091,8 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
           len = sg.y;
           acc[2 * p.xslot] += len;
           acc[2 * p.xslot + 1] += len;
-          if (len >= WARP_ROW) {
-            warp_row = true;  // counted (if filtered) and emitted by a warp
+          if (len >= WARP_ROW || (p.npost && len > (u32)GP_BATCH)) {
+            warp_row = true;  // counted (if filtered) by the block, emitted by a warp / the block
             cnt = p.npost ? 0u : len;
           } else if (p.npost == 0) {
             cnt = len;
@@ -1074,16 +1113,58 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
     s_pre[tid] = cnt;
     if (warp_row) s_long[atomicAdd(&s_nlong, 1)] = tid;
     __syncthreads();
-    if (p.npost) {  // warp-cooperative counting of long candidate lists
-      for (int q = warp; q < s_nlong; q += TS_THREADS / 32) {
-        const int rl = s_long[q];
-        const u32 L = s_len[rl], ax = s_aux[rl];
-        u32 c = 0;
-        for (u32 j = lane; j < L; j += 32) c += gpost(p, s_in, base + rl, __ldg(p.X.dst + ax + j), s_acc);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) s_pre[rl] = c;
+    const int nlong = s_nlong;
+    bool surv_ok = true;
+    if (p.npost && nlong) {
+      // Block-cooperative counting of the long rows: their candidates form
+      // one flattened index space that all 256 threads stride over (a hub
+      // row is spread over the whole block, not one warp), with each row's
+      // row-invariant filter segments looked up once.  Survivors are kept
+      // (row, candidate) in shared memory when they fit, so the emit pass
+      // does not evaluate the filters again.
+      u32 myl = 0;
+      if (tid < nlong) {
+        const int rl = s_long[tid];
+        myl = s_len[rl];
+        s_lcnt[tid] = 0;
+        for (int h = 0; h < HOIST && h < p.npost; h++) {
+          const FSpec& f = p.f[p.npre + h];
+          if (f.kc < p.a) s_rsg[tid][h] = seg_lookup(f.R, __ldg(s_in.col[f.kc] + base + rl));
+        }
       }
+      u32 xs = myl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, xs, o);
+        if (lane >= o) xs += y;
+      }
+      if (lane == 31) s_wsum[warp] = xs;
+      if (tid == 0) s_nsurv = 0;
+      __syncthreads();
+      u32 runl = xs - myl;
+      for (int w = 0; w < warp; w++) runl += (u32)s_wsum[w];
+      if (tid < nlong) s_lpre[tid] = runl;
+      if (tid == nlong - 1) s_lpre[nlong] = runl + myl;
+      __syncthreads();
+      const u32 tl = s_lpre[nlong];
+      for (u32 f = tid; f < tl; f += TS_THREADS) {
+        int lo = 0, hi = nlong - 1;  // last q with s_lpre[q] <= f
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_lpre[mid] <= f) lo = mid;
+          else hi = mid - 1;
+        }
+        const int rl = s_long[lo];
+        const u32 cand = __ldg(p.X.dst + s_aux[rl] + (f - s_lpre[lo]));
+        if (gpost_h(p, s_in, base + rl, cand, s_rsg[lo], s_acc)) {
+          atomicAdd(&s_lcnt[lo], 1u);
+          const u32 k = atomicAdd(&s_nsurv, 1u);
+          if (k < GSURV) s_surv[k] = make_uint2((u32)lo, cand);
+        }
+      }
+      __syncthreads();
+      if (tid < nlong) s_pre[s_long[tid]] = s_lcnt[tid];
+      surv_ok = s_nsurv <= GSURV;
       __syncthreads();
     }
     trace_at(it, 2);
@@ -1121,7 +1202,35 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
           if ((mask >> j) & 1u) gwrite(p, s_in, r, __ldg(p.X.dst + aux + j), pos++);
       }
     }
-    for (int q = warp; q < s_nlong; q += TS_THREADS / 32) {
+    if (p.npost && nlong) {
+      // long rows with post filters: positions inside a row by a shared
+      // cursor (row order is not contractual), the survivors
+      // from the count pass, or -- when they did not fit -- re-evaluated
+      if (tid < nlong) s_lcnt[tid] = 0;
+      __syncthreads();
+      if (surv_ok) {
+        for (u32 k = tid; k < s_nsurv; k += TS_THREADS) {
+          const uint2 sv = s_surv[k];
+          const int rl = s_long[sv.x];
+          gwrite(p, s_in, base + rl, sv.y, gbase + s_pre[rl] + atomicAdd(&s_lcnt[sv.x], 1u));
+        }
+      } else {
+        const u32 tl = s_lpre[nlong];
+        for (u32 f = tid; f < tl; f += TS_THREADS) {
+          int lo = 0, hi = nlong - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_lpre[mid] <= f) lo = mid;
+            else hi = mid - 1;
+          }
+          const int rl = s_long[lo];
+          const u32 cand = __ldg(p.X.dst + s_aux[rl] + (f - s_lpre[lo]));
+          if (gpost_h(p, s_in, base + rl, cand, s_rsg[lo], nullptr))
+            gwrite(p, s_in, base + rl, cand, gbase + s_pre[rl] + atomicAdd(&s_lcnt[lo], 1u));
+        }
+      }
+    }
+    for (int q = warp; q < s_nlong && !p.npost; q += TS_THREADS / 32) {
       const int rl = s_long[q];
       const u32 L = s_len[rl], ax = s_aux[rl];
       i64 pos = gbase + s_pre[rl];
@@ -1758,6 +1867,7 @@ struct gsm_context {
   u32* d_ctr = nullptr;     // device epoch counter (mirrored by `epoch`)
   u64* d_slice = nullptr;   // equal-E partition: per-chunk candidate sums (SLICE_CHUNKS)
   bool use_equal_e = true;  // GSM_EQUAL_ROWS=1: partition the first table by rows
+  bool use_intersect = true;  // GSM_NO_INTERSECT=1: no fusion of intersection-shaped filters
   u32* hd_stage = nullptr;  // device alias of h_stage (zero-copy results)
   u32* hd_rows = nullptr;   // = hd_stage + STAGE_HEAD
   u32* h_stage = nullptr;  // pinned host copy
@@ -2046,6 +2156,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if ((e = cudaMalloc(&c->d_slice, sizeof(u64) * SLICE_CHUNKS)) != cudaSuccess)
     return fail(cuda_error(e, "cudaMalloc(slice sums)"));
   c->use_equal_e = !getenv("GSM_EQUAL_ROWS");
+  c->use_intersect = !getenv("GSM_NO_INTERSECT");
   if ((e = cudaMemset(c->d_ctr, 0, 16)) != cudaSuccess) return fail(cuda_error(e, "cudaMemset"));
   if ((e = cudaMalloc(&c->d_block, sizeof(QueryBlock))) != cudaSuccess)
     return fail(cuda_error(e, "cudaMalloc(query block)"));
@@ -2060,11 +2171,17 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
     return fail(cuda_error(e, "cudaEventCreate"));
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
+  // Default arena: 16x the store (64 MB .. 4 GB, at most a quarter of the
+  // free memory); a query that outgrows it grows it and re-runs, so a small
+  // store's context is cheap to create (the reference's test suites build
+  // hundreds of tiny stores).  The staging buffer likewise starts at 2 MB
+  // and grows with the results.
+  const size_t by_store = std::max<size_t>((size_t)64 << 20, (size_t)store->bytes * 16);
   size_t want = arena_bytes > 0 ? (size_t)arena_bytes
-                                : std::min<size_t>((size_t)1 << 32, free_b / 4);
+                                : std::min<size_t>(std::min<size_t>((size_t)1 << 32, free_b / 4), by_store);
   gsm_status st = ctx_set_arena(c, want);
   if (st != GSM_OK) return fail(st);
-  st = ctx_set_stage(c, std::min<size_t>((size_t)64 << 20, c->stage_max));
+  st = ctx_set_stage(c, std::min<size_t>((size_t)2 << 20, c->stage_max));
   if (st != GSM_OK) return fail(st);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tilescan<ExpandP>, TS_THREADS, 0);
@@ -2286,6 +2403,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   u32 g_x_fanout = 0;  // longest candidate list of the group's expand
   i64 g_x_avg = 0, g_x_est = 0;  // its average run, expected output rows
   Home g_in_home = H_NONE;
+  int g_x_var = -1;    // the variable the group's expand binds
   std::vector<int> group_id(n, -1);
   int n_groups = 0;
   Orient slice_R{};  // the first join's orientation / left key column: equal-E partition
@@ -2337,9 +2455,13 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       bool join = false;
       if (c->use_fusion && g_open) {
         if (is_expand) join = !g_has_x;
-        else if (g_has_x)  // short runs, or an intermediate too large to materialise well
+        else if (g_has_x)  // short runs, or an intermediate too large to materialise well,
+                           // or a filter whose key is bound before the expand: a sorted-run
+                           // intersection per row (its segment looked up once per row)
           join = g_npost < MAXF && (g_x_fanout <= FUSE_MAX_FANOUT ||
-                                    (g_x_est >= c->fuse_huge && g_x_fanout <= 64 * std::max<i64>(1, g_x_avg)));
+                                    (g_x_est >= c->fuse_huge && g_x_fanout <= 64 * std::max<i64>(1, g_x_avg)) ||
+                                    (c->use_intersect && g_npost < HOIST && jv[0] != g_x_var &&
+                                     g_x_fanout < (1u << 23)));
         else join = g_npre < MAXF;
       }
       if (!join) {
@@ -2351,6 +2473,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       }
       if (is_expand) {
         g_has_x = true;
+        g_x_var = jv[0] == p.s_var ? p.o_var : p.s_var;
         const bool on_s = jv[0] == p.s_var;
         const HostAux& gha = on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid];
         g_x_fanout = gha.max_run;
@@ -2621,7 +2744,9 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     d_image = S.pre_image;
   } else if (graphs) {
     GSM_CUDA(cudaMalloc(&d_image, sizeof(QueryBlock)));
-    cudaError_t ce = cudaMemcpy(d_image, hb, used, cudaMemcpyHostToDevice);
+    // k_init copies whole 16-byte words: the tail past `used` must be defined
+    cudaError_t ce = cudaMemset(d_image, 0, sizeof(QueryBlock));
+    if (ce == cudaSuccess) ce = cudaMemcpy(d_image, hb, used, cudaMemcpyHostToDevice);
     if (ce != cudaSuccess) {
       cudaFree(d_image);
       return cuda_error(ce, "cudaMemcpy(query image)");
@@ -3212,7 +3337,8 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
         if (p) cudaFree(p);
     };
     for (int i = 0; i < n; i++)
-      if (cudaMalloc(&imgs[i], sizeof(QueryBlock)) != cudaSuccess) {
+      if (cudaMalloc(&imgs[i], sizeof(QueryBlock)) != cudaSuccess ||
+          cudaMemset(imgs[i], 0, sizeof(QueryBlock)) != cudaSuccess) {
         cudaGetLastError();
         drop_imgs();
         return false;

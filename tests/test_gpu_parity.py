@@ -245,10 +245,10 @@ def test_expand_layouts_vs_oracle(store_factory):
 
 def test_execution_variants_agree(store_factory):
     """Graph replay, programmatic dependent launch, step fusion and hub
-    deferral and projection fusion are pure optimisations: each query gives
-    the same bag and the same per-step report with them switched off
-    (GSM_NO_GRAPHS / GSM_NO_PDL / GSM_NO_FUSION / GSM_NO_DEFER /
-    GSM_NO_PROJ_FUSION), a tiny staging buffer (GSM_STAGE_MAX) forces the
+    deferral, projection fusion and the fused run intersection are pure
+    optimisations: each query gives the same bag and the same per-step report
+    with them switched off (GSM_NO_GRAPHS / GSM_NO_PDL / GSM_NO_FUSION /
+    GSM_NO_DEFER / GSM_NO_PROJ_FUSION / GSM_NO_INTERSECT), a tiny staging buffer (GSM_STAGE_MAX) forces the
     device-resident result paths, and repeated (replayed) executions agree."""
     import json
     import os
@@ -285,7 +285,7 @@ def test_execution_variants_agree(store_factory):
     # result, no k_pack) and DISTINCT / sizes above the zero-copy limit take
     # the device paths
     for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION", "GSM_NO_DEFER",
-                    "GSM_NO_PROJ_FUSION", "GSM_NO_BATCH_GRAPH", "GSM_STAGE_MAX=65536", "GSM_TILE_ITEMS=2", "GSM_FUSE_HUGE=1",
+                    "GSM_NO_PROJ_FUSION", "GSM_NO_BATCH_GRAPH", "GSM_STAGE_MAX=65536", "GSM_TILE_ITEMS=2", "GSM_FUSE_HUGE=1", "GSM_NO_INTERSECT",
                     "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER,GSM_NO_PROJ_FUSION"):
         env = dict(os.environ)
         for item in filter(None, variant.split(",")):
