@@ -43,7 +43,10 @@ typedef enum {
   GSM_ERR_CUDA = 5,            /* driver/runtime failure                                */
   GSM_ERR_UNSORTED = 6,        /* ValueError "pair list not sorted" (storage.py:44-45)  */
   GSM_ERR_UNKNOWN_ID = 7,      /* UnknownIdError: decode of an absent id (dictionary.py:84-87) */
-  GSM_ERR_PARSE = 8            /* ParseError "line N: ..." (qparser.py:80-92)            */
+  GSM_ERR_PARSE = 8,           /* ParseError "line N: ..." (qparser.py:80-92)            */
+  GSM_ERR_DEVICE_MEMORY = 9    /* ResourceLimitError subclass: an intermediate table does
+                                  not fit device memory even after growing the arena; the
+                                  host re-runs the plan in left-row chunks (part/parts)   */
 } gsm_status;
 
 typedef struct gsm_store gsm_store;
@@ -155,6 +158,12 @@ gsm_status gsm_context_free(gsm_context* ctx);
  * host synchronisation between the library's launches and its own. */
 gsm_status gsm_context_stream(gsm_context* ctx, uint64_t* stream);
 
+/* Largest arena (bytes) the context can grow to: 90% of the free device
+ * memory plus its current arena, capped by GSM_ARENA_MAX.  An intermediate
+ * table of R rows x k columns needs 8*R*k bytes of it (two halves); larger
+ * plans fail with GSM_ERR_DEVICE_MEMORY and are run in left-row chunks. */
+gsm_status gsm_context_capacity(gsm_context* ctx, int64_t* bytes);
+
 /* Replaces executor.execute (executor.py:296-368) for mode="gpu":
  * evaluates `n_steps` patterns in plan order as a left-deep chain of SM-based
  * joins on the device, then projects onto `proj` (variable indices, n_proj of
@@ -264,8 +273,17 @@ gsm_status gsm_result_shape(const gsm_result* res, int64_t* n_rows, int32_t* n_c
  * gsm_execute on the same context (else GSM_ERR_VALUE). */
 gsm_status gsm_result_copy(const gsm_result* res, uint32_t* host_rows);
 
-/* Device pointer of the row-major result (valid until gsm_result_free). */
+/* Device pointer of the row-major result (valid until gsm_result_free, or
+ * until the next gsm_execute on the context for results left in its arena
+ * because no separate buffer could be allocated). */
 gsm_status gsm_result_device_ptr(const gsm_result* res, uint64_t* device_ptr);
+
+/* Order-independent multiset fingerprint of the result rows, computed on the
+ * device without copying the rows to the host: out[0] = rows, out[1] = sum,
+ * out[2] = xor of the per-row splitmix64 chain over the row's ids (the
+ * summary a left-row-chunked evaluation reports when the whole result would
+ * not fit host memory; executor.execute_summary). */
+gsm_status gsm_result_fingerprint(const gsm_result* res, uint64_t* out);
 
 gsm_status gsm_result_free(gsm_result* res);
 

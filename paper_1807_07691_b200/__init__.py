@@ -7,6 +7,7 @@ as a chain of sm_100a CUDA kernels and returns a ``BindingTable``.
 """
 
 from .errors import (
+    DeviceMemoryError,
     GsmatError,
     ParseError,
     ResourceLimitError,
@@ -19,9 +20,12 @@ from .executor import (
     DEFAULT_ROW_BUDGET,
     BindingTable,
     ExecutionReport,
+    ResultSummary,
     StepReport,
     execute,
     execute_batch,
+    execute_summary,
+    fingerprint_rows,
 )
 from .frontend import Plan, QueryGraph, TriplePattern, bind_constants, make_plan, parse_query
 from .decode import decode_rows, format_term, result_tsv, write_tsv
@@ -46,6 +50,7 @@ __all__ = [
     "DeviceStore",
     "ExecutionReport",
     "GsmatError",
+    "DeviceMemoryError",
     "ParseError",
     "Plan",
     "QueryGraph",
@@ -60,6 +65,9 @@ __all__ = [
     "bind_constants",
     "execute",
     "execute_batch",
+    "execute_summary",
+    "fingerprint_rows",
+    "ResultSummary",
     "from_store",
     "load",
     "make_plan",

@@ -25,6 +25,7 @@ GSM_ERR_CUDA = 5
 GSM_ERR_UNSORTED = 6
 GSM_ERR_UNKNOWN_ID = 7
 GSM_ERR_PARSE = 8
+GSM_ERR_DEVICE_MEMORY = 9
 
 GSM_BUDGET_SEQUENTIAL = 0
 GSM_BUDGET_PARALLEL = 1
@@ -65,6 +66,8 @@ EXPORTS = (
     "gsm_ntriples_parse",
     "gsm_build_store",
     "gsm_sort_triples",
+    "gsm_context_capacity",
+    "gsm_result_fingerprint",
 )
 
 
@@ -156,6 +159,7 @@ def lib() -> C.CDLL:
             "gsm_context_create": (i32, [vp, i64, P(vp)]),
             "gsm_context_free": (i32, [vp]),
             "gsm_context_stream": (i32, [vp, P(C.c_uint64)]),
+            "gsm_context_capacity": (i32, [vp, P(i64)]),
             "gsm_execute": (
                 i32,
                 [vp, P(Pattern), i32, P(i32), i32, i32, i64, i32, i64, i64, P(Report), P(vp)],
@@ -176,6 +180,7 @@ def lib() -> C.CDLL:
             "gsm_result_copy": (i32, [vp, vp]),
             "gsm_result_device_ptr": (i32, [vp, P(C.c_uint64)]),
             "gsm_result_free": (i32, [vp]),
+            "gsm_result_fingerprint": (i32, [vp, P(C.c_uint64)]),
             "gsm_results_shape": (i32, [P(vp), i32, P(i64), P(i32)]),
             "gsm_results_copy": (i32, [P(vp), i32, P(vp), i32]),
             "gsm_last_error": (C.c_char_p, []),
@@ -202,6 +207,8 @@ def check(status: int) -> None:
 
 
 def raise_status(status: int, msg: str) -> None:
+    if status == GSM_ERR_DEVICE_MEMORY:
+        raise errors.DeviceMemoryError(msg)
     if status == GSM_ERR_RESOURCE:
         raise errors.ResourceLimitError(msg)
     if status == GSM_ERR_STORE_FORMAT:

@@ -1,4 +1,5 @@
 // gsm_api.cu — error plumbing, device queries, result handles.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -27,6 +28,44 @@ gsm_status cuda_error(cudaError_t e, const char* what) {
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 }  // namespace gsm
+
+namespace {
+
+// Multiset fingerprint of n row-major k-column rows: per row the splitmix64
+// chain h = mix(h ^ id) from h0 = golden ratio, then sum and xor over rows
+// (wrapping).  Rows are read with warp-contiguous loads: a warp walks 32
+// consecutive rows, so its k strided loads cover one contiguous 128*k-byte
+// span.  Reads host-mapped (staged) rows through UVA as well.
+__device__ __forceinline__ u64 fp_mix(u64 h, u32 v) {
+  u64 z = (h ^ (u64)v) + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) k_fingerprint(const u32* __restrict__ rows, i64 n, int k,
+                                                     unsigned long long* __restrict__ out) {
+  u64 s = 0, x = 0;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const u32* row = rows + r * k;
+    u64 h = 0x9E3779B97F4A7C15ull;
+    for (int c = 0; c < k; c++) h = fp_mix(h, __ldg(row + c));
+    s += h;
+    x ^= h;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    x ^= __shfl_xor_sync(0xffffffffu, x, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out + 1, (unsigned long long)s);
+    atomicXor(out + 2, (unsigned long long)x);
+  }
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -62,8 +101,11 @@ gsm_status gsm_result_copy(const gsm_result* res, uint32_t* host_rows) {
     memcpy(host_rows, res->staged, bytes);
     return GSM_OK;
   }
+  if (res->dev_view && gsm::context_generation(res->ctx) != res->gen)
+    return gsm::set_error(GSM_ERR_VALUE, "result invalidated by a later gsm_execute on its context");
   GSM_CUDA(cudaSetDevice(res->device));
-  GSM_CUDA(cudaMemcpy(host_rows, res->rows, bytes, cudaMemcpyDeviceToHost));
+  GSM_CUDA(cudaMemcpy(host_rows, res->dev_view ? res->dev_view : res->rows, bytes,
+                      cudaMemcpyDeviceToHost));
   return GSM_OK;
 }
 
@@ -80,7 +122,51 @@ gsm_status gsm_result_device_ptr(const gsm_result* res, uint64_t* device_ptr) {
     *device_ptr = (uint64_t)(uintptr_t)d;
     return GSM_OK;
   }
+  if (res->dev_view) {
+    if (gsm::context_generation(res->ctx) != res->gen)
+      return gsm::set_error(GSM_ERR_VALUE, "result invalidated by a later gsm_execute on its context");
+    *device_ptr = (uint64_t)(uintptr_t)res->dev_view;
+    return GSM_OK;
+  }
   *device_ptr = (uint64_t)(uintptr_t)res->rows;
+  return GSM_OK;
+}
+
+gsm_status gsm_result_fingerprint(const gsm_result* res, uint64_t* out) {
+  if (!res || !out) return gsm::set_error(GSM_ERR_VALUE, "null result");
+  out[0] = (uint64_t)res->n;
+  out[1] = out[2] = 0;
+  if (res->n == 0) return GSM_OK;
+  if (res->k == 0) {  // every row is the empty tuple: h = h0
+    const u64 h0 = 0x9E3779B97F4A7C15ull;
+    out[1] = h0 * (u64)res->n;
+    out[2] = (res->n & 1) ? h0 : 0;
+    return GSM_OK;
+  }
+  const u32* rows = res->rows;
+  if (res->staged || res->dev_view) {
+    if (gsm::context_generation(res->ctx) != res->gen)
+      return gsm::set_error(GSM_ERR_VALUE, "result invalidated by a later gsm_execute on its context");
+    rows = res->staged ? res->staged : res->dev_view;
+  }
+  GSM_CUDA(cudaSetDevice(res->device));
+  unsigned long long* d = nullptr;
+  GSM_CUDA(cudaMalloc(&d, 3 * sizeof(unsigned long long)));
+  cudaError_t e = cudaMemset(d, 0, 3 * sizeof(unsigned long long));
+  if (e == cudaSuccess) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, res->device);
+    const i64 blocks = std::min<i64>((i64)sms * 8, (res->n + 255) / 256);
+    k_fingerprint<<<(unsigned)blocks, 256>>>(rows, res->n, res->k, d);
+    gsm::count_launch();
+    e = cudaGetLastError();
+  }
+  unsigned long long h[3] = {0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return gsm::cuda_error(e, "gsm_result_fingerprint");
+  out[1] = h[1];
+  out[2] = h[2];
   return GSM_OK;
 }
 

@@ -1891,6 +1891,7 @@ struct gsm_context {
   // fused kernel) (GSM_FUSE_HUGE)
   i64 fuse_huge = (i64)1 << 25;
   size_t stage_max = (size_t)1 << 30;  // the staging buffer grows up to this (GSM_STAGE_MAX)
+  size_t arena_max = ~(size_t)0;       // the arena grows up to this (GSM_ARENA_MAX)
   // A prepared plan: the captured launch sequence plus what the host needs
   // to replay and complete it without re-planning.
   struct GraphEntry {
@@ -1965,6 +1966,7 @@ gsm_status ctx_set_arena(gsm_context* c, size_t bytes) {
     c->d_status = nullptr;
   }
   bytes = (bytes + 255) & ~(size_t)255;
+  c->gen++;  // results left in the old arena expire
   GSM_CUDA(cudaMalloc(&c->arena, bytes));
   c->arena_bytes = bytes;
   size_t half = bytes / 2;
@@ -2145,6 +2147,9 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* fh = getenv("GSM_FUSE_HUGE")) c->fuse_huge = std::max<i64>(1, atoll(fh));
   if (const char* ti = getenv("GSM_TILE_ITEMS")) c->tile_items = std::min(2, std::max(0, atoi(ti)));
   if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
+  // cap on the arena (bytes): below it a plan is evaluated in left-row
+  // chunks by the host (tests force chunking on small stores with it)
+  if (const char* am = getenv("GSM_ARENA_MAX")) c->arena_max = std::max<size_t>(1 << 20, strtoull(am, nullptr, 10));
   auto fail = [&](gsm_status st) {
     gsm_context_free(c);
     return st;
@@ -2179,7 +2184,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   const size_t by_store = std::max<size_t>((size_t)64 << 20, (size_t)store->bytes * 16);
   size_t want = arena_bytes > 0 ? (size_t)arena_bytes
                                 : std::min<size_t>(std::min<size_t>((size_t)1 << 32, free_b / 4), by_store);
-  gsm_status st = ctx_set_arena(c, want);
+  gsm_status st = ctx_set_arena(c, std::min(want, c->arena_max));
   if (st != GSM_OK) return fail(st);
   st = ctx_set_stage(c, std::min<size_t>((size_t)2 << 20, c->stage_max));
   if (st != GSM_OK) return fail(st);
@@ -2189,6 +2194,17 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   c->grid_ts = sms * std::max(1, std::min(occ, 4));
   *out = c;
+  return GSM_OK;
+}
+
+gsm_status gsm_context_capacity(gsm_context* c, int64_t* bytes) {
+  if (!c || !bytes) return set_error(GSM_ERR_VALUE, "null context or output");
+  GSM_CUDA(cudaSetDevice(c->device));
+  size_t free_b = 0, total_b = 0;
+  GSM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  size_t avail = free_b + c->arena_bytes;
+  if (c->arena_max != ~(size_t)0) avail = std::min(avail, c->arena_max / 9 * 10);
+  *bytes = (int64_t)((avail * 9) / 10);
   return GSM_OK;
 }
 
@@ -3083,16 +3099,20 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     size_t avail = free_b + c->arena_bytes;
-    if (attempt >= 8 || need > (avail * 9) / 10) {
-      char msg[256];
-      snprintf(msg, sizeof msg,
-               "intermediate result of %lld rows x %d columns exceeds device memory",
-               (long long)need_rows, need_arity);
-      return set_error(GSM_ERR_RESOURCE, msg);
-    }
+    if (c->arena_max != ~(size_t)0) avail = std::min(avail, c->arena_max / 9 * 10);
+    char msg[256];
+    snprintf(msg, sizeof msg, "intermediate result of %lld rows x %d columns exceeds device memory",
+             (long long)need_rows, need_arity);
+    // GSM_ERR_DEVICE_MEMORY: the host re-runs the plan in left-row chunks
+    if (attempt >= 8 || need > (avail * 9) / 10) return set_error(GSM_ERR_DEVICE_MEMORY, msg);
     grow = std::min(grow, (avail * 9) / 10);
-    gsm_status s2 = ctx_set_arena(c, grow);
-    if (s2 != GSM_OK) return s2;
+    const size_t prev = c->arena_bytes;
+    if (ctx_set_arena(c, grow) != GSM_OK) {  // fragmentation: keep the old arena
+      cudaGetLastError();
+      gsm_status s3 = ctx_set_arena(c, prev);
+      if (s3 != GSM_OK) return s3;
+      return set_error(GSM_ERR_DEVICE_MEMORY, msg);
+    }
   }
 
   const QueryBlock* hb = c->h_block;
@@ -3209,11 +3229,16 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     r->n = nrows;
     size_t bytes = (size_t)nrows * row_bytes;
     cudaError_t e = cudaMalloc(&r->rows, std::max<size_t>(bytes, 4));
-    if (e != cudaSuccess) {
-      delete r;
-      return cuda_error(e, "cudaMalloc(result)");
+    if (e == cudaSuccess) {
+      if (bytes) GSM_CUDA(cudaMemcpyAsync(r->rows, pack_out, bytes, cudaMemcpyDeviceToDevice, st));
+    } else {
+      // No room beside the arena (a left-row chunk near device capacity):
+      // the result stays where the query packed it, valid until the next
+      // gsm_execute on this context (like staged results).
+      cudaGetLastError();
+      r->rows = nullptr;
+      r->dev_view = pack_out;
     }
-    if (bytes) GSM_CUDA(cudaMemcpyAsync(r->rows, pack_out, bytes, cudaMemcpyDeviceToDevice, st));
     GSM_CUDA(cudaStreamSynchronize(st));
     if (bytes > c->stage_bytes && bytes <= c->stage_max) ctx_set_stage(c, bytes + bytes / 4);
   }

@@ -48,6 +48,7 @@ struct gsm_result {
   const gsm_context* ctx = nullptr;
   u64 gen = 0;                 // staging generation the rows belong to
   bool zc = false;             // staged rows were written to host memory only (no device copy)
+  const u32* dev_view = nullptr;  // rows left in the context's arena (not owned; valid while gen matches)
 };
 
 namespace gsm {

@@ -29,11 +29,13 @@ from __future__ import annotations
 
 import ctypes as C
 import operator
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib
+from .errors import DeviceMemoryError, ResourceLimitError
 from .storage import DeviceStore, from_store
 
 DEFAULT_ROW_BUDGET = 10**8
@@ -115,6 +117,7 @@ class ExecutionReport:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     kernels: int = 0
+    chunks: int = 0  # left-row chunks the plan ran in (0 = one pass)
     exchanged_bytes: int = 0  # multi-GPU: bytes this rank sent to its peers
     collectives: int = 0
     host_syncs: int = 0
@@ -203,13 +206,16 @@ def execute(
     report: ExecutionReport | None = None,
     *,
     partition: tuple[int, int] = (0, 1),
+    chunks: int | None = None,
 ) -> BindingTable:
     """Evaluate a plan on the GPU and project onto the query's projection.
 
     ``worker_count`` is accepted for signature compatibility (the grid is
     sized from the device).  ``partition=(i, k)`` evaluates only the i-th of
     k contiguous slices of the first step's rows (multi-GPU row partitioning,
-    see :mod:`.distributed`).
+    see :mod:`.distributed`).  A plan whose intermediate tables exceed device
+    memory is evaluated in left-row chunks (:func:`_execute_chunked`);
+    ``chunks=k`` forces at least k of them.
     """
     if mode not in _MODES:
         raise ValueError(f"unknown mode {mode!r}")
@@ -230,18 +236,259 @@ def execute(
         rep_struct, bufs = _new_report(n)
 
     L = _lib.lib()
-    res = C.c_void_p()
     part, parts = partition
+    if chunks is not None:
+        return _execute_chunked(dstore, query, steps, arr, proj_arr, nproj, budget, budget_mode,
+                                report, "rows", _pow2(chunks))
+    res = C.c_void_p()
     st = L.gsm_execute(
         dstore.context(), arr, n, proj_arr, nproj, 1 if query.distinct else 0, budget,
         budget_mode, int(part), int(parts), C.byref(rep_struct) if rep_struct is not None else None,
         C.byref(res),
     )
+    if st == _lib.GSM_ERR_DEVICE_MEMORY and (part, parts) == (0, 1):
+        return _execute_chunked(dstore, query, steps, arr, proj_arr, nproj, budget, budget_mode,
+                                report, "rows", _first_parts(dstore, _lib.last_error()))
     _lib.check(st)
     out = _fetch(L, res)
     if report is not None:
         _fill_report(report, steps, rep_struct, *bufs)
     return BindingTable(tuple(query.projection), array=out)
+
+
+@dataclass(frozen=True)
+class ResultSummary:
+    """What :func:`execute_summary` returns instead of the rows: the row
+    count and an order-independent multiset fingerprint (wrapping sum and
+    xor of a per-row splitmix64 chain over the row's ids; the same value for
+    the same bag of rows whatever their order)."""
+
+    schema: tuple
+    rows: int
+    sum: int
+    xor: int
+
+    @property
+    def fingerprint(self) -> tuple[int, int, int]:
+        return self.rows, self.sum, self.xor
+
+
+_M64 = (1 << 64) - 1
+
+
+def fingerprint_rows(a: np.ndarray) -> tuple[int, int, int]:
+    """Host-side twin of ``gsm_result_fingerprint`` for an (n, k) id array."""
+    a = np.asarray(a, dtype=np.uint64)
+    n = int(a.shape[0])
+    if n == 0:
+        return 0, 0, 0
+    with np.errstate(over="ignore"):
+        h = np.full(n, 0x9E3779B97F4A7C15, dtype=np.uint64)
+        for c in range(a.shape[1]):
+            z = (h ^ a[:, c]) + np.uint64(0x9E3779B97F4A7C15)
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            h = z ^ (z >> np.uint64(31))
+        return n, int(h.sum(dtype=np.uint64)), int(np.bitwise_xor.reduce(h))
+
+
+def execute_summary(query, plan, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW_BUDGET,
+                    report: ExecutionReport | None = None, *, chunks: int | None = None
+                    ) -> ResultSummary:
+    """Evaluate a plan like :func:`execute` but return only the result's row
+    count and multiset fingerprint, computed on the device: the rows never
+    reach the host, so results larger than host memory (a 19G-row star on a
+    power-law store) can still be answered and checked.  Plans whose
+    intermediates exceed device memory run in left-row chunks, each chunk's
+    result reduced on the device.  Budget rules and errors as in
+    :func:`execute` (on the whole plan's counters)."""
+    if mode not in _MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if not plan.steps:
+        raise ValueError("cannot execute an empty plan")
+    dstore = store if isinstance(store, DeviceStore) else from_store(store)
+    if getattr(dstore, "shard", None) is not None and dstore.shard[1] > 1:
+        raise ValueError(
+            f"store holds shard {dstore.shard} only; evaluate it with sharded.execute_sharded")
+    steps, arr, proj_arr, nproj = compile_plan(query, plan)
+    budget_mode = _budget_mode(mode)
+    budget = min(int(row_budget), (1 << 63) - 1)
+    parts0 = _pow2(chunks) if chunks is not None else 1
+    return _execute_chunked(dstore, query, steps, arr, proj_arr, nproj, budget, budget_mode,
+                            report, "summary", parts0)
+
+
+_MAX_PARTS = 4096  # the first table is cut at 1/4096-of-E granularity (k_slice_pick)
+_NO_BUDGET = (1 << 63) - 1
+
+
+def _pow2(k: int) -> int:
+    k = int(k)
+    if k < 1:
+        raise ValueError("chunks must be >= 1")
+    p = 1
+    while p < k:
+        p <<= 1
+    return min(p, _MAX_PARTS)
+
+
+def _first_parts(dstore, msg: str) -> int:
+    """Chunk count for a plan that failed with "intermediate result of R rows
+    x k columns exceeds device memory": enough chunks for 8*R*k bytes (two
+    arena halves) to fit the context's capacity, with 25% headroom (equal-E
+    chunks balance the first join only, so later steps may split further)."""
+    import re
+
+    m = re.search(r"of (\d+) rows x (\d+) columns", msg)
+    cap = C.c_int64(0)
+    _lib.check(_lib.lib().gsm_context_capacity(dstore.context(), C.byref(cap)))
+    if not m or cap.value <= 0:
+        return 2
+    need = 8 * int(m.group(1)) * max(1, int(m.group(2)))
+    return _pow2(max(2, -(-need * 5 // (4 * cap.value))))
+
+
+def _host_budget_bytes() -> int:
+    try:
+        return int(os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE") * 0.7)
+    except (ValueError, OSError, AttributeError):
+        return 1 << 40
+
+
+def _check_budget_totals(kinds, rows, pre, budget: int, budget_mode: int) -> None:
+    """The three budget rules of complete_query (executor.py:158-163,
+    192-193, 237-241) applied, in plan order, to counters summed over the
+    left-row chunks: the same error the one-pass evaluation raises."""
+    for s in range(1, len(kinds)):
+        k = kinds[s]
+        if k in ("cross", "gate"):
+            nl = rows[s - 1]
+            nr = (rows[s] // nl) if nl else 0
+            if nl * nr > budget:
+                raise ResourceLimitError(f"cross product of {nl} x {nr} rows exceeds budget {budget}")
+        elif k in ("expand", "filter"):
+            if budget_mode == _lib.GSM_BUDGET_PARALLEL and pre[s] > budget:
+                raise ResourceLimitError(
+                    f"pre-allocated join region of {pre[s]} rows exceeds budget {budget}")
+            if budget_mode == _lib.GSM_BUDGET_SEQUENTIAL and rows[s] > budget:
+                raise ResourceLimitError(f"join output exceeds row budget {budget}")
+
+
+def _dedupe_first(a: np.ndarray) -> np.ndarray:
+    """DISTINCT across chunks: first occurrence of every row, in order."""
+    if a.shape[0] <= 1 or a.shape[1] == 0:
+        return a[:1] if a.shape[1] == 0 else a
+    v = np.ascontiguousarray(a).view(np.dtype((np.void, a.dtype.itemsize * a.shape[1])))
+    _, first = np.unique(v.reshape(-1), return_index=True)
+    return a[np.sort(first)]
+
+
+def _execute_chunked(dstore, query, steps, arr, proj_arr, nproj, budget, budget_mode, report,
+                     sink: str, parts0: int):
+    """Left-row chunking (SURVEY.md §5, §7 hard part 2; the sizing it
+    replaces is executor.py:197-215): the plan runs once per slice of its
+    first table (``gsm_execute`` part/parts: equal-E slices, so the union
+    of the slices of ``parts`` is the slice of ``parts/2`` they refine), each
+    slice's intermediates sized to the device.  A slice that still overflows
+    is split in two in place, so the slices stay in first-table order and
+    the concatenated rows are the one-pass result.  Budgets are checked on
+    the summed counters; each slice's rows are copied out (``sink="rows"``)
+    or reduced to a fingerprint on the device (``sink="summary"``) before
+    the next slice runs."""
+    from collections import deque
+
+    L = _lib.lib()
+    ctx = dstore.context()
+    n = len(steps)
+    distinct = 1 if query.distinct else 0
+    keep_rows = sink == "rows" or distinct
+    rows_t, pre_t, ms_t = [0] * n, [0] * n, [0.0] * n
+    meta = None
+    pieces: list[np.ndarray] = []
+    held = 0
+    host_cap = _host_budget_bytes() if keep_rows else 0
+    cnt = fsum = fxor = 0
+    done = 0
+    dev_s = 0.0
+    h2d = d2h = kern = 0
+    queue = deque((i, parts0) for i in range(parts0))
+    while queue:
+        part, parts = queue.popleft()
+        rep_struct, bufs = _new_report(n)
+        res = C.c_void_p()
+        st = L.gsm_execute(ctx, arr, n, proj_arr, nproj, distinct, _NO_BUDGET, budget_mode,
+                           part, parts, C.byref(rep_struct), C.byref(res))
+        if st == _lib.GSM_ERR_DEVICE_MEMORY:
+            msg = _lib.last_error()
+            if parts >= _MAX_PARTS:
+                raise DeviceMemoryError(f"{msg} (in one of {parts} left-row chunks)")
+            queue.appendleft((2 * part + 1, 2 * parts))
+            queue.appendleft((2 * part, 2 * parts))
+            continue
+        _lib.check(st)
+        done += 1
+        rows_buf, pre_buf, ms_buf, kind_buf, ar_buf, fused_buf = bufs
+        for i in range(n):
+            rows_t[i] += int(rows_buf[i])
+            pre_t[i] += int(pre_buf[i])
+            ms_t[i] += float(ms_buf[i])
+        if meta is None:
+            meta = ([_lib.STEP_KINDS[kind_buf[i]] for i in range(n)],
+                    [int(ar_buf[i]) for i in range(n)], [int(fused_buf[i]) for i in range(n)])
+        dev_s += rep_struct.total_device_ms / 1e3
+        h2d += int(rep_struct.h2d_bytes)
+        d2h += int(rep_struct.d2h_bytes)
+        kern += int(rep_struct.kernels)
+        if keep_rows:
+            nrows = C.c_int64(0)
+            ncols = C.c_int32(0)
+            L.gsm_result_shape(res, C.byref(nrows), C.byref(ncols))
+            held += 4 * int(nrows.value) * int(ncols.value)
+            if held > host_cap:
+                L.gsm_result_free(res)
+                raise ResourceLimitError(
+                    f"result of more than {held // max(4 * nproj, 1)} rows exceeds host memory "
+                    "(execute_summary returns its count and fingerprint)")
+            pieces.append(_fetch(L, res))
+        else:
+            fp = (C.c_uint64 * 3)()
+            try:
+                _lib.check(L.gsm_result_fingerprint(res, fp))
+            finally:
+                L.gsm_result_free(res)
+            cnt += int(fp[0])
+            fsum = (fsum + int(fp[1])) & _M64
+            fxor ^= int(fp[2])
+    kinds, arities, fused = meta
+    _check_budget_totals(kinds, rows_t, pre_t, budget, budget_mode)
+    if keep_rows:
+        out = np.concatenate(pieces) if pieces else np.empty((0, nproj), dtype=np.uint32)
+        if distinct:
+            out = _dedupe_first(out)
+    if report is not None:
+        seen: set[int] = set()
+        for pat in steps:
+            if pat.p not in seen:
+                seen.add(pat.p)
+                report.preparations += 1
+            report.uses += 1
+        for i, pat in enumerate(steps):
+            report.steps.append(StepReport(_pattern_text(pat), rows_t[i], pre_t[i], ms_t[i] / 1e3))
+        if isinstance(report, ExecutionReport):
+            report.kinds.extend(kinds)
+            report.arities.extend(arities)
+            report.fused.extend(fused)
+            report.device_seconds += dev_s
+            report.h2d_bytes += h2d
+            report.d2h_bytes += d2h
+            report.kernels += kern
+            report.chunks = done
+    schema = tuple(query.projection)
+    if sink == "rows":
+        return BindingTable(schema, array=out)
+    if keep_rows:
+        return ResultSummary(schema, *fingerprint_rows(out))
+    return ResultSummary(schema, cnt, fsum, fxor)
 
 
 def _fetch(L, res) -> np.ndarray:
@@ -387,6 +634,12 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
     if st != _lib.GSM_OK:
         msg = _lib.last_error()
         L.gsm_results_copy(outs, n, None, 1)
+        if st == _lib.GSM_ERR_DEVICE_MEMORY:
+            # a query's intermediates exceed device memory: evaluate the
+            # batch one query at a time, the oversize ones in left-row chunks
+            return [execute(q, p, dstore, mode=mode, row_budget=row_budget,
+                            report=None if reports is None else reports[i])
+                    for i, (q, p) in enumerate(items)]
         _lib.raise_status(st, msg)
     # shapes, then ONE host buffer for all results (views per query), copy + free
     L.gsm_results_shape(outs, n, prep.nrows, prep.ncols)
