@@ -719,6 +719,40 @@ static uint32_t bisect_right(const double* cum, double x, uint32_t hi) {
   }
   return lo;
 }
+/* bisect_right(cum, x, 0, n-1) through a guide table: guide[b] =
+   bisect_right(cum, b*total/G), so the answer for x in bucket b lies in
+   [guide[b], guide[b+1]]; one bucket of slack on each side absorbs the
+   rounding of x*G/total, and the final bisection compares against cum
+   itself, so the result is exactly the full bisection's. */
+typedef struct {
+  const double* cum;
+  uint32_t n, G;
+  double scale; /* G / total */
+  uint32_t* guide;  /* G + 1 entries */
+} Guide;
+static Guide guide_build(const double* cum, uint32_t n, uint32_t G) {
+  Guide g = {cum, n, G, (double)G / cum[n - 1], xmalloc(sizeof(uint32_t) * ((size_t)G + 1))};
+  const double total = cum[n - 1];
+  uint32_t j = 0;
+  for (uint32_t b = 0; b <= G; b++) {
+    const double edge = total * ((double)b / (double)G);
+    while (j < n - 1 && !(edge < cum[j])) j++;
+    g.guide[b] = j;
+  }
+  return g;
+}
+static uint32_t guide_find(const Guide* g, double x) {
+  double fb = x * g->scale;
+  uint32_t b = fb <= 0.0 ? 0 : (fb >= (double)g->G ? g->G : (uint32_t)fb);
+  uint32_t lo = g->guide[b > 0 ? b - 1 : 0];
+  uint32_t hi = g->guide[b + 2 <= g->G ? b + 2 : g->G];
+  if (hi > g->n - 1) hi = g->n - 1;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) / 2;
+    if (x < g->cum[mid]) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
 static double* cumulative_weights(uint32_t n, double exponent) { /* generate.py:35-41 */
   double* cum = xmalloc(sizeof(double) * n);
   double acc = 0.0;
@@ -739,6 +773,7 @@ static void gen_powerlaw(uint64_t triples, uint32_t predicates, double zipf, uin
   double* pcum = cumulative_weights(predicates, zipf);
   double* ncum = cumulative_weights((uint32_t)nodes, node_skew);
   double ptotal = pcum[predicates - 1] + 0.0, ntotal = ncum[nodes - 1] + 0.0;
+  Guide ng = guide_build(ncum, (uint32_t)nodes, nodes > (1u << 24) ? (1u << 24) : (uint32_t)nodes);
   /* node/pred ids in first-occurrence order without string hashing: the terms
      are "n<k>" / "p<k>", so a direct k -> id table is an exact dictionary. */
   uint32_t* nid = calloc(nodes + 1, sizeof(uint32_t));
@@ -751,8 +786,8 @@ static void gen_powerlaw(uint64_t triples, uint32_t predicates, double zipf, uin
   while (remaining > 0) {
     uint32_t k = remaining < 10000 ? (uint32_t)remaining : 10000;
     for (uint32_t i = 0; i < k; i++) bp[i] = 1 + bisect_right(pcum, py_random() * ptotal, predicates - 1);
-    for (uint32_t i = 0; i < k; i++) bs[i] = 1 + bisect_right(ncum, py_random() * ntotal, (uint32_t)nodes - 1);
-    for (uint32_t i = 0; i < k; i++) bo[i] = 1 + bisect_right(ncum, py_random() * ntotal, (uint32_t)nodes - 1);
+    for (uint32_t i = 0; i < k; i++) bs[i] = 1 + guide_find(&ng, py_random() * ntotal);
+    for (uint32_t i = 0; i < k; i++) bo[i] = 1 + guide_find(&ng, py_random() * ntotal);
     for (uint32_t i = 0; i < k; i++) {
       uint32_t s = bs[i], p = bp[i], o = bo[i];
       if (!nid[s]) { nid[s] = ++nn; norder[nn] = s; }
@@ -773,6 +808,7 @@ static void gen_powerlaw(uint64_t triples, uint32_t predicates, double zipf, uin
     int l = snprintf(buf, sizeof buf, "p%u", porder[i]);
     dict_encode(&g_preds, buf, (size_t)l);
   }
+  free(ng.guide);
   free(pcum); free(ncum); free(nid); free(pid); free(norder); free(porder);
   free(bp); free(bs); free(bo);
 }

@@ -237,6 +237,18 @@ typedef struct {
 gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
                              gsm_status* statuses, gsm_result** outs, float* device_ms);
 
+/* gsm_execute_batch that also hands the rows over: query i's result rows
+ * (n_rows[i] x n_cols[i], always set when statuses[i] == GSM_OK) are copied
+ * into dst[i] when they fit dst_cap[i] ids, as soon as query i finishes
+ * (while the rest of the batch still runs), and outs[i] is then NULL;
+ * otherwise outs[i] holds the result as in gsm_execute_batch.  dst / dst_cap
+ * may be NULL (nothing copied).  The reference's callers get a list of
+ * BindingTables; this is the one-call form of execute + rows copy. */
+gsm_status gsm_execute_batch_into(gsm_context* const* ctxs, int32_t n_queries,
+                                  const gsm_query* queries, gsm_status* statuses,
+                                  uint32_t* const* dst, const int64_t* dst_cap, int64_t* n_rows,
+                                  int32_t* n_cols, gsm_result** outs, float* device_ms);
+
 /* Replaces executor.sm_join / parallel_sm_join / cross_product
  * (executor.py:155-280) on arbitrary binding tables (not store-backed):
  * `left` is n_left x a and `right` n_right x b row-major uint32 host arrays.

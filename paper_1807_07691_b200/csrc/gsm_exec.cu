@@ -33,6 +33,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -533,9 +534,18 @@ struct ExpandP {
   // per warp).  For small left arities the row's left values are hoisted into
   // registers and the columns are streamed through precomputed pointers, so a
   // chunk costs little more than its a+1 coalesced stores.
+  //
+  // Columns are 16-byte aligned (the arena halves are, and cap_for() keeps
+  // the column stride a multiple of 4 ids), so after a head of < 4
+  // candidates that brings pos + j to a multiple of 4, every lane writes 4
+  // consecutive output slots of each column with one 128-bit store (the
+  // left columns are the same value 4 times): one store instruction per
+  // column per 128 candidates instead of 4.  Each lane loads its 4
+  // candidates with 4 scalar loads (the run's start is not 16-byte aligned);
+  // the warp's 4 loads together cover 512 contiguous bytes.
   template <int A>
   __device__ void row_warp_cols(const DTable& s, i64 r, u32 aux, i64 c, i64 pos) const {
-    constexpr int U = 8;
+    constexpr int U = 4;  // quads per lane in flight: 16 loads before the stores
     const int lane = threadIdx.x & 31;
     u32 lv[A > 0 ? A : 1];
 #pragma unroll
@@ -543,22 +553,42 @@ struct ExpandP {
     const u32* src = R.dst + aux;
     u32* ob = out + pos;  // column cc of output slot pos + j is ob[cc * cap + j]
     const i64 lim = min(c, cap - pos);
-    for (i64 j0 = 0; j0 < c; j0 += 32 * U) {
-      u32 v[U];
+    if (lim <= 0) return;
+    const int h = (int)min((i64)((4 - (pos & 3)) & 3), lim);  // head: scalar
+    if (lane < h) {
+#pragma unroll
+      for (int cc = 0; cc < A; cc++) ob[(i64)cc * cap + lane] = lv[cc];
+      ob[(i64)A * cap + lane] = __ldg(src + lane);
+    }
+    const u32* s4 = src + h;
+    u32* o4 = ob + h;  // 16-byte aligned in every column
+    const i64 nq = (lim - h) >> 2;
+    for (i64 q0 = 0; q0 < nq; q0 += 32 * U) {
+      u32 v[U][4];
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const i64 j = j0 + 32 * u + lane;
-        v[u] = j < c ? __ldg(src + j) : 0u;
+        const i64 q = q0 + 32 * u + lane;
+#pragma unroll
+        for (int k = 0; k < 4; k++) v[u][k] = q < nq ? __ldg(s4 + 4 * q + k) : 0u;
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const i64 j = j0 + 32 * u + lane;
-        if (j < lim) {
+        const i64 q = q0 + 32 * u + lane;
+        if (q < nq) {
 #pragma unroll
-          for (int cc = 0; cc < A; cc++) ob[(i64)cc * cap + j] = lv[cc];
-          ob[(i64)A * cap + j] = v[u];
+          for (int cc = 0; cc < A; cc++)
+            *reinterpret_cast<uint4*>(o4 + (i64)cc * cap + 4 * q) = make_uint4(lv[cc], lv[cc], lv[cc], lv[cc]);
+          *reinterpret_cast<uint4*>(o4 + (i64)A * cap + 4 * q) =
+              make_uint4(v[u][0], v[u][1], v[u][2], v[u][3]);
         }
       }
+    }
+    const i64 t0 = h + 4 * nq;  // tail: < 4 candidates, scalar
+    if (t0 + lane < lim) {
+      const i64 j = t0 + lane;
+#pragma unroll
+      for (int cc = 0; cc < A; cc++) ob[(i64)cc * cap + j] = lv[cc];
+      ob[(i64)A * cap + j] = __ldg(src + j);
     }
   }
   template <int K>
@@ -1922,6 +1952,10 @@ struct gsm_context {
   std::unordered_map<std::string, BatchEntry> batches;
   u64 bufgen = 0;  // process-unique; renewed whenever captured pointers change
   cudaEvent_t ev_fork = nullptr;
+  // Recorded (as an external event node) at the end of this context's
+  // branch of a batch graph: the host completes each query as soon as its
+  // own branch is done, while the rest of the batch still runs.
+  cudaEvent_t ev_ext = nullptr;
 };
 
 namespace gsm {
@@ -2064,7 +2098,9 @@ struct Exec {
     }
     return t;
   }
-  i64 cap_for(int a) const { return a == 0 ? ((i64)1 << 62) : (i64)(half / (4 * (size_t)a)); }
+  // column stride: a multiple of 4 ids, so every column is 16-byte aligned
+  // (the vectorised writers' 128-bit stores)
+  i64 cap_for(int a) const { return a == 0 ? ((i64)1 << 62) : (i64)(half / (4 * (size_t)a)) & ~(i64)3; }
   static Home other(Home h) { return h == H_A ? H_B : H_A; }
 
   // Zero-copy table for a pattern read as a whole table (first step, or the
@@ -2172,7 +2208,8 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if ((e = cudaEventCreate(&c->ev_q0)) != cudaSuccess || (e = cudaEventCreate(&c->ev_q1)) != cudaSuccess ||
       (e = cudaEventCreate(&c->ev_q2)) != cudaSuccess || (e = cudaEventCreate(&c->ev_b0)) != cudaSuccess ||
       (e = cudaEventCreate(&c->ev_b1)) != cudaSuccess || (e = cudaEventCreate(&c->ev_done)) != cudaSuccess ||
-      (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess)
+      (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->ev_ext, cudaEventDisableTiming)) != cudaSuccess)
     return fail(cuda_error(e, "cudaEventCreate"));
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -2234,7 +2271,7 @@ gsm_status gsm_context_free(gsm_context* c) {
   if (c->ev_q0) cudaEventDestroy(c->ev_q0);
   if (c->ev_q1) cudaEventDestroy(c->ev_q1);
   if (c->ev_q2) cudaEventDestroy(c->ev_q2);
-  for (cudaEvent_t ev : {c->ev_b0, c->ev_b1, c->ev_done, c->ev_fork})
+  for (cudaEvent_t ev : {c->ev_b0, c->ev_b1, c->ev_done, c->ev_fork, c->ev_ext})
     if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -3389,6 +3426,9 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       ok = launch_query(ctxs[i], qa[i], S[i]) == GSM_OK;
       S[i].capture_only = false;
       ctxs[i]->use_pdl = pdl;
+      if (ok)
+        ok = cudaEventRecordWithFlags(ctxs[i]->ev_ext, ctxs[i]->stream, cudaEventRecordExternal) ==
+             cudaSuccess;
     }
     // Join every forked stream back, also after a failed plan (a planning
     // error returns before issuing anything): an unjoined stream would leave
@@ -3483,8 +3523,23 @@ double now_s() {
 }
 }  // namespace
 
-gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
-                             gsm_status* statuses, gsm_result** outs, float* device_ms) {
+// A finished query's rows go straight into the caller's buffer when they fit
+// (the result handle is then freed and outs[i] left NULL).
+static void deliver(gsm_result*& r, uint32_t* const* dst, const int64_t* dst_cap, int i,
+                    int64_t* n_rows, int32_t* n_cols) {
+  if (!r) return;
+  if (n_rows) n_rows[i] = r->n;
+  if (n_cols) n_cols[i] = r->k;
+  if (!dst || !dst[i] || !dst_cap || r->n * (i64)std::max(r->k, 1) > dst_cap[i]) return;
+  if (gsm_result_copy(r, dst[i]) != GSM_OK) return;  // left to the caller
+  gsm_result_free(r);
+  r = nullptr;
+}
+
+static gsm_status batch_impl(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
+                             gsm_status* statuses, gsm_result** outs, float* device_ms,
+                             uint32_t* const* dst, const int64_t* dst_cap, int64_t* n_rows,
+                             int32_t* n_cols) {
   const double t_begin = g_host_times.on ? now_s() : 0.0;
   if (n_queries < 0 || (n_queries > 0 && (!ctxs || !queries || !outs)))
     return set_error(GSM_ERR_VALUE, "bad batch arguments");
@@ -3532,17 +3587,54 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
     if (n_queries > 0) cudaStreamSynchronize(as_graph ? ctxs[0]->stream : ctxs[n_queries - 1]->stream);
     t_waited = now_s();
   }
-  if (as_graph && n_queries > 0) {  // one wait for the whole batch graph
-    GSM_CUDA(cudaStreamSynchronize(ctxs[0]->stream));
-    for (int i = 0; i < n_queries; i++) S[i].synced = true;
+  std::vector<char> done((size_t)n_queries, 0);
+  auto finish = [&](int i) {
+    if (st[i] == GSM_OK) {
+      st[i] = complete_query(ctxs[i], qa[i], S[i], &outs[i]);
+      if (st[i] != GSM_OK) msg[i] = gsm_last_error();
+      else deliver(outs[i], dst, dst_cap, i, n_rows, n_cols);
+    }
+    done[i] = 1;
+  };
+  if (as_graph && n_queries > 0) {
+    // Complete each query as soon as its own branch of the graph is done
+    // (its external event fired), while the other branches still run: the
+    // budget checks and the copy of its rows overlap the rest of the batch.
+    int left = n_queries;
+    cudaError_t bad = cudaSuccess;
+    while (left > 0 && bad == cudaSuccess) {
+      bool progressed = false;
+      for (int i = 0; i < n_queries && bad == cudaSuccess; i++) {
+        if (done[i]) continue;
+        const cudaError_t q = cudaEventQuery(ctxs[i]->ev_ext);
+        if (q == cudaErrorNotReady) continue;
+        if (q != cudaSuccess) {
+          bad = q;
+          break;
+        }
+        S[i].synced = true;
+        finish(i);
+        left--;
+        progressed = true;
+      }
+      if (!progressed && bad == cudaSuccess) std::this_thread::yield();
+    }
+    // the join (and the batch's end event) on the origin stream
+    const cudaError_t e = cudaStreamSynchronize(ctxs[0]->stream);
+    if (bad == cudaSuccess) bad = e;
+    if (bad != cudaSuccess) {
+      for (int i = 0; i < n_queries; i++)
+        if (outs[i]) {
+          gsm_result_free(outs[i]);
+          outs[i] = nullptr;
+        }
+      return cuda_error(bad, "batch graph");
+    }
   }
   gsm_status first = GSM_OK;
   std::string first_msg;
   for (int i = 0; i < n_queries; i++) {
-    if (st[i] == GSM_OK) {
-      st[i] = complete_query(ctxs[i], qa[i], S[i], &outs[i]);
-      if (st[i] != GSM_OK) msg[i] = gsm_last_error();
-    }
+    if (!done[i]) finish(i);
     if (statuses) statuses[i] = st[i];
     if (st[i] != GSM_OK && first == GSM_OK) {
       first = st[i];
@@ -3563,6 +3655,25 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
   }
   if (first != GSM_OK) set_error(first, first_msg);
   return first;
+}
+
+gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const gsm_query* queries,
+                             gsm_status* statuses, gsm_result** outs, float* device_ms) {
+  return batch_impl(ctxs, n_queries, queries, statuses, outs, device_ms, nullptr, nullptr, nullptr,
+                    nullptr);
+}
+
+gsm_status gsm_execute_batch_into(gsm_context* const* ctxs, int32_t n_queries,
+                                  const gsm_query* queries, gsm_status* statuses,
+                                  uint32_t* const* dst, const int64_t* dst_cap, int64_t* n_rows,
+                                  int32_t* n_cols, gsm_result** outs, float* device_ms) {
+  if (n_queries > 0 && (!n_rows || !n_cols)) return set_error(GSM_ERR_VALUE, "bad batch arguments");
+  for (int i = 0; i < n_queries; i++) {
+    n_rows[i] = 0;
+    n_cols[i] = 0;
+  }
+  return batch_impl(ctxs, n_queries, queries, statuses, outs, device_ms, dst, dst_cap, n_rows,
+                    n_cols);
 }
 
 

@@ -350,7 +350,7 @@ def _first_parts(dstore, msg: str) -> int:
 
 def _host_budget_bytes() -> int:
     try:
-        return int(os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE") * 0.7)
+        return int(os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE") * 0.5)
     except (ValueError, OSError, AttributeError):
         return 1 << 40
 
@@ -544,7 +544,23 @@ class _PreparedBatch:
     plans keep their compiled encoding (see :func:`compile_plan`)."""
 
     __slots__ = ("items", "compiled", "ctx_arr", "qarr", "outs", "statuses", "nrows", "ncols",
-                 "nrows_np", "ncols_np", "dsts", "ms", "steps", "schemas")
+                 "nrows_np", "ncols_np", "dsts", "caps", "offsets", "total_cap", "ms", "steps",
+                 "schemas")
+
+
+def _size_slices(prep, sizes) -> None:
+    """Per-query slices of the batch's host buffer: the last result sizes
+    (ids) plus 1/8 headroom, so a result that varies a little still lands in
+    place."""
+    off = 0
+    offsets = []
+    for i, sz in enumerate(sizes):
+        cap = sz + sz // 8
+        prep.caps[i] = cap
+        offsets.append(off)
+        off += cap
+    prep.offsets = offsets
+    prep.total_cap = off
 
 
 def _prepared_batch(dstore, items, budget_mode: int, budget: int) -> _PreparedBatch:
@@ -581,6 +597,8 @@ def _prepared_batch(dstore, items, budget_mode: int, budget: int) -> _PreparedBa
     prep.nrows_np = np.frombuffer(prep.nrows, dtype=np.int64)  # views of the ctypes arrays
     prep.ncols_np = np.frombuffer(prep.ncols, dtype=np.int32)
     prep.dsts = (C.c_void_p * n)()
+    prep.caps = (C.c_int64 * n)()
+    _size_slices(prep, [0] * n)
     prep.ms = C.c_float(0.0)
     prep.steps = [c[0] for c in compiled]
     prep.schemas = [tuple(q.projection) for q, _ in items]
@@ -623,9 +641,20 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
             rep_bufs.append((rep_struct, bufs))
     L = _lib.lib()
     ms = prep.ms
+    # One host buffer for all results, sized by this batch's previous
+    # results: each query's rows are copied into their slice as soon as the
+    # query finishes (gsm_execute_batch_into), overlapping the rest of the
+    # batch; a result that outgrew its slice is copied afterwards.
+    caps = prep.caps
+    buf = np.empty(prep.total_cap, dtype=np.uint32)
+    base = buf.ctypes.data
+    dsts = prep.dsts
+    for i, off in enumerate(prep.offsets):
+        dsts[i] = base + 4 * off
     try:
-        st = L.gsm_execute_batch(prep.ctx_arr, n, qarr, prep.statuses, prep.outs,
-                                 C.byref(ms) if batch_timing is not None else None)
+        st = L.gsm_execute_batch_into(prep.ctx_arr, n, qarr, prep.statuses, dsts, caps,
+                                      prep.nrows, prep.ncols, prep.outs,
+                                      C.byref(ms) if batch_timing is not None else None)
     finally:
         if reports is not None:
             for i in range(n):
@@ -641,21 +670,23 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
                             report=None if reports is None else reports[i])
                     for i, (q, p) in enumerate(items)]
         _lib.raise_status(st, msg)
-    # shapes, then ONE host buffer for all results (views per query), copy + free
-    L.gsm_results_shape(outs, n, prep.nrows, prep.ncols)
     nr = prep.nrows_np.tolist()
     nc = prep.ncols_np.tolist()
-    sizes = [a * b for a, b in zip(nr, nc)]
-    buf = np.empty(sum(sizes), dtype=np.uint32)
-    base = buf.ctypes.data
     arrays = []
-    ptrs = []
-    off = 0
-    for sz, r, k in zip(sizes, nr, nc):
-        arrays.append(buf[off:off + sz].reshape(r, k))
-        ptrs.append(base + 4 * off if sz else None)
-        off += sz
-    _lib.check(L.gsm_results_copy(outs, n, (C.c_void_p * n)(*ptrs), 1))
+    grown = False
+    for i, (r, k, off) in enumerate(zip(nr, nc, prep.offsets)):
+        if outs[i]:  # did not fit its slice: copy it now, give the slice room next time
+            a = np.empty((r, k), dtype=np.uint32)
+            st = L.gsm_result_copy(outs[i], a.ctypes.data) if a.size else _lib.GSM_OK
+            L.gsm_result_free(outs[i])
+            outs[i] = None
+            _lib.check(st)
+            arrays.append(a)
+            grown = True
+        else:
+            arrays.append(buf[off:off + r * k].reshape(r, k))
+    if grown:
+        _size_slices(prep, [r * max(k, 1) for r, k in zip(nr, nc)])
     if reports is not None:
         for i in range(n):
             rep_struct, bufs = rep_bufs[i]

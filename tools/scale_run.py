@@ -36,6 +36,47 @@ REPO = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(REPO))
 
 
+def summary_run(g, q, plan, store, budget, name, why):
+    """execute_summary twice: with the chunk count the executor picks, then
+    with twice as many chunks (different slice boundaries, so a dropped or
+    doubled row would change the fingerprint)."""
+    rep = g.ExecutionReport()
+    t0 = time.perf_counter()
+    s1 = g.execute_summary(q, plan, store, row_budget=budget, report=rep)
+    wall = time.perf_counter() - t0
+    rep2 = g.ExecutionReport()
+    s2 = g.execute_summary(q, plan, store, row_budget=budget, report=rep2,
+                           chunks=max(2, 2 * rep.chunks))
+    join = sum(s.rows for s in rep.steps[1:])
+    return {"query": name, "mode": "execute_summary (rows not materialised on the host)",
+            "why": why, "rows": s1.rows, "fingerprint": [s1.rows, s1.sum, s1.xor],
+            "chunks": rep.chunks, "step_rows": [s.rows for s in rep.steps],
+            "step_prealloc": [s.prealloc_total for s in rep.steps], "kinds": rep.kinds,
+            "gpu_ms": round(1e3 * rep.device_seconds, 3), "wall_s": round(wall, 3),
+            "join_rows": join, "join_rows_per_s": round(join / max(rep.device_seconds, 1e-9), 1),
+            "rechunked": {"chunks": rep2.chunks, "same_fingerprint": s2.fingerprint == s1.fingerprint,
+                          "same_step_rows": [s.rows for s in rep2.steps] == [s.rows for s in rep.steps]},
+            "parity": "oracle not run (intermediate beyond host RAM); see the reduced-store "
+                      "chunked parity in tests/test_gpu_chunked.py"}
+
+
+def degree_stats(store_dir, np, top=4):
+    """Largest out/in degree of the biggest predicates (the hub sizes the
+    skew produces; SURVEY.md §8(d) T4 asks for hubs of 1e5-1e6)."""
+    d = Path(store_dir)
+    sizes = sorted(((f.stat().st_size, f) for f in d.glob("p*.so")), reverse=True)[:top]
+    out = {}
+    for _, f in sizes:
+        pid = f.stem
+        for ext, what in (("so", "max_out"), ("os", "max_in")):
+            keys = np.fromfile(d / f"{pid}.{ext}", dtype="<u8")[0::2]
+            if keys.size:
+                b = np.flatnonzero(np.diff(keys)) + 1
+                runs = np.diff(np.concatenate(([0], b, [keys.size])))
+                out.setdefault(pid, {"pairs": int(keys.size)})[what] = int(runs.max())
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kind", choices=["lubm", "powerlaw", "watdiv"], default="lubm")
@@ -43,6 +84,10 @@ def main():
     ap.add_argument("--univ", type=int, default=1000)
     ap.add_argument("--triples", type=int, default=100_000_000)
     ap.add_argument("--predicates", type=int, default=40)
+    ap.add_argument("--node-skew", type=float, default=0.5,
+                    help="powerlaw endpoint exponent (generate.py NODE_SKEW; T4 uses 0.9)")
+    ap.add_argument("--qdir", default=None,
+                    help="query directory under datagen/queries (default: the kind's own)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--exact-rows", type=int, default=20_000_000)
@@ -50,6 +95,9 @@ def main():
                     help="skip the oracle when a step materialises more rows (host RAM guard)")
     ap.add_argument("--store", default=None, help="reuse an existing store directory")
     ap.add_argument("--only", default=None, help="comma-separated query names to run")
+    ap.add_argument("--summary", default="",
+                    help="comma-separated query names evaluated by execute_summary only (results "
+                         "larger than host memory)")
     args = ap.parse_args()
 
     import numpy as np
@@ -73,7 +121,8 @@ def main():
         elif args.kind == "watdiv":
             gen += ["--scale", str(args.scale)]
         else:  # generate.py's model (Zipf predicates, i^-0.5 endpoints, nodes = triples/4)
-            gen += ["--triples", str(args.triples), "--predicates", str(args.predicates)]
+            gen += ["--triples", str(args.triples), "--predicates", str(args.predicates),
+                    "--node-skew", str(args.node_skew)]
         subprocess.run(gen, check=True, stdout=subprocess.DEVNULL)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
@@ -84,7 +133,11 @@ def main():
                       "load_s": round(t_load, 2), "device_bytes": store.device_bytes()}),
           flush=True)
     prep = orc.PreparedStore(store.matrices)
-    if args.kind == "lubm":
+    if args.kind == "powerlaw":
+        print(json.dumps({"degrees": degree_stats(store_dir, np)}), flush=True)
+    if args.qdir:
+        qfiles = sorted((REPO / "datagen/queries" / args.qdir).glob("*.rq"))
+    elif args.kind == "lubm":
         qfiles = sorted((REPO / "datagen/queries/lubm").glob("*.rq")) + \
             sorted((REPO / "datagen/queries/lubm_complex").glob("*.rq"))
     else:
@@ -97,12 +150,18 @@ def main():
         q = g.bind_constants(g.parse_query(qf.read_text()), store.dictionary)
         plan = g.make_plan(q, store.stats)
         budget = 1 << 62
+        if qf.stem in set(args.summary.split(",")):
+            print(json.dumps(summary_run(g, q, plan, store, budget, qf.stem, "--summary")), flush=True)
+            summary["summary_only"] = summary.get("summary_only", 0) + 1
+            continue
         try:
             res = g.execute(q, plan, store, row_budget=budget)
         except g.ResourceLimitError as e:
-            # not materialisable on one device (nor by the CPU engines)
-            print(json.dumps({"query": qf.stem, "error": str(e)}), flush=True)
-            summary["infeasible"] = summary.get("infeasible", 0) + 1
+            # the rows do not fit host memory: count + fingerprint on the
+            # device, the plan in left-row chunks where its intermediates
+            # exceed device memory
+            print(json.dumps(summary_run(g, q, plan, store, budget, qf.stem, str(e))), flush=True)
+            summary["summary_only"] = summary.get("summary_only", 0) + 1
             continue
         dev = []
         rep = None
@@ -114,6 +173,8 @@ def main():
                "step_prealloc": [s.prealloc_total for s in rep.steps], "kinds": rep.kinds,
                "gpu_ms": round(1e3 * statistics.median(dev), 3),
                "join_rows": sum(s.rows for s in rep.steps[1:])}
+        if rep.chunks:
+            rec["chunks"] = rep.chunks
         rec["join_rows_per_s"] = round(rec["join_rows"] / statistics.median(dev), 1)
         # HBM roofline of the whole query: algorithmic bytes of its join steps
         # (bench._step_bytes) / device time
