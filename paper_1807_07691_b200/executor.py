@@ -545,7 +545,7 @@ class _PreparedBatch:
 
     __slots__ = ("items", "compiled", "ctx_arr", "qarr", "outs", "statuses", "nrows", "ncols",
                  "nrows_np", "ncols_np", "dsts", "caps", "offsets", "total_cap", "ms", "steps",
-                 "schemas")
+                 "schemas", "sig")
 
 
 def _size_slices(prep, sizes) -> None:
@@ -563,17 +563,29 @@ def _size_slices(prep, sizes) -> None:
     prep.total_cap = off
 
 
+def _batch_sig(items):
+    """Everything a batch's encoding depends on, flattened: every plan
+    step's pattern (EncodedPattern is frozen, so equal patterns encode
+    equally), every projection and DISTINCT flag.  One comprehension over
+    the batch instead of a compile_plan validation per query."""
+    return ([s.pattern for _, p in items for s in p.steps],
+            [(len(p.steps), q.projection, q.distinct) for q, p in items])
+
+
 def _prepared_batch(dstore, items, budget_mode: int, budget: int) -> _PreparedBatch:
-    compiled = [compile_plan(q, p) for q, p in items]
-    key = (tuple(map(id, compiled)), budget_mode, budget)
     cache = dstore.__dict__.setdefault("_batch_prep", {})
+    # ids only pick the cache slot (a reused id is caught by the signature)
+    key = (tuple(map(id, items)), budget_mode, budget)
+    sig = _batch_sig(items)
     prep = cache.get(key)
-    if prep is not None and all(a is b for a, b in zip(prep.compiled, compiled)):
+    if prep is not None and prep.sig == sig:
         return prep
+    compiled = [compile_plan(q, p) for q, p in items]
     n = len(items)
     prep = _PreparedBatch()
-    prep.items = items  # keeps the compiled encodings (and so their ids) alive
+    prep.items = items  # keeps the queries and plans (and so their ids) alive
     prep.compiled = compiled
+    prep.sig = sig
     ctxs = dstore.context_pool(n)
     prep.ctx_arr = (C.c_void_p * n)(*[c.value for c in ctxs])
     prep.qarr = (_lib.Query * n)()
@@ -649,8 +661,7 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
     buf = np.empty(prep.total_cap, dtype=np.uint32)
     base = buf.ctypes.data
     dsts = prep.dsts
-    for i, off in enumerate(prep.offsets):
-        dsts[i] = base + 4 * off
+    dsts[:] = [base + 4 * off for off in prep.offsets]
     try:
         st = L.gsm_execute_batch_into(prep.ctx_arr, n, qarr, prep.statuses, dsts, caps,
                                       prep.nrows, prep.ncols, prep.outs,

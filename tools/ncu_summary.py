@@ -21,6 +21,10 @@ KEYS = [
     ("launch__grid_size", "grid"),
     ("launch__registers_per_thread", "regs"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_%"),
+    ("smsp__inst_executed.sum", "instructions"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_st.sum", "global_store_requests"),
+    ("lts__t_sectors_srcunit_tex_op_write.sum", "l2_write_sectors"),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "l2_read_sectors"),
 ]
 
 

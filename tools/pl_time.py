@@ -15,6 +15,8 @@ import paper_1807_07691_b200 as g  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--triples", type=int, default=100_000_000)
 ap.add_argument("--store", default=None)
+ap.add_argument("--only", default=None, help="comma-separated query names")
+ap.add_argument("--reps", type=int, default=5)
 args = ap.parse_args()
 with tempfile.TemporaryDirectory() as tmp:
     sd = args.store
@@ -24,6 +26,8 @@ with tempfile.TemporaryDirectory() as tmp:
                         "--predicates", "40", "--seed", "0", "--out", sd], check=True, stdout=subprocess.DEVNULL)
     st = g.load(sd)
     for f in sorted((REPO / "datagen/queries/powerlaw").glob("*.rq")):
+        if args.only and f.stem not in args.only.split(","):
+            continue
         q = g.bind_constants(g.parse_query(f.read_text()), st.dictionary)
         plan = g.make_plan(q, st.stats)
         try:
@@ -32,7 +36,7 @@ with tempfile.TemporaryDirectory() as tmp:
             print(f.stem, "infeasible")
             continue
         ts = []
-        for _ in range(5):
+        for _ in range(args.reps):
             rep = g.ExecutionReport()
             g.execute(q, plan, st, row_budget=1 << 62, report=rep)
             ts.append(rep.device_seconds)
