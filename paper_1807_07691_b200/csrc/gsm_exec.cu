@@ -1507,14 +1507,22 @@ __global__ void k_slice(DTable* T, int a, i64 part, i64 parts, StepStat* st) {
 }
 
 // Equal-E row partitioning of the first table ("balanced by
-// the count pass's prefix (equal E, not equal L)").  The first table is cut
-// into SLICE_CHUNKS contiguous chunks; k_slice_sums adds up the first join's
-// per-row candidate counts N_i (its segment lengths) per chunk, k_slice_pick
-// scans the chunk sums and gives rank `part` the chunks whose exclusive
-// prefix falls in [E*part/parts, E*(part+1)/parts).  Any split is correct
-// (the ranks' slices tile the table); this one balances E to within one
-// chunk.  E = 0 falls back to equal rows.
+// the count pass's prefix (equal E, not equal L)").  Row r of the first
+// table belongs to part own(r) = min(floor(X_r * parts / E), parts - 1),
+// X_r = the exclusive prefix of the first join's per-row candidate counts
+// N_i (segment lengths), E = their total; part p keeps the contiguous rows
+// [B(p), B(p+1)), B(q) = the first row with own >= q.  Row-granular and
+// nested: for parts a power of two, own_2P(r) / 2 == own_P(r), so part p of
+// P is exactly parts 2p and 2p+1 of 2P (the left-row chunking splits a
+// chunk in place on that).  k_slice_sums adds up N_i over SLICE_CHUNKS
+// contiguous chunks; k_slice_pick finds, per boundary, the chunk holding it
+// from the chunk prefixes, then the row inside that chunk by a block scan of
+// its rows.  E = 0 falls back to equal rows (n*p/parts, also nested).
 constexpr int SLICE_CHUNKS = 4096;
+__device__ __forceinline__ i64 slice_owner(u64 x, u64 E, i64 parts) {
+  const i64 o = (i64)((unsigned __int128)x * (u64)parts / E);
+  return o < parts - 1 ? o : parts - 1;
+}
 __global__ void k_slice_sums(const DTable* T, int key, Orient R, u64* __restrict__ sums) {
   pdl_wait();
   pdl_trigger();
@@ -1533,12 +1541,16 @@ __global__ void k_slice_sums(const DTable* T, int key, Orient R, u64* __restrict
   }
 }
 __global__ void __launch_bounds__(1024) k_slice_pick(DTable* T, int a, i64 part, i64 parts,
-                                                     StepStat* st, const u64* __restrict__ sums) {
+                                                     StepStat* st, const u64* __restrict__ sums,
+                                                     int key, Orient R) {
   pdl_wait();
   pdl_trigger();
   constexpr int PER = SLICE_CHUNKS / 1024;
   __shared__ u64 s_w[32];
-  __shared__ unsigned long long s_lo, s_hi;
+  __shared__ int s_chunk[2];
+  __shared__ u64 s_base[2];
+  __shared__ unsigned long long s_row;
+  __shared__ u64 s_run;
   const i64 n = T->n;
   const int nch = (int)(n < SLICE_CHUNKS ? n : SLICE_CHUNKS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1556,37 +1568,83 @@ __global__ void __launch_bounds__(1024) k_slice_pick(DTable* T, int a, i64 part,
     if (lane >= o) x += y;
   }
   if (lane == 31) s_w[warp] = x;
-  if (tid == 0) s_lo = s_hi = 0;
+  if (tid < 2) {
+    s_chunk[tid] = -1;
+    s_base[tid] = 0;
+  }
   __syncthreads();
   u64 before = x - tot, E = 0;
   for (int w = 0; w < 32; w++) {
     if (w < warp) before += s_w[w];
     E += s_w[w];
   }
-  unsigned long long c_lo = 0, c_hi = 0;  // chunks owned by ranks < part / <= part
+  i64 bound[2];
+  if (E == 0) {  // no candidates anywhere: equal rows
+    bound[0] = (i64)((__int128)n * part / parts);
+    bound[1] = (i64)((__int128)n * (part + 1) / parts);
+  } else {
+    // boundary q in {part, part + 1}: the chunk holding B(q) is the last
+    // chunk whose first row's owner is < q (B(0) = 0, B(parts) = n)
 #pragma unroll
-  for (int i = 0; i < PER; i++) {
-    const int ch = tid * PER + i;
-    if (ch < nch && E > 0) {
-      i64 own = (i64)((unsigned __int128)before * (u64)parts / E);
-      if (own > parts - 1) own = parts - 1;
-      c_lo += own < part;
-      c_hi += own <= part;
+    for (int i = 0; i < PER; i++) {
+      const int ch = tid * PER + i;
+      if (ch < nch) {
+        const i64 own = slice_owner(before, E, parts);
+        const u64 nxt = before + v[i];
+        const i64 own_next = ch + 1 < nch ? slice_owner(nxt, E, parts) : parts;
+        for (int b = 0; b < 2; b++) {
+          const i64 q = part + b;
+          if (q > 0 && q < parts && own < q && own_next >= q) {
+            s_chunk[b] = ch;
+            s_base[b] = before;
+          }
+        }
+      }
+      before += v[i];
     }
-    before += v[i];
+    __syncthreads();
+    for (int b = 0; b < 2; b++) {
+      const i64 q = part + b;
+      if (q <= 0 || q >= parts) {
+        bound[b] = q <= 0 ? 0 : n;
+        continue;
+      }
+      const int ch = s_chunk[b];
+      const i64 lo = (i64)((__int128)n * ch / nch), hi = (i64)((__int128)n * (ch + 1) / nch);
+      if (tid == 0) {
+        s_row = (unsigned long long)hi;  // no row of the chunk qualifies: the next chunk's first
+        s_run = s_base[b];
+      }
+      __syncthreads();
+      const u32* kc = T->col[key];
+      for (i64 r0 = lo; r0 < hi; r0 += 1024) {
+        const i64 r = r0 + tid;
+        const u64 c = r < hi ? seg_lookup(R, __ldg(kc + r)).y : 0;
+        u64 y = c;  // block-wide inclusive scan of the rows' counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u64 z = __shfl_up_sync(0xffffffffu, y, o);
+          if (lane >= o) y += z;
+        }
+        if (lane == 31) s_w[warp] = y;
+        __syncthreads();
+        u64 off = 0;
+        for (int w = 0; w < warp; w++) off += s_w[w];
+        u64 all = 0;
+        for (int w = 0; w < 32; w++) all += s_w[w];
+        const u64 xr = s_run + off + y - c;  // exclusive prefix of row r
+        if (r < hi && slice_owner(xr, E, parts) >= q) atomicMin(&s_row, (unsigned long long)r);
+        __syncthreads();
+        if (tid == 0) s_run += all;
+        __syncthreads();
+        if (s_row < (unsigned long long)hi) break;
+      }
+      bound[b] = (i64)s_row;
+      __syncthreads();
+    }
   }
-  if (c_lo) atomicAdd(&s_lo, c_lo);
-  if (c_hi) atomicAdd(&s_hi, c_hi);
-  __syncthreads();
   if (tid == 0) {
-    i64 lo, hi;
-    if (E > 0) {
-      lo = (i64)((__int128)n * (i64)s_lo / nch);
-      hi = (i64)((__int128)n * (i64)s_hi / nch);
-    } else {
-      lo = (i64)((__int128)n * part / parts);
-      hi = (i64)((__int128)n * (part + 1) / parts);
-    }
+    const i64 lo = bound[0], hi = bound[1] > bound[0] ? bound[1] : bound[0];
     for (int c = 0; c < a; c++) T->col[c] += lo;
     T->n = hi - lo;
     st->rows = hi - lo;
@@ -2834,7 +2892,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       GSM_CUDA(launch(c->use_pdl, k_slice_sums, (int)std::max<i64>(1, std::min<i64>(c->grid_ts, (nch + 7) / 8)),
                       256, st, (const DTable*)(dT + ex.plan[0].out_table), slice_key, slice_R, c->d_slice));
       GSM_CUDA(launch(c->use_pdl, k_slice_pick, 1, 1024, st, dT + ex.plan[0].out_table,
-                      (int)ex.plan[0].schema.size(), part, parts, dS + 0, (const u64*)c->d_slice));
+                      (int)ex.plan[0].schema.size(), part, parts, dS + 0, (const u64*)c->d_slice,
+                      slice_key, slice_R));
       nk += 2;
     } else if (parts > 1) {
       GSM_CUDA(launch(c->use_pdl, k_slice, 1, 64, st, dT + ex.plan[0].out_table,

@@ -318,7 +318,9 @@ def execute_summary(query, plan, store, mode: str = "gpu", row_budget: int = DEF
                             report, "summary", parts0)
 
 
-_MAX_PARTS = 4096  # the first table is cut at 1/4096-of-E granularity (k_slice_pick)
+# slices are row-granular (k_slice_pick), so splitting stops only when one
+# first-table row's own chain outgrows the device
+_MAX_PARTS = 1 << 30
 _NO_BUDGET = (1 << 63) - 1
 
 

@@ -64,6 +64,6 @@ def test_fingerprint_rows_matches_oracle():
 
 def test_chunk_counts_are_powers_of_two():
     assert [ex._pow2(k) for k in (1, 2, 3, 5, 64, 65)] == [1, 2, 4, 8, 64, 128]
-    assert ex._pow2(10**9) == ex._MAX_PARTS
+    assert ex._pow2(10**12) == ex._MAX_PARTS
     with pytest.raises(ValueError):
         ex._pow2(0)

@@ -178,3 +178,16 @@ def test_batch_falls_back_to_chunks(capped):
     for (q, p), r in zip(items, res):
         one = g.execute(q, p, capped, row_budget=1 << 62)
         assert _bag(one.array) == _bag(r.array)
+
+
+def test_row_granular_chunks_beyond_the_chunk_table(full):
+    """More left-row chunks than k_slice_sums' 4096 chunks (and than first-
+    table rows): row-granular equal-E slices still tile the table exactly."""
+    q, plan = _plan(full, PROBE)
+    r1, r2 = g.ExecutionReport(), g.ExecutionReport()
+    a = g.execute(q, plan, full, row_budget=1 << 62, report=r1)
+    b = g.execute(q, plan, full, row_budget=1 << 62, report=r2, chunks=16384)
+    assert r1.steps[0].rows < 16384
+    assert r2.chunks == 16384
+    assert np.array_equal(a.array, b.array)  # slices concatenated in first-table order
+    assert [s.rows for s in r1.steps] == [s.rows for s in r2.steps]
