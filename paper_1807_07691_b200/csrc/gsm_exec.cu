@@ -903,6 +903,12 @@ struct FilterP {
 // ---------------------------------------------------------------------------
 constexpr int MAXF = 8;              // filters on each side of the expand
 constexpr u32 FUSE_MAX_FANOUT = 4;   // post-expand filters fuse only below this fan-out
+// A fused intersection evaluates every candidate of a row inside the block
+// that owns the row: a hub row of 10^5 candidates (each a search of the
+// closing run) then runs alone on one SM long after the rest (T4 skew store:
+// 17 ms for a 2.9M-row expand).  Above this longest run the expand is
+// materialised instead and the filter kernel spreads its rows evenly.
+constexpr u32 INTERSECT_MAX_FANOUT = 1u << 14;
 constexpr int MAXGS = 2 * MAXF + 1;  // steps in a group
 
 struct FSpec {
@@ -1972,6 +1978,7 @@ struct gsm_context {
   bool use_defer = true;   // spread hub rows over all SMs (k_drain)
   bool use_proj_fusion = true;  // write the projected result from the last join
   bool use_batch_graph = true;  // a repeated batch replays as one graph (gsm_execute_batch)
+  bool batch_poll = true;       // complete batch members as their branches finish (GSM_BATCH_POLL=0: one wait)
   int tile_items = 0;           // expand tile rows per thread: 0 = by size, 1 or 2 (GSM_TILE_ITEMS)
   // post filters also fuse into an expand expected to output at least this
   // many rows (left rows x average run), whatever its fan-out, unless its
@@ -2238,6 +2245,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* nd = getenv("GSM_NO_DEFER")) c->use_defer = !(nd[0] == '1');
   if (const char* npf = getenv("GSM_NO_PROJ_FUSION")) c->use_proj_fusion = !(npf[0] == '1');
   if (const char* nb = getenv("GSM_NO_BATCH_GRAPH")) c->use_batch_graph = !(nb[0] == '1');
+  if (const char* bp = getenv("GSM_BATCH_POLL")) c->batch_poll = !(bp[0] == '0');
   if (const char* fh = getenv("GSM_FUSE_HUGE")) c->fuse_huge = std::max<i64>(1, atoll(fh));
   if (const char* ti = getenv("GSM_TILE_ITEMS")) c->tile_items = std::min(2, std::max(0, atoi(ti)));
   if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
@@ -2572,7 +2580,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           join = g_npost < MAXF && (g_x_fanout <= FUSE_MAX_FANOUT ||
                                     (g_x_est >= c->fuse_huge && g_x_fanout <= 64 * std::max<i64>(1, g_x_avg)) ||
                                     (c->use_intersect && g_npost < HOIST && jv[0] != g_x_var &&
-                                     g_x_fanout < (1u << 23)));
+                                     g_x_fanout < INTERSECT_MAX_FANOUT));
         else join = g_npre < MAXF;
       }
       if (!join) {
@@ -3655,7 +3663,10 @@ static gsm_status batch_impl(gsm_context* const* ctxs, int32_t n_queries, const 
     }
     done[i] = 1;
   };
-  if (as_graph && n_queries > 0) {
+  if (as_graph && n_queries > 0 && !ctxs[0]->batch_poll) {  // one wait for the whole graph
+    GSM_CUDA(cudaStreamSynchronize(ctxs[0]->stream));
+    for (int i = 0; i < n_queries; i++) S[i].synced = true;
+  } else if (as_graph && n_queries > 0) {
     // Complete each query as soon as its own branch of the graph is done
     // (its external event fired), while the other branches still run: the
     // budget checks and the copy of its rows overlap the rest of the batch.

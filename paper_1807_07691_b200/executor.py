@@ -274,6 +274,9 @@ class ResultSummary:
 
 
 _M64 = (1 << 64) - 1
+# GSM_BATCH_INTO=0: execute_batch copies every result after the whole batch
+# (A/B of the in-flight copy; tools/e2e_ab.py)
+_BATCH_INTO = os.environ.get("GSM_BATCH_INTO", "1") != "0"
 
 
 def fingerprint_rows(a: np.ndarray) -> tuple[int, int, int]:
@@ -659,7 +662,7 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
     # results: each query's rows are copied into their slice as soon as the
     # query finishes (gsm_execute_batch_into), overlapping the rest of the
     # batch; a result that outgrew its slice is copied afterwards.
-    caps = prep.caps
+    caps = prep.caps if _BATCH_INTO else None
     buf = np.empty(prep.total_cap, dtype=np.uint32)
     base = buf.ctypes.data
     dsts = prep.dsts

@@ -113,7 +113,7 @@ def main():
     tmp = tempfile.mkdtemp(prefix="gsm_scale_")
     store_dir = args.store or f"{tmp}/{args.kind}"
     t0 = time.perf_counter()
-    if not args.store:
+    if not args.store or not Path(args.store, "meta").exists():  # --store DIR: generated once
         gen = [str(REPO / "oracle/_build/gsmgen"), args.kind, "--seed", str(args.seed),
                "--out", store_dir]
         if args.kind == "lubm":
