@@ -1979,6 +1979,14 @@ struct gsm_context {
   bool use_proj_fusion = true;  // write the projected result from the last join
   bool use_batch_graph = true;  // a repeated batch replays as one graph (gsm_execute_batch)
   bool batch_poll = true;       // complete batch members as their branches finish (GSM_BATCH_POLL=0: one wait)
+  // Adaptive grids: a plan's persistent grids are sized from host-side upper
+  // bounds on its tables' rows until it has run once; then from the rows it
+  // actually produced (x2 headroom) and its graph is captured again.  Any
+  // grid is correct (blocks take tiles from a counter), but a 592-block grid
+  // over 20 tiles pays 592 tile-counter atomics, 592 last-block atomics and
+  // SM slots other queries of a batch need (GSM_NO_ROW_HINTS=1: off).
+  bool use_row_hints = true;
+  std::unordered_map<std::string, std::vector<i64>> row_hints;  // plan key -> rows per step
   int tile_items = 0;           // expand tile rows per thread: 0 = by size, 1 or 2 (GSM_TILE_ITEMS)
   // post filters also fuse into an expand expected to output at least this
   // many rows (left rows x average run), whatever its fan-out, unless its
@@ -2215,6 +2223,14 @@ struct Exec {
     ub[t] = d.n;
     return t;
   }
+  // Rows to size a grid for: table t's upper bound, or (once the plan has
+  // run) twice the rows step `step` produced then, whichever is smaller.
+  const std::vector<i64>* hint = nullptr;
+  i64 hinted(int t, int step) const {
+    i64 r = ub[t];
+    if (hint && step >= 0 && step < (int)hint->size()) r = std::min(r, 2 * (*hint)[step] + 1);
+    return r;
+  }
   // Persistent-grid size for a kernel whose input has at most `rows` rows.
   int grid_for_rows(i64 rows, int per_block) const {
     i64 g = (rows + per_block - 1) / per_block;
@@ -2246,6 +2262,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* npf = getenv("GSM_NO_PROJ_FUSION")) c->use_proj_fusion = !(npf[0] == '1');
   if (const char* nb = getenv("GSM_NO_BATCH_GRAPH")) c->use_batch_graph = !(nb[0] == '1');
   if (const char* bp = getenv("GSM_BATCH_POLL")) c->batch_poll = !(bp[0] == '0');
+  if (const char* rh = getenv("GSM_NO_ROW_HINTS")) c->use_row_hints = !(rh[0] == '1');
   if (const char* fh = getenv("GSM_FUSE_HUGE")) c->fuse_huge = std::max<i64>(1, atoll(fh));
   if (const char* ti = getenv("GSM_TILE_ITEMS")) c->tile_items = std::min(2, std::max(0, atoi(ti)));
   if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
@@ -2425,6 +2442,7 @@ static std::string query_key(gsm_context* c, const QueryArgs& qa, ExecState& S) 
   S.plan_key = key;
   key.append(reinterpret_cast<const char*>(&c->guess), sizeof c->guess);
   key.push_back(S.big ? 'B' : 'S');
+  key.push_back(c->use_row_hints && c->row_hints.count(S.plan_key) ? 'H' : 'U');  // grids from rows seen
   return key;
 }
 
@@ -2455,7 +2473,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // Prepared plan: replay the captured launch sequence with the saved
   // query-block image and fresh epochs — no re-planning on the host.
   // (Seeded queries read a caller buffer: never cached.)
-  const bool graphs = c->use_graphs && qa.seed_k < 0 && !S.capture_only;
+  // (a left-row chunk of many is run once: not worth a capture)
+  const bool graphs = c->use_graphs && qa.seed_k < 0 && !S.capture_only && qa.parts < 64;
   if (graphs) {
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
@@ -2468,6 +2487,10 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   ex.c = c;
   ex.steps = steps;
   ex.n = n;
+  if (c->use_row_hints) {
+    auto rh = c->row_hints.find(S.plan_key);
+    if (rh != c->row_hints.end()) ex.hint = &rh->second;
+  }
   ex.hb = hb;
   ex.half = c->arena_bytes / 2;
   ex.plan.assign(n, StepPlan());
@@ -2687,8 +2710,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       L.items = c->tile_items > 0 ? c->tile_items
                                   : (lub >= (i64)16 * c->grid_ts * TS_TILE && avg_run <= 16 ? 2 : 1);
     }
-    L.grid = L.kind == S_CROSS ? ex.grid_for_rows(ex.ub[L.out], 256)
-                               : ex.grid_for_rows(lub, TS_TILE * L.items);
+    L.grid = L.kind == S_CROSS ? ex.grid_for_rows(ex.hinted(L.out, s), 256)
+                               : ex.grid_for_rows(ex.hinted(cur, s - 1), TS_TILE * L.items);
     ex.plan[s].kind = L.kind;
     ex.plan[s].schema = out_schema;
     ex.plan[s].out_table = L.out;
@@ -2988,7 +3011,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       // DISTINCT reads the packed rows on the device, so only plain
       // projections are packed straight into the pinned staging buffer.
       u32* host_dst = distinct ? nullptr : stage_rows;
-      GSM_CUDA(launch(c->use_pdl, k_pack, ex.grid_for_rows(ex.ub[cur], 256), 256, st,
+      GSM_CUDA(launch(c->use_pdl, k_pack, ex.grid_for_rows(ex.hinted(cur, n - 1), 256), 256, st,
                       (const DTable*)(dT + cur), pa, n_proj, pack_out, pack_cap, host_dst,
                       stage_cap, dS + pack_stat, xlast));
       nk++;
@@ -3220,6 +3243,12 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
   }
 
   const QueryBlock* hb = c->h_block;
+  if (c->use_row_hints && !c->row_hints.count(plan_key)) {
+    if (c->row_hints.size() > 4096) c->row_hints.clear();
+    std::vector<i64> rows((size_t)n);
+    for (int s = 0; s < n; s++) rows[s] = hb->stats[s].rows;
+    c->row_hints.emplace(plan_key, std::move(rows));
+  }
   if (rep) {
     for (int s = 0; s < n; s++) {
       StepKind k = (StepKind)S.kinds[s];

@@ -270,12 +270,12 @@ def test_execution_variants_agree(store_factory):
         "    q = g.bind_constants(g.parse_query(text), st.dictionary)\n"
         "    p = g.make_plan(q, st.stats)\n"
         "    runs = []\n"
-        "    for _ in range(2):\n"
+        "    for _ in range(3):  # capture, re-capture with grids from the rows seen, replay\n"
         "        rep = g.ExecutionReport()\n"
         "        r = g.execute(q, p, st, report=rep, row_budget=1 << 62)\n"
         "        runs.append([[str(v) for v in orc.fingerprint_array(r.array)],\n"
         "                     [s.rows for s in rep.steps], [s.prealloc_total for s in rep.steps]])\n"
-        "    assert runs[0] == runs[1]\n"
+        "    assert runs[0] == runs[1] == runs[2]\n"
         "    out.append(runs[0])\n"
         "print(json.dumps(out))\n" % (str(GOLDEN.parents[1]), str(GOLDEN.parent), str(d))
     )
@@ -286,6 +286,7 @@ def test_execution_variants_agree(store_factory):
     # the device paths
     for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION", "GSM_NO_DEFER",
                     "GSM_NO_PROJ_FUSION", "GSM_NO_BATCH_GRAPH", "GSM_STAGE_MAX=65536", "GSM_TILE_ITEMS=2", "GSM_FUSE_HUGE=1", "GSM_NO_INTERSECT",
+                    "GSM_NO_ROW_HINTS",
                     "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER,GSM_NO_PROJ_FUSION"):
         env = dict(os.environ)
         for item in filter(None, variant.split(",")):
