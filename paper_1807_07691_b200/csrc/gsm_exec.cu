@@ -126,11 +126,24 @@ __device__ void defer_row(const P& p, const DTable& s, const ChunkQueue& q, i64 
 // head of the result buffer, so the host reads counters and result rows with
 // ONE device->host copy.  "Last block" detection: every block bumps a counter
 // after its own counter updates; the block that sees gridDim.x - 1 copies.
+//
+// Self-cleaning query block (img != null): after the export the same block
+// restores the whole query block from the plan's device image and takes the
+// next replay's look-back epochs from the context's epoch counter — what
+// k_init does at the start of a query, done at the end of the previous one
+// instead, so a replay of the same plan on the same context (a prepared
+// statement, a repeated batch) needs no k_init launch in front of its joins.
 struct ExportArgs {
   const StepStat* src = nullptr;
   StepStat* dst = nullptr;  // null: this kernel is not the query's last
   int n = 0;
   u32* done = nullptr;
+  const uint4* img = nullptr;  // self-cleaning: the plan's query-block image
+  uint4* blk = nullptr;        // ... the context's query block
+  int words16 = 0;
+  u32* ctr = nullptr;          // context epoch counter
+  u32* epochs = nullptr;       // the block's epoch slots
+  int n_epochs = 0;
 };
 __device__ __forceinline__ void export_if_last(const ExportArgs& x) {
   if (!x.dst) return;
@@ -146,6 +159,16 @@ __device__ __forceinline__ void export_if_last(const ExportArgs& x) {
     const volatile i64* src = reinterpret_cast<const volatile i64*>(x.src);
     i64* dst = reinterpret_cast<i64*>(x.dst);
     for (int i = threadIdx.x; i < x.n * 4; i += blockDim.x) dst[i] = src[i];
+    if (x.img) {
+      __syncthreads();  // the counters are exported before the block is reset
+      for (int w = threadIdx.x; w < x.words16; w += blockDim.x) x.blk[w] = x.img[w];
+      __syncthreads();
+      if (threadIdx.x == 0 && x.n_epochs > 0) {
+        const u32 base = *x.ctr;
+        for (int e = 0; e < x.n_epochs; e++) x.epochs[e] = base + 1 + (u32)e;
+        *x.ctr = base + (u32)x.n_epochs;
+      }
+    }
   }
 }
 
@@ -554,6 +577,28 @@ struct ExpandP {
     u32* ob = out + pos;  // column cc of output slot pos + j is ob[cc * cap + j]
     const i64 lim = min(c, cap - pos);
     if (lim <= 0) return;
+    if ((((uintptr_t)out | (uintptr_t)(cap * 4)) & 15) != 0) {
+      // columns not 16-byte aligned (table-level joins size them exactly):
+      // 32-bit coalesced stores
+      for (i64 j0 = 0; j0 < lim; j0 += 32 * U) {
+        u32 v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const i64 j = j0 + 32 * u + lane;
+          v[u] = j < lim ? __ldg(src + j) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const i64 j = j0 + 32 * u + lane;
+          if (j < lim) {
+#pragma unroll
+            for (int cc = 0; cc < A; cc++) ob[(i64)cc * cap + j] = lv[cc];
+            ob[(i64)A * cap + j] = v[u];
+          }
+        }
+      }
+      return;
+    }
     const int h = (int)min((i64)((4 - (pos & 3)) & 3), lim);  // head: scalar
     if (lane < h) {
 #pragma unroll
@@ -1466,7 +1511,8 @@ struct ResolveArgs {
 // that the host mirrors (reserve_epochs), so tile status words never need
 // re-zeroing between launches.
 __global__ void k_init(const uint4* __restrict__ src, uint4* __restrict__ dst, int words16, u32* ctr,
-                       u32* epochs, int n_epochs, ResolveArgs res, DTable* tables, StepStat* stats) {
+                       u32* epochs, int n_epochs, ResolveArgs res, DTable* tables, StepStat* stats,
+                       DTable* img_tables, StepStat* img_stats) {
   pdl_wait();
   pdl_trigger();
   // The three parts are independent chains of (cold, after an L2 flush)
@@ -1495,6 +1541,13 @@ __global__ void k_init(const uint4* __restrict__ src, uint4* __restrict__ dst, i
   if (jb.kind == J_SEG) tables[jb.table].col[0] = const_cast<u32*>(jb.R.dst) + sg.x;
   tables[jb.table].n = n;
   if (jb.stat >= 0) stats[jb.stat].rows = n;
+  // the store is immutable: the resolved scans go into the plan's image too,
+  // so self-cleaning replays (no k_init) find them already in the block
+  if (img_tables) {
+    if (jb.kind == J_SEG) img_tables[jb.table].col[0] = const_cast<u32*>(jb.R.dst) + sg.x;
+    img_tables[jb.table].n = n;
+    if (jb.stat >= 0) img_stats[jb.stat].rows = n;
+  }
 }
 
 // Multi-GPU row partitioning of the first table: keep rows [n*i/k, n*(i+1)/k).
@@ -1986,6 +2039,7 @@ struct gsm_context {
   // over 20 tiles pays 592 tile-counter atomics, 592 last-block atomics and
   // SM slots other queries of a batch need (GSM_NO_ROW_HINTS=1: off).
   bool use_row_hints = true;
+  bool use_self_clean = true;  // GSM_NO_SELF_CLEAN=1: every replay starts with k_init
   std::unordered_map<std::string, std::vector<i64>> row_hints;  // plan key -> rows per step
   int tile_items = 0;           // expand tile rows per thread: 0 = by size, 1 or 2 (GSM_TILE_ITEMS)
   // post filters also fuse into an expand expected to output at least this
@@ -2009,6 +2063,12 @@ struct gsm_context {
     i64 h2d = 0;
     bool zc = false;
     char* d_image = nullptr;  // device copy of `image` (k_init's source)
+    // Self-cleaning plans (graphs, no DISTINCT tail): the last kernel
+    // restores the query block from d_image, so `warm` — the same sequence
+    // without k_init — replays while this image is the one installed.
+    bool self_clean = false;
+    u64 image_id = 0;                  // process-unique id of d_image's contents
+    cudaGraphExec_t warm = nullptr;
     std::vector<int> kinds, arities, fused_in;
   };
   std::unordered_map<std::string, GraphEntry> graphs;
@@ -2019,6 +2079,7 @@ struct gsm_context {
   // context's buffers are unchanged (bufgen).
   struct BatchEntry {
     cudaGraphExec_t exec = nullptr;
+    cudaGraphExec_t warm = nullptr;  // every member without k_init (all installed)
     std::vector<u64> bufgens;
     std::vector<GraphEntry> metas;  // per query (exec unused)
   };
@@ -2029,6 +2090,9 @@ struct gsm_context {
   // branch of a batch graph: the host completes each query as soon as its
   // own branch is done, while the rest of the batch still runs.
   cudaEvent_t ev_ext = nullptr;
+  // image_id of the self-cleaning plan whose image the query block holds
+  // (left clean by that plan's last kernel); 0 = unknown / dirty
+  u64 installed = 0;
 };
 
 namespace gsm {
@@ -2045,8 +2109,14 @@ u64 next_bufgen() {
   return ++g;
 }
 
+u64 next_image_id() {
+  static std::atomic<u64> g{0};
+  return ++g;
+}
+
 void free_batch(gsm_context::BatchEntry& b) {
   cudaGraphExecDestroy(b.exec);
+  if (b.warm) cudaGraphExecDestroy(b.warm);
   for (auto& m : b.metas)
     if (m.d_image) cudaFree(m.d_image);
 }
@@ -2054,8 +2124,10 @@ void free_batch(gsm_context::BatchEntry& b) {
 void ctx_clear_graphs(gsm_context* c) {
   for (auto& kv : c->graphs) {
     cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.warm) cudaGraphExecDestroy(kv.second.warm);
     if (kv.second.d_image) cudaFree(kv.second.d_image);
   }
+  c->installed = 0;
   c->graphs.clear();
   for (auto& kv : c->batches) free_batch(kv.second);
   c->batches.clear();
@@ -2263,6 +2335,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* nb = getenv("GSM_NO_BATCH_GRAPH")) c->use_batch_graph = !(nb[0] == '1');
   if (const char* bp = getenv("GSM_BATCH_POLL")) c->batch_poll = !(bp[0] == '0');
   if (const char* rh = getenv("GSM_NO_ROW_HINTS")) c->use_row_hints = !(rh[0] == '1');
+  if (const char* sc = getenv("GSM_NO_SELF_CLEAN")) c->use_self_clean = !(sc[0] == '1');
   if (const char* fh = getenv("GSM_FUSE_HUGE")) c->fuse_huge = std::max<i64>(1, atoll(fh));
   if (const char* ti = getenv("GSM_TILE_ITEMS")) c->tile_items = std::min(2, std::max(0, atoi(ti)));
   if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
@@ -2397,6 +2470,7 @@ struct ExecState {
   // issue the launch sequence into it and describe it in `meta`.
   bool capture_only = false;
   char* pre_image = nullptr;  // batch capture: the d_image buffer to use
+  bool warm_capture = false;  // batch capture: issue the sequence without k_init
   bool zc = false;            // counters and result rows written straight to pinned host memory
   bool big = false;           // this plan's last result outgrew the staging buffer
   gsm_context::GraphEntry meta;
@@ -2406,8 +2480,14 @@ struct ExecState {
 
 // Restore a prepared plan into the context: query-block image with fresh
 // epochs, and the host-side facts the completion needs.
-static void apply_entry(gsm_context* c, const gsm_context::GraphEntry& P, ExecState& S) {
-  reserve_epochs(c, P.n_epochs);  // k_init takes them on the device
+// Epochs a replay takes from the device counter: k_init's (install
+// variant) plus, for a self-cleaning plan, the next replay's at its end.
+static int replay_epochs(const gsm_context::GraphEntry& P, bool warm) {
+  return warm ? P.n_epochs : (P.self_clean ? 2 * P.n_epochs : P.n_epochs);
+}
+static void apply_entry(gsm_context* c, const gsm_context::GraphEntry& P, ExecState& S,
+                        bool warm = false) {
+  reserve_epochs(c, replay_epochs(P, warm));
   S.zc = P.zc;
   S.pack_stat = P.pack_stat;
   S.pack_cap = P.pack_cap;
@@ -2478,12 +2558,17 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   if (graphs) {
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
-      apply_entry(c, it->second, S);
-      GSM_CUDA(cudaGraphLaunch(it->second.exec, st));
+      const gsm_context::GraphEntry& P = it->second;
+      const bool warm = P.warm && c->installed == P.image_id;
+      apply_entry(c, P, S, warm);
+      if (warm) kernels--;  // no k_init
+      GSM_CUDA(cudaGraphLaunch(warm ? P.warm : P.exec, st));
+      c->installed = P.self_clean ? P.image_id : 0;
       count_launch(kernels);
       return GSM_OK;
     }
   }
+  c->installed = 0;  // the block is about to be rewritten by a fresh plan
   ex.c = c;
   ex.steps = steps;
   ex.n = n;
@@ -2870,8 +2955,10 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       n_epoch_slots++;
   // k_init takes them from the device counter; mirror it (any wrap-around
   // re-zeroing is enqueued here, before a capture starts — a batch capture
-  // made room beforehand, epoch_headroom)
-  reserve_epochs(c, n_epoch_slots);
+  // made room beforehand, epoch_headroom).  A self-cleaning plan's last
+  // kernel takes the next replay's epochs as well.
+  const bool self_clean = c->use_self_clean && (graphs || S.capture_only) && !distinct && qa.seed_k < 0;
+  reserve_epochs(c, self_clean ? 2 * n_epoch_slots : n_epoch_slots);
   ProjArgs pa{};
   for (int j = 0; j < n_proj; j++) pa.col[j] = pj_idx[j];
   const size_t used = offsetof(QueryBlock, tables) + sizeof(DTable) * (size_t)ex.ntables;
@@ -2900,17 +2987,23 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     return capturing ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
                      : cudaEventRecord(ev, st);
   };
-  auto issue = [&]() -> gsm_status {
+  // warm: the self-cleaning variant without k_init (the block already holds
+  // this plan's image, left clean by its previous replay)
+  auto issue = [&](bool warm) -> gsm_status {
     int nk = 0;
     if (timing) GSM_CUDA(record(c->ev_q0));
     // the query block: a replayed graph copies its device image in k_init;
     // otherwise it is uploaded here
     if (!d_image) GSM_CUDA(cudaMemcpyAsync(c->d_block, hb, used, cudaMemcpyHostToDevice, st));
     if (timing) GSM_CUDA(record(c->ev[0]));  // step 0 (scan) = k_init's constant resolution
-    GSM_CUDA(launch(c->use_pdl, k_init, 1, 256, st, reinterpret_cast<const uint4*>(d_image),
-                    reinterpret_cast<uint4*>(c->d_block), d_image ? (int)((used + 15) / 16) : 0, c->d_ctr,
-                    c->d_block->epochs, n_epoch_slots, ex.res, dT, dS));
-    nk++;
+    if (!warm) {
+      QueryBlock* img = reinterpret_cast<QueryBlock*>(d_image);
+      GSM_CUDA(launch(c->use_pdl, k_init, 1, 256, st, reinterpret_cast<const uint4*>(d_image),
+                      reinterpret_cast<uint4*>(c->d_block), d_image ? (int)((used + 15) / 16) : 0, c->d_ctr,
+                      c->d_block->epochs, n_epoch_slots, ex.res, dT, dS,
+                      img ? img->tables : nullptr, img ? img->stats : nullptr));
+      nk++;
+    }
     if (qa.seed_k > 0 && qa.seed_n > 0) {
       const i64 cells = qa.seed_n * qa.seed_k;
       k_rows_to_cols<<<(int)std::max<i64>(1, std::min<i64>(c->grid_ts, (cells + 255) / 256)), 256, 0, st>>>(
@@ -2933,8 +3026,17 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     }
     if (timing) GSM_CUDA(record(c->ev[1]));
     // the query's last kernel exports the step counters to the stage head
-    const ExportArgs xlast{dS, reinterpret_cast<StepStat*>(S.zc ? c->hd_stage : c->d_stage), n + 1,
-                           c->d_block->done};
+    // (and, self-cleaning, restores the block for the next replay)
+    ExportArgs xlast{dS, reinterpret_cast<StepStat*>(S.zc ? c->hd_stage : c->d_stage), n + 1,
+                     c->d_block->done};
+    if (self_clean) {
+      xlast.img = reinterpret_cast<const uint4*>(d_image);
+      xlast.blk = reinterpret_cast<uint4*>(c->d_block);
+      xlast.words16 = (int)((used + 15) / 16);
+      xlast.ctr = c->d_ctr;
+      xlast.epochs = c->d_block->epochs;
+      xlast.n_epochs = n_epoch_slots;
+    }
     int last_launch = -1;
     for (int i = (int)launches.size() - 1; i >= 0 && fused; i--)
       if (launches[i].kind != S_EMPTY) {
@@ -3036,11 +3138,13 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   }
   if (S.capture_only) {  // the caller's capture records the sequence
     capturing = true;
-    gsm_status is = issue();
+    const bool w = S.warm_capture && self_clean;
+    gsm_status is = issue(w);
     capturing = false;
     if (is != GSM_OK) return is;
     gsm_context::GraphEntry& P = S.meta;
-    P.kernels = kernels;
+    P.kernels = kernels + (w ? 1 : 0);  // counted with k_init
+    P.self_clean = self_clean;
     P.image.assign(reinterpret_cast<const char*>(hb), reinterpret_cast<const char*>(hb) + used);
     P.n_epochs = n_epoch_slots;
     P.pack_stat = pack_stat;
@@ -3059,25 +3163,32 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     cudaGraphExec_t ge = nullptr;
     {
       if (c->graphs.size() >= 1024) ctx_clear_graphs(c);
-      GSM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      capturing = true;
-      gsm_status is = issue();
-      capturing = false;
-      cudaGraph_t g = nullptr;
-      cudaError_t ce = cudaStreamEndCapture(st, &g);
-      if (is != GSM_OK || ce != cudaSuccess) {
+      // the install variant (k_init first) and, self-cleaning, the warm one
+      cudaGraphExec_t gw = nullptr;
+      int nk_install = 0;
+      for (int v = 0; v < (self_clean ? 2 : 1); v++) {
+        GSM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
+        gsm_status is = issue(v == 1);
+        capturing = false;
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(st, &g);
+        cudaGraphExec_t* dst = v == 0 ? &ge : &gw;
+        if (is == GSM_OK && ce == cudaSuccess) ce = cudaGraphInstantiate(dst, g, 0);
         if (g) cudaGraphDestroy(g);
-        cudaFree(d_image);
-        return is != GSM_OK ? is : cuda_error(ce, "cudaStreamEndCapture");
+        if (is != GSM_OK || ce != cudaSuccess) {
+          if (ge) cudaGraphExecDestroy(ge);
+          cudaFree(d_image);
+          return is != GSM_OK ? is : cuda_error(ce, "graph capture");
+        }
+        if (v == 0) nk_install = kernels;
       }
-      ce = cudaGraphInstantiate(&ge, g, 0);
-      cudaGraphDestroy(g);
-      if (ce != cudaSuccess) {
-        cudaFree(d_image);
-        return cuda_error(ce, "cudaGraphInstantiate");
-      }
+      kernels = nk_install;
       gsm_context::GraphEntry P;
       P.exec = ge;
+      P.warm = gw;
+      P.self_clean = self_clean;
+      P.image_id = next_image_id();
       P.kernels = kernels;
       P.image.assign(reinterpret_cast<const char*>(hb), reinterpret_cast<const char*>(hb) + used);
       P.n_epochs = n_epoch_slots;
@@ -3091,11 +3202,14 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       P.kinds = S.kinds;
       P.arities = S.arities;
       P.fused_in = S.fused_in;
+      c->installed = 0;
+      const u64 id = P.image_id;
       c->graphs.emplace(key, std::move(P));
+      GSM_CUDA(cudaGraphLaunch(ge, st));
+      c->installed = self_clean ? id : 0;
     }
-    GSM_CUDA(cudaGraphLaunch(ge, st));
   } else {
-    gsm_status is = issue();
+    gsm_status is = issue(false);
     if (is != GSM_OK) return is;
   }
   count_launch(kernels);
@@ -3328,7 +3442,7 @@ static gsm_status complete_query(gsm_context* c, const QueryArgs& qa, ExecState&
     GSM_CUDA(cudaMemsetAsync(c->d_block->counters + GSM_MAX_STEPS + 2, 0, 4, st));
     reserve_epochs(c, 1);
     k_init<<<1, 32, 0, st>>>(nullptr, nullptr, 0, c->d_ctr, c->d_block->epochs + GSM_MAX_STEPS + 2, 1,
-                             ResolveArgs{}, nullptr, nullptr);
+                             ResolveArgs{}, nullptr, nullptr, nullptr, nullptr);
     count_launch();
     kernels++;
     TileSync ts{c->d_status, c->d_block->counters + GSM_MAX_STEPS + 2,
@@ -3457,8 +3571,8 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     if (validate_query(ctxs[i], qa[i]) != GSM_OK) return false;
   }
   if (cudaSetDevice(c0->device) != cudaSuccess) return false;
-  for (int i = 0; i < n; i++)
-    if (epoch_headroom(ctxs[i], GSM_MAX_STEPS + 4) != GSM_OK) return false;
+  for (int i = 0; i < n; i++)  // install + the self-cleaning end: 2 x the launches' epochs
+    if (epoch_headroom(ctxs[i], 2 * (GSM_MAX_STEPS + 4)) != GSM_OK) return false;
   std::string bkey;
   std::vector<std::string> keys((size_t)n);
   for (int i = 0; i < n; i++) {
@@ -3471,6 +3585,7 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     bkey += keys[i];
   }
   cudaStream_t s0 = c0->stream;
+  bool use_warm = false;
   auto it = c0->batches.find(bkey);
   if (it != c0->batches.end()) {
     bool ok = true;
@@ -3501,12 +3616,17 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
         drop_imgs();
         return false;
       }
+    // Two captures of the batch: with every member's k_init (installs the
+    // query blocks), and the warm one in which self-cleaning members skip it.
+    cudaGraphExec_t gx[2] = {nullptr, nullptr};
+    bool ok = true;
+    for (int v = 0; v < 2 && ok; v++) {
     if (cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
-      drop_imgs();
-      return false;
+      ok = false;
+      break;
     }
-    bool ok = cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
+    ok = cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
     int forked = 1;  // streams joined to the capture (ctxs[0]'s is the origin)
     for (; forked < n && ok; forked++) ok = cudaStreamWaitEvent(ctxs[forked]->stream, c0->ev_fork, 0) == cudaSuccess;
     if (!ok) forked--;
@@ -3518,9 +3638,11 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       const bool pdl = ctxs[i]->use_pdl;
       ctxs[i]->use_pdl = false;
       S[i].capture_only = true;
+      S[i].warm_capture = v == 1;
       S[i].pre_image = imgs[i];
       ok = launch_query(ctxs[i], qa[i], S[i]) == GSM_OK;
       S[i].capture_only = false;
+      S[i].warm_capture = false;
       ctxs[i]->use_pdl = pdl;
       if (ok)
         ok = cudaEventRecordWithFlags(ctxs[i]->ev_ext, ctxs[i]->stream, cudaEventRecordExternal) ==
@@ -3536,10 +3658,12 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     }
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(s0, &g);
-    cudaGraphExec_t ge = nullptr;
-    if (ok && ce == cudaSuccess && g) ok = cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+    if (ok && ce == cudaSuccess && g) ok = cudaGraphInstantiate(&gx[v], g, 0) == cudaSuccess;
     else ok = false;
     if (g) cudaGraphDestroy(g);
+    }
+    cudaGraphExec_t ge = gx[0];
+    if (!ok && gx[1]) cudaGraphExecDestroy(gx[1]);
     for (int i = 0; i < n && ok; i++)
       ok = cudaMemcpy(imgs[i], S[i].meta.image.data(), S[i].meta.image.size(), cudaMemcpyHostToDevice) ==
            cudaSuccess;
@@ -3555,26 +3679,39 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     }
     gsm_context::BatchEntry E;
     E.exec = ge;
+    E.warm = gx[1];
     for (int i = 0; i < n; i++) {
       E.bufgens.push_back(ctxs[i]->bufgen);
+      S[i].meta.image_id = next_image_id();
       E.metas.push_back(std::move(S[i].meta));
+      S[i].kernels = E.metas[i].kernels;
     }
     it = c0->batches.emplace(bkey, std::move(E)).first;
-    // the capture planned every query: its query-block image is in place
+    // the capture planned every query (epochs reserved for the install run)
     for (int i = 0; i < n; i++) count_launch(S[i].kernels);
+    use_warm = false;
   } else {
+    const gsm_context::BatchEntry& B = it->second;
+    use_warm = B.warm != nullptr;
+    for (int i = 0; i < n && use_warm; i++)
+      if (B.metas[i].self_clean && ctxs[i]->installed != B.metas[i].image_id) use_warm = false;
     for (int i = 0; i < n; i++) {
       ctxs[i]->gen++;
-      apply_entry(ctxs[i], it->second.metas[i], S[i]);
+      const bool w = use_warm && B.metas[i].self_clean;
+      apply_entry(ctxs[i], B.metas[i], S[i], w);
+      if (w) S[i].kernels--;
       count_launch(S[i].kernels);
     }
   }
   if (timed && cudaEventRecord(c0->ev_b0, s0) != cudaSuccess) return false;
   const auto tg0 = std::chrono::steady_clock::now();
-  if (cudaGraphLaunch(it->second.exec, s0) != cudaSuccess) {
+  if (cudaGraphLaunch(use_warm ? it->second.warm : it->second.exec, s0) != cudaSuccess) {
     cudaGetLastError();
+    for (int i = 0; i < n; i++) ctxs[i]->installed = 0;
     return false;
   }
+  for (int i = 0; i < n; i++)
+    ctxs[i]->installed = it->second.metas[i].self_clean ? it->second.metas[i].image_id : 0;
   note_graph_launch(std::chrono::duration<double>(std::chrono::steady_clock::now() - tg0).count());
   if (timed) cudaEventRecord(c0->ev_b1, s0);
   for (int i = 0; i < n; i++) S[i].sync_stream = s0;

@@ -248,8 +248,12 @@ def test_execution_variants_agree(store_factory):
     deferral, projection fusion and the fused run intersection are pure
     optimisations: each query gives the same bag and the same per-step report
     with them switched off (GSM_NO_GRAPHS / GSM_NO_PDL / GSM_NO_FUSION /
-    GSM_NO_DEFER / GSM_NO_PROJ_FUSION / GSM_NO_INTERSECT), a tiny staging buffer (GSM_STAGE_MAX) forces the
-    device-resident result paths, and repeated (replayed) executions agree."""
+    GSM_NO_DEFER / GSM_NO_PROJ_FUSION / GSM_NO_INTERSECT / GSM_NO_ROW_HINTS /
+    GSM_NO_SELF_CLEAN), a tiny staging buffer (GSM_STAGE_MAX) forces the
+    device-resident result paths, and repeated executions agree: the first
+    captures the plan (k_init installs the block), the second re-captures it
+    with grids sized from the rows seen, the third replays the warm variant
+    (no k_init; the block was left clean by the second's last kernel)."""
     import json
     import os
     import subprocess
@@ -286,7 +290,7 @@ def test_execution_variants_agree(store_factory):
     # the device paths
     for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION", "GSM_NO_DEFER",
                     "GSM_NO_PROJ_FUSION", "GSM_NO_BATCH_GRAPH", "GSM_STAGE_MAX=65536", "GSM_TILE_ITEMS=2", "GSM_FUSE_HUGE=1", "GSM_NO_INTERSECT",
-                    "GSM_NO_ROW_HINTS",
+                    "GSM_NO_ROW_HINTS", "GSM_NO_SELF_CLEAN", "GSM_BATCH_POLL=0",
                     "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER,GSM_NO_PROJ_FUSION"):
         env = dict(os.environ)
         for item in filter(None, variant.split(",")):
