@@ -53,7 +53,7 @@ W_ID = 4  # bytes per id
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--univ", type=int, default=10)
@@ -475,6 +475,8 @@ def run_ours(args):
                            "(14 concurrent streams) per GPU",
             "e2e": {"value": round(rows_all / wall_s, 1) if wall_s > 0 else 0.0, "unit": "rows/s",
                     "ms_per_step": round(1e3 * wall_s / args.steps, 4),
+                    "median_ms_per_step": round(1e3 * statistics.median(
+                        st_["wall_batch"] for st_ in steps), 4),
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "sequential": {"value": round(rows_all / dev_seq, 1) if dev_seq > 0 else 0.0,
                            "ms_per_step": round(1e3 * dev_seq / args.steps, 4),
@@ -711,7 +713,8 @@ def run_reference(args):
                                  row_budget=1 << 62, report=rep)
                 lat[name] = time.perf_counter() - tq
                 rows += sum(s.rows for s in rep.steps[1:])
-            return time.perf_counter() - t0, rows, lat
+            el = time.perf_counter() - t0
+            return el, rows, lat
 
         # the reference's two modes (cli.py:40): sequential on one core (its
         # default) and parallel on every host core (GIL-bound thread pool)

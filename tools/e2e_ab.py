@@ -44,7 +44,7 @@ def main():
             if i >= 10:
                 wall.append(t * 1e6)
                 dev.append(bt[0] * 1e6)
-        env = {k: v for k, v in os.environ.items() if k.startswith("GSM_")}
+        env = {k: v for k, v in os.environ.items() if k.startswith(("GSM_", "CUDA_DEVICE_MAX"))}
         print(json.dumps({"env": env, "e2e_us": round(statistics.median(wall), 1),
                           "device_us": round(statistics.median(dev), 1)}))
 
