@@ -2084,8 +2084,14 @@ struct gsm_context {
   // context's buffers are unchanged (bufgen).
   struct BatchEntry {
     cudaGraphExec_t exec = nullptr;
-    cudaGraphExec_t warm = nullptr;  // every member without k_init (all installed)
-    bool resolved = false;           // the install variant ran: images hold the resolved scans
+    // The captured graph (kept: the k_init nodes are toggled in `exec` per
+    // launch with cudaGraphNodeSetEnabled): member i's k_init node, and
+    // whether it is currently enabled.  A self-cleaning member whose context
+    // still holds its image (left clean by its previous replay) runs warm.
+    cudaGraph_t graph = nullptr;
+    std::vector<cudaGraphNode_t> init_node;
+    std::vector<char> init_on;
+    bool resolved = false;  // k_init ran once: the images hold the resolved scans
     std::vector<u64> bufgens;
     std::vector<GraphEntry> metas;  // per query (exec unused)
   };
@@ -2122,7 +2128,7 @@ u64 next_image_id() {
 
 void free_batch(gsm_context::BatchEntry& b) {
   cudaGraphExecDestroy(b.exec);
-  if (b.warm) cudaGraphExecDestroy(b.warm);
+  if (b.graph) cudaGraphDestroy(b.graph);
   for (auto& m : b.metas)
     if (m.d_image) cudaFree(m.d_image);
 }
@@ -2476,7 +2482,6 @@ struct ExecState {
   // issue the launch sequence into it and describe it in `meta`.
   bool capture_only = false;
   char* pre_image = nullptr;  // batch capture: the d_image buffer to use
-  bool warm_capture = false;  // batch capture: issue the sequence without k_init
   bool zc = false;            // counters and result rows written straight to pinned host memory
   bool big = false;           // this plan's last result outgrew the staging buffer
   gsm_context::GraphEntry meta;
@@ -3144,12 +3149,11 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   }
   if (S.capture_only) {  // the caller's capture records the sequence
     capturing = true;
-    const bool w = S.warm_capture && self_clean;
-    gsm_status is = issue(w);
+    gsm_status is = issue(false);  // with k_init: the batch toggles its node per launch
     capturing = false;
     if (is != GSM_OK) return is;
     gsm_context::GraphEntry& P = S.meta;
-    P.kernels = kernels + (w ? 1 : 0);  // counted with k_init
+    P.kernels = kernels;
     P.self_clean = self_clean;
     P.image.assign(reinterpret_cast<const char*>(hb), reinterpret_cast<const char*>(hb) + used);
     P.n_epochs = n_epoch_slots;
@@ -3591,7 +3595,7 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     bkey += keys[i];
   }
   cudaStream_t s0 = c0->stream;
-  bool use_warm = false, b0_recorded = false;
+
   auto it = c0->batches.find(bkey);
   if (it != c0->batches.end()) {
     bool ok = true;
@@ -3622,17 +3626,12 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
         drop_imgs();
         return false;
       }
-    // Two captures of the batch: with every member's k_init (installs the
-    // query blocks), and the warm one in which self-cleaning members skip it.
-    cudaGraphExec_t gx[2] = {nullptr, nullptr};
-    bool ok = true;
-    for (int v = 0; v < 2 && ok; v++) {
     if (cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
-      ok = false;
-      break;
+      drop_imgs();
+      return false;
     }
-    ok = cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
+    bool ok = cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
     int forked = 1;  // streams joined to the capture (ctxs[0]'s is the origin)
     for (; forked < n && ok; forked++) ok = cudaStreamWaitEvent(ctxs[forked]->stream, c0->ev_fork, 0) == cudaSuccess;
     if (!ok) forked--;
@@ -3644,11 +3643,9 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       const bool pdl = ctxs[i]->use_pdl;
       ctxs[i]->use_pdl = false;
       S[i].capture_only = true;
-      S[i].warm_capture = v == 1;
       S[i].pre_image = imgs[i];
       ok = launch_query(ctxs[i], qa[i], S[i]) == GSM_OK;
       S[i].capture_only = false;
-      S[i].warm_capture = false;
       ctxs[i]->use_pdl = pdl;
       if (ok)
         ok = cudaEventRecordWithFlags(ctxs[i]->ev_ext, ctxs[i]->stream, cudaEventRecordExternal) ==
@@ -3664,18 +3661,40 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     }
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(s0, &g);
-    if (ok && ce == cudaSuccess && g) ok = cudaGraphInstantiate(&gx[v], g, 0) == cudaSuccess;
+    cudaGraphExec_t ge = nullptr;
+    if (ok && ce == cudaSuccess && g) ok = cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
     else ok = false;
-    if (g) cudaGraphDestroy(g);
+    // member i's k_init node: the kernel node of k_init whose destination is
+    // ctxs[i]'s query block
+    std::vector<cudaGraphNode_t> init_node((size_t)n, nullptr);
+    if (ok) {
+      size_t nn = 0;
+      ok = cudaGraphGetNodes(g, nullptr, &nn) == cudaSuccess;
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (ok && nn) ok = cudaGraphGetNodes(g, nodes.data(), &nn) == cudaSuccess;
+      for (size_t k = 0; k < nn && ok; k++) {
+        cudaGraphNodeType ty;
+        if (cudaGraphNodeGetType(nodes[k], &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp{};
+        if (cudaGraphKernelNodeGetParams(nodes[k], &kp) != cudaSuccess) continue;
+        if (kp.func != reinterpret_cast<void*>(k_init) || !kp.kernelParams) continue;
+        const void* dst = *reinterpret_cast<void* const*>(kp.kernelParams[1]);
+        for (int i = 0; i < n; i++)
+          if (dst == ctxs[i]->d_block) init_node[i] = nodes[k];
+      }
+      cudaGetLastError();
     }
-    cudaGraphExec_t ge = gx[0];
-    if (!ok && gx[1]) cudaGraphExecDestroy(gx[1]);
+    if (!ok && g) {
+      cudaGraphDestroy(g);
+      g = nullptr;
+    }
     for (int i = 0; i < n && ok; i++)
       ok = cudaMemcpy(imgs[i], S[i].meta.image.data(), S[i].meta.image.size(), cudaMemcpyHostToDevice) ==
            cudaSuccess;
     if (!ok) {
       cudaGetLastError();
       if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
       drop_imgs();
       for (int i = 0; i < n; i++) {
         // the captured plans took epochs from the host mirror only
@@ -3685,7 +3704,9 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     }
     gsm_context::BatchEntry E;
     E.exec = ge;
-    E.warm = gx[1];
+    E.graph = g;
+    E.init_node = init_node;
+    E.init_on.assign((size_t)n, 1);
     for (int i = 0; i < n; i++) {
       E.bufgens.push_back(ctxs[i]->bufgen);
       S[i].meta.image_id = next_image_id();
@@ -3695,49 +3716,38 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     it = c0->batches.emplace(bkey, std::move(E)).first;
     // the capture planned every query (epochs reserved for the install run)
     for (int i = 0; i < n; i++) count_launch(S[i].kernels);
-    use_warm = false;
   } else {
-    const gsm_context::BatchEntry& B = it->second;
-    // Warm unless many members' blocks hold another plan (a context used
-    // by other queries in between): those few are installed by their own
-    // k_init on the origin stream ahead of the warm graph (the images
-    // already hold the resolved scans once the install variant has run).
-    int stale = 0;
-    for (int i = 0; i < n; i++)
-      stale += B.metas[i].self_clean && ctxs[i]->installed != B.metas[i].image_id;
-    use_warm = B.warm != nullptr && B.resolved && 4 * stale <= n;
-    // the batch's device time includes any pre-install
-    if (timed && cudaEventRecord(c0->ev_b0, s0) != cudaSuccess) return false;
-    b0_recorded = timed;
+    // Per member: skip k_init (disable its node) when the member's context
+    // still holds the member's image, left clean by its previous replay;
+    // members whose context ran another plan in between install theirs.
+    gsm_context::BatchEntry& B = it->second;
     for (int i = 0; i < n; i++) {
       ctxs[i]->gen++;
       const gsm_context::GraphEntry& M = B.metas[i];
-      const bool w = use_warm && M.self_clean;
-      if (w && ctxs[i]->installed != M.image_id) {
-        reserve_epochs(ctxs[i], M.n_epochs);  // room was made above (epoch_headroom)
-        gsm_context* ci = ctxs[i];
-        k_init<<<1, 256, 0, s0>>>(reinterpret_cast<const uint4*>(M.d_image),
-                                  reinterpret_cast<uint4*>(ci->d_block),
-                                  (int)((M.image.size() + 15) / 16), ci->d_ctr, ci->d_block->epochs,
-                                  M.n_epochs, ResolveArgs{}, nullptr, nullptr, nullptr, nullptr);
-        if (cudaGetLastError() != cudaSuccess) return false;
-        count_launch();
+      const bool w = B.resolved && M.self_clean && B.init_node[i] &&
+                     ctxs[i]->installed == M.image_id;
+      if ((B.init_on[i] != 0) == w) {  // toggle
+        if (cudaGraphNodeSetEnabled(B.exec, B.init_node[i], w ? 0 : 1) != cudaSuccess) {
+          cudaGetLastError();
+          return false;
+        }
+        B.init_on[i] = w ? 0 : 1;
       }
       apply_entry(ctxs[i], M, S[i], w);
       if (w) S[i].kernels--;
       count_launch(S[i].kernels);
     }
   }
-  if (timed && !b0_recorded && cudaEventRecord(c0->ev_b0, s0) != cudaSuccess) return false;
+  if (timed && cudaEventRecord(c0->ev_b0, s0) != cudaSuccess) return false;
   const auto tg0 = std::chrono::steady_clock::now();
-  if (cudaGraphLaunch(use_warm ? it->second.warm : it->second.exec, s0) != cudaSuccess) {
+  if (cudaGraphLaunch(it->second.exec, s0) != cudaSuccess) {
     cudaGetLastError();
     for (int i = 0; i < n; i++) ctxs[i]->installed = 0;
     return false;
   }
   for (int i = 0; i < n; i++)
     ctxs[i]->installed = it->second.metas[i].self_clean ? it->second.metas[i].image_id : 0;
-  if (!use_warm) it->second.resolved = true;
+  it->second.resolved = true;  // every member's k_init has run at least once
   note_graph_launch(std::chrono::duration<double>(std::chrono::steady_clock::now() - tg0).count());
   if (timed) cudaEventRecord(c0->ev_b1, s0);
   for (int i = 0; i < n; i++) S[i].sync_stream = s0;

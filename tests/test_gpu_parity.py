@@ -340,6 +340,17 @@ def test_execute_batch_matches_sequential(store_factory):
     again = g.execute_batch(items, store)
     for a, b in zip(again, seq):
         assert orc.fingerprint_array(a.array) == orc.fingerprint_array(b.array)
+    # one member's context runs another plan in between (a one-query batch on
+    # pool context 0): the warm batch graph installs that member first
+    for _ in range(2):
+        g.execute_batch(items, store)
+        one = g.execute_batch([items[-1]], store)
+        assert orc.fingerprint_array(one[0].array) == orc.fingerprint_array(seq[-1].array)
+        reps = [g.ExecutionReport() for _ in items]
+        again = g.execute_batch(items, store, reports=reps)
+        for a, b, r, r0 in zip(again, seq, reps, seq_reps):
+            assert orc.fingerprint_array(a.array) == orc.fingerprint_array(b.array)
+            assert [s.rows for s in r.steps] == [s.rows for s in r0.steps]
     # a budget violation in one query raises the reference's error
     q9 = dict(lubm_queries())["q09"]
     bad = items[:3] + [_plan(store, q9)]
