@@ -72,15 +72,26 @@ def main() -> None:
         for f in sorted((REPO / "datagen" / "queries" / "lubm").glob("*.rq")):
             q, p = plan(st, f.read_text())
             items.append((q, p))
-            for _ in range(2):  # capture, then replay
+            for _ in range(3):  # capture, re-capture with grids from the rows seen, warm replay
                 res = g.execute(q, p, st)
                 assert [str(v) for v in orc.fingerprint_array(res.array)] == gold[f.stem]["fingerprint"]
                 checks += 1
-        for _ in range(2):
+        # batch: capture, hinted re-capture, warm replay (k_init nodes off),
+        # then one member's context runs another plan (its k_init back on)
+        for rnd in range(5):
+            if rnd == 3:
+                g.execute_batch([items[0]], st)
             outs = g.execute_batch(items, st)
             for (q, p), res, f in zip(items, outs, sorted((REPO / "datagen" / "queries" / "lubm").glob("*.rq"))):
                 assert [str(v) for v in orc.fingerprint_array(res.array)] == gold[f.stem]["fingerprint"]
                 checks += 1
+        # left-row chunks (forced), with the device fingerprint
+        q, p = items[8]
+        exp = gold[sorted((REPO / "datagen" / "queries" / "lubm").glob("*.rq"))[8].stem]["fingerprint"]
+        res = g.execute(q, p, st, chunks=8)
+        assert [str(v) for v in orc.fingerprint_array(res.array)] == exp
+        assert [str(v) for v in g.execute_summary(q, p, st, chunks=4).fingerprint] == exp
+        checks += 2
         ub = "PREFIX ub: <http://swat.cse.lehigh.edu/onto/univ-bench.owl#> "
         rdf = "PREFIX rdf: <http://www.w3.org/1999/02/22-rdf-syntax-ns#> "
         prep = orc.PreparedStore(st.matrices)
