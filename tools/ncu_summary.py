@@ -33,8 +33,11 @@ def launches(path):
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.defaultdict(list)
     for r in rows[hdr + 1:]:
+        if mi is not None and len(r) > mi and r[mi] != "gpu__time_duration.sum":
+            continue
         if len(r) > vi:
             name = r[ki].split("(")[0].replace("void ", "")
             agg[name].append(float(r[vi].replace(",", "")) / 1e3)
