@@ -959,6 +959,12 @@ constexpr u32 FUSE_MAX_FANOUT = 4;   // post-expand filters fuse only below this
 // 17 ms for a 2.9M-row expand).  Above this longest run the expand is
 // materialised instead and the filter kernel spreads its rows evenly.
 constexpr u32 INTERSECT_MAX_FANOUT = 1u << 14;
+// ... and below this average run the materialised expand is cheap and the
+// filter kernel's rows-in-parallel lookups beat the fused per-row chain
+// (power-law triangle, avg run 2: 1.45 ms unfused vs 1.87 fused; LUBM-1000
+// c3, 0.15 candidates per left row: 0.22 vs 0.36; c1, 6.2: 1.07 vs 0.54;
+// c8, 36: 0.89 vs 0.45)
+constexpr i64 INTERSECT_MIN_AVG = 4;
 constexpr int MAXGS = 2 * MAXF + 1;  // steps in a group
 
 struct FSpec {
@@ -1054,7 +1060,7 @@ constexpr int GP_BATCH = 4;
 constexpr int GSURV = 1024;  // survivors of a tile's long rows kept from the count pass
 static_assert(GP_BATCH >= (int)FUSE_MAX_FANOUT, "fused post filters must fit one batch");
 __device__ __forceinline__ u32 gpost_batch(const GroupP& p, const DTable& s, i64 r, u32 aux, u32 len,
-                                           i64* acc) {
+                                           i64* acc, const uint2* hsg) {
   u32 cand[GP_BATCH];
 #pragma unroll
   for (int j = 0; j < GP_BATCH; j++) cand[j] = (u32)j < len ? __ldg(p.X.dst + aux + j) : 0u;
@@ -1069,7 +1075,9 @@ __device__ __forceinline__ u32 gpost_batch(const GroupP& p, const DTable& s, i64
       tgt[j] = 0u;
       if ((alive >> j) & 1u) {
         const u32 key = vcol(s, p.a, f.kc, r, cand[j]);
-        sg[j] = seg_lookup(f.R, key);
+        // a filter keyed on a left column searches the row's one segment,
+        // looked up by the count phase alongside the expand's (hsg)
+        sg[j] = (i - p.npre < HOIST && f.kc < p.a) ? hsg[i - p.npre] : seg_lookup(f.R, key);
         tgt[j] = f.mode == F_PAIR ? vcol(s, p.a, f.tc, r, cand[j]) : f.mode == F_CONST ? f.cval : key;
       }
     }
@@ -1172,6 +1180,15 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
           len = 1;
           cnt = 1;
         } else {
+          // post filters keyed on a left column: their segment lookups go
+          // out together with the expand's, not after the candidates
+          uint2 hsg[HOIST];
+#pragma unroll
+          for (int h = 0; h < HOIST; h++) {
+            hsg[h] = make_uint2(0u, 0u);
+            if (h < p.npost && p.f[p.npre + h].kc < p.a)
+              hsg[h] = seg_lookup(p.f[p.npre + h].R, __ldg(s_in.col[p.f[p.npre + h].kc] + r));
+          }
           const uint2 sg = seg_lookup(p.X, __ldg(s_in.col[p.xk] + r));
           aux = sg.x;
           len = sg.y;
@@ -1183,7 +1200,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
           } else if (p.npost == 0) {
             cnt = len;
           } else if (len <= (u32)GP_BATCH) {
-            mask = gpost_batch(p, s_in, r, aux, len, s_acc);
+            mask = gpost_batch(p, s_in, r, aux, len, s_acc, hsg);
             cnt = __popc(mask);
           } else {  // (the host fuses post filters only for fan-out <= GP_BATCH)
             mask = 0;
@@ -2642,6 +2659,18 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   i64 g_x_avg = 0, g_x_est = 0;  // its average run, expected output rows
   Home g_in_home = H_NONE;
   int g_x_var = -1;    // the variable the group's expand binds
+  int g_x_step = -1;   // ... and its plan step
+  // Candidates per left row of the group's expand: the orientation's
+  // average run, or — once the plan has run (row hints) — what the expand
+  // actually produced per left row (LUBM-1000 c3: average run >= 4 but 0.15
+  // candidates per left row, since most left keys have no run at all)
+  auto x_yield = [&]() -> i64 {
+    if (ex.hint && g_x_step >= 1 && g_x_step < (int)ex.hint->size()) {
+      const i64 l = (*ex.hint)[g_x_step - 1], o = (*ex.hint)[g_x_step];
+      return l > 0 ? o / l : 0;
+    }
+    return g_x_avg;
+  };
   std::vector<int> group_id(n, -1);
   int n_groups = 0;
   Orient slice_R{};  // the first join's orientation / left key column: equal-E partition
@@ -2699,7 +2728,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           join = g_npost < MAXF && (g_x_fanout <= FUSE_MAX_FANOUT ||
                                     (g_x_est >= c->fuse_huge && g_x_fanout <= 64 * std::max<i64>(1, g_x_avg)) ||
                                     (c->use_intersect && g_npost < HOIST && jv[0] != g_x_var &&
-                                     g_x_fanout < INTERSECT_MAX_FANOUT));
+                                     g_x_fanout < INTERSECT_MAX_FANOUT && x_yield() >= INTERSECT_MIN_AVG));
         else join = g_npre < MAXF;
       }
       if (!join) {
@@ -2711,6 +2740,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       }
       if (is_expand) {
         g_has_x = true;
+        g_x_step = s;
         g_x_var = jv[0] == p.s_var ? p.o_var : p.s_var;
         const bool on_s = jv[0] == p.s_var;
         const HostAux& gha = on_s ? c->store->aux_so[p.pid] : c->store->aux_os[p.pid];
