@@ -7,22 +7,26 @@
 Workload (BASELINE.json configs[1]): LUBM-style synthetic store at scale U
 (default 10, ~1.38M triples, datagen/gsmgen) and queries Q1-Q14
 (datagen/queries/lubm, plain BGPs).  One "step" = the 14 queries executed
-once, each through the public drop-in API
-(``paper_1807_07691_b200.execute``), with L2 flushed before every step (the
-store is smaller than the 126 MB L2).
+once as one ``execute_batch`` call (the public drop-in API; 14 concurrent
+streams), with L2 flushed before every step (the store is smaller than the
+126 MB L2).  The K timed steps run back to back; diagnostic passes (one
+query at a time with and without reports, per-query latency) run after them.
 
 * value          join output rows / s (sum over join steps of StepReport.rows,
-                 SURVEY.md §8(d)), device time (CUDA events around each query
+                 SURVEY.md §8(d)), device time (CUDA events around the batch
                  inside the library), whole job over all ranks
-* e2e            the same through execute() as a user calls it: host-side plan
-                 encoding, H2D of the query block from pinned memory, kernels,
-                 D2H of the result rows into host numpy arrays (wall clock)
+* e2e            the same through execute_batch() as a user calls it, wall
+                 clock: launch, per-query completion and budget checks, the
+                 result rows copied into host numpy arrays
 * roofline       dominant kernel class (join kernel), algorithmic bytes per
                  SURVEY.md §8(d) / its measured event time vs MEASURED_PEAKS.json
 * cpu_baseline   the C oracle port (oracle/gsm_oracle.c, 1 core) on the same
                  queries, bounded sample
 * --impl reference  the unmodified reference package (oracle/_ref) on the host
-                 cores, mode="parallel", worker_count=os.cpu_count()
+                 cores, both of its modes (sequential: 1 core; parallel:
+                 worker_count=os.cpu_count()); value = the faster
+* scale_lubm     configs[2] (LUBM-style U=1000) in the same run: per-query
+                 device time and parity against the C oracle
 
 Multi-GPU (torchrun): every rank holds a replica of the store and serves its
 own copy of the query stream (weak scaling, no data-path collective); timing
@@ -299,14 +303,26 @@ def run_ours(args):
 
         items = [(q, plan) for _, q, plan in queries]
 
-        def one_step(collect):
-            """One step = the 14 queries, three passes, each after an L2 flush:
+        def batch_step():
+            """The timed step (value, e2e): the 14 queries as one
+            execute_batch() call (concurrent streams) after an L2 flush —
+            device time (CUDA events) and wall clock (the whole call: launch,
+            per-query completion, budget checks, rows copied into numpy)."""
+            flush.add_(1)
+            torch.cuda.synchronize()
+            bt = []
+            t0 = time.perf_counter()
+            g.execute_batch(items, store, batch_timing=bt)
+            wall_batch = time.perf_counter() - t0
+            return {"wall_batch": wall_batch, "dev_batch": bt[0]}
+
+        def diag_step():
+            """Diagnostic passes over the same 14 queries, each after an L2
+            flush (run after the timed batch steps, not interleaved with them):
             (A) one by one with a report: per-query device latency (CUDA
                 events inside the library), step counters, per-kernel times;
             (B) one by one exactly as a user calls execute() (no report), wall
                 clock incl. H2D of the query block and D2H of the result rows;
-            (C) the same 14 queries as one execute_batch() call (concurrent
-                streams): device time (events) and wall clock;
             (D) one by one again, each as a one-query execute_batch() whose
                 device time is taken around the whole launch sequence only
                 (no per-step events): the per-query latency."""
@@ -325,19 +341,12 @@ def run_ours(args):
             wall_seq = time.perf_counter() - t0
             flush.add_(1)
             torch.cuda.synchronize()
-            bt = []
-            t0 = time.perf_counter()
-            g.execute_batch(items, store, batch_timing=bt)
-            wall_batch = time.perf_counter() - t0
-            flush.add_(1)
-            torch.cuda.synchronize()
             lat_q = {}
             for name, q, plan in queries:
                 one = []
                 g.execute_batch([(q, plan)], store, batch_timing=one)
                 lat_q[name] = one[0]
-            return {"per_q": per_q, "wall_seq": wall_seq, "wall_batch": wall_batch,
-                    "dev_batch": bt[0], "lat": lat_q}
+            return {"per_q": per_q, "wall_seq": wall_seq, "lat": lat_q}
 
         # Cold first execution of every query (a statement never run before on
         # this store: host planning, launch-sequence capture, the run, the
@@ -354,15 +363,18 @@ def run_ours(args):
         clk = ClockSampler(local).__enter__()  # sampling starts before warm-up (nvidia-smi start-up)
         time.sleep(0.5)
         for _ in range(max(3, args.warmup)):
-            one_step(False)
+            diag_step()
+            batch_step()
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         launches0 = _lib.kernel_launches()
-        steps = []
         n_before = len(clk.samples)
-        for _ in range(args.steps):
-            steps.append(one_step(True))
+        bsteps = [batch_step() for _ in range(args.steps)]
+        torch.cuda.synchronize()
+        launches = _lib.kernel_launches() - launches0
+        dsteps = [diag_step() for _ in range(args.steps)]
+        steps = [dict(b, **d) for b, d in zip(bsteps, dsteps)]
         torch.cuda.synchronize()
         time.sleep(0.25)
         clk.__exit__(None, None, None)
@@ -370,7 +382,6 @@ def run_ours(args):
             clk.samples = clk.samples[n_before:]
         if world > 1:
             torch.distributed.barrier()
-        launches = _lib.kernel_launches() - launches0
 
         all_q = [x for st_ in steps for x in st_["per_q"]]
         dev_seq = sum(sum(st_["lat"].values()) for st_ in steps)

@@ -150,8 +150,12 @@ __device__ __forceinline__ void export_if_last(const ExportArgs& x) {
   __shared__ bool s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(x.done, 1u) == gridDim.x - 1;
+    if (gridDim.x == 1) {
+      s_last = true;  // the only block is the last (its writes are ordered by the barrier)
+    } else {
+      __threadfence();
+      s_last = atomicAdd(x.done, 1u) == gridDim.x - 1;
+    }
   }
   __syncthreads();
   if (s_last) {
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   __shared__ u32 s_aux[TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
   __shared__ LBShared s_lb;
-  __shared__ u32 s_tile;
+  __shared__ u32 s_tile, s_next;
   __shared__ int s_long[TILE];
   __shared__ int s_nlong;
   __shared__ DTable s_in;
@@ -304,9 +308,12 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   pdl_wait();  // everything below reads the previous kernel's output
   pdl_trigger();
   ts.epoch = *ts.epoch_ptr;
-  // The first tile grab overlaps the descriptor load.
+  // Block b's first tile is tile b (every block of the grid is resident, and
+  // blocks are dispatched in index order, so look-back only ever waits on
+  // running or finished tiles); later tiles come from the counter, offset by
+  // the grid.  No atomic in front of a block's first tile.
   if (tid == 0) {
-    s_tile = atomicAdd(ts.counter, 1u);
+    s_tile = blockIdx.x;
     s_nlong = 0;
   }
   p.prepare(s_in);
@@ -324,13 +331,15 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       // every tile was taken by some block's first grab: skip the atomic
       if (ntiles <= (i64)gridDim.x) break;
       if (tid == 0) {
-        s_tile = atomicAdd(ts.counter, 1u);
+        s_tile = s_next;  // grabbed while the previous tile ran
         s_nlong = 0;
       }
       __syncthreads();
     }
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
+    // the next tile's index, fetched now: its atomic overlaps this tile
+    if (tid == 0 && ntiles > (i64)gridDim.x) s_next = gridDim.x + atomicAdd(ts.counter, 1u);
     trace_at(it, 1);
     const i64 base = (i64)t * TILE;
 #pragma unroll
@@ -1121,7 +1130,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
   __shared__ u32 s_len[TS_TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
   __shared__ i64 s_base;
-  __shared__ u32 s_tile;
+  __shared__ u32 s_tile, s_next;
   __shared__ int s_long[TS_TILE];
   __shared__ int s_nlong;
   __shared__ DTable s_in;
@@ -1140,8 +1149,8 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
   pdl_wait();
   pdl_trigger();
   ts.epoch = *ts.epoch_ptr;
-  if (tid == 0) {
-    s_tile = atomicAdd(ts.counter, 1u);
+  if (tid == 0) {  // first tile = block index (see k_tilescan)
+    s_tile = blockIdx.x;
     s_nlong = 0;
   }
   copy_desc(s_in, p.L, p.a);
@@ -1159,13 +1168,15 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       // every tile was taken by some block's first grab: skip the atomic
       if (ntiles <= (i64)gridDim.x) break;
       if (tid == 0) {
-        s_tile = atomicAdd(ts.counter, 1u);
+        s_tile = s_next;  // grabbed while the previous tile ran
         s_nlong = 0;
       }
       __syncthreads();
     }
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
+    // the next tile's index, fetched now: its atomic overlaps this tile
+    if (tid == 0 && ntiles > (i64)gridDim.x) s_next = gridDim.x + atomicAdd(ts.counter, 1u);
     trace_at(it, 1);
     const i64 base = (i64)t * TS_TILE;
     const i64 r = base + tid;
