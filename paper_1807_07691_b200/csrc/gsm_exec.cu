@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   __shared__ u32 s_aux[TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
   __shared__ LBShared s_lb;
-  __shared__ u32 s_tile, s_next;
+  __shared__ u32 s_tile;
   __shared__ int s_long[TILE];
   __shared__ int s_nlong;
   __shared__ DTable s_in;
@@ -331,15 +331,13 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       // every tile was taken by some block's first grab: skip the atomic
       if (ntiles <= (i64)gridDim.x) break;
       if (tid == 0) {
-        s_tile = s_next;  // grabbed while the previous tile ran
+        s_tile = gridDim.x + atomicAdd(ts.counter, 1u);
         s_nlong = 0;
       }
       __syncthreads();
     }
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
-    // the next tile's index, fetched now: its atomic overlaps this tile
-    if (tid == 0 && ntiles > (i64)gridDim.x) s_next = gridDim.x + atomicAdd(ts.counter, 1u);
     trace_at(it, 1);
     const i64 base = (i64)t * TILE;
 #pragma unroll
@@ -1130,7 +1128,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
   __shared__ u32 s_len[TS_TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
   __shared__ i64 s_base;
-  __shared__ u32 s_tile, s_next;
+  __shared__ u32 s_tile;
   __shared__ int s_long[TS_TILE];
   __shared__ int s_nlong;
   __shared__ DTable s_in;
@@ -1168,15 +1166,13 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       // every tile was taken by some block's first grab: skip the atomic
       if (ntiles <= (i64)gridDim.x) break;
       if (tid == 0) {
-        s_tile = s_next;  // grabbed while the previous tile ran
+        s_tile = gridDim.x + atomicAdd(ts.counter, 1u);
         s_nlong = 0;
       }
       __syncthreads();
     }
     const u32 t = s_tile;
     if ((i64)t >= ntiles) break;
-    // the next tile's index, fetched now: its atomic overlaps this tile
-    if (tid == 0 && ntiles > (i64)gridDim.x) s_next = gridDim.x + atomicAdd(ts.counter, 1u);
     trace_at(it, 1);
     const i64 base = (i64)t * TS_TILE;
     const i64 r = base + tid;

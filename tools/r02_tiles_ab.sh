@@ -10,7 +10,7 @@ if not os.path.exists("/tmp/pl100m/meta"):
                     "--seed", "0", "--out", "/tmp/pl100m"], check=True, stdout=subprocess.DEVNULL)
 PY
 PREV=$PWD/paper_1807_07691_b200/_lib/libgsmat_b200_prev.so
-for rnd in 1 2; do
+for rnd in 1; do
 for lib in "$PREV" ""; do
   echo "== lib=${lib:-new}"
   GSM_LIB=$lib python tools/e2e_ab.py --reps 300 --store /tmp/lubm10
@@ -18,3 +18,5 @@ for lib in "$PREV" ""; do
   GSM_LIB=$lib python bench.py --only-probe 2>/dev/null | tail -1 | cut -c1-400
 done
 done
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_tables.py tests/test_gpu_chunked.py -x -q -p no:cacheprovider > gpurun_out/tiles_pytest.log 2>&1
+echo "pytest rc=$?"; tail -2 gpurun_out/tiles_pytest.log
