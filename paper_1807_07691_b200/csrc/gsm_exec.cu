@@ -2061,6 +2061,7 @@ struct gsm_context {
   bool use_proj_fusion = true;  // write the projected result from the last join
   bool use_batch_graph = true;  // a repeated batch replays as one graph (gsm_execute_batch)
   bool batch_poll = true;       // complete batch members as their branches finish (GSM_BATCH_POLL=0: one wait)
+  bool batch_pdl = false;       // programmatic dependent launch inside batch graphs (GSM_BATCH_PDL=1)
   // Adaptive grids: a plan's persistent grids are sized from host-side upper
   // bounds on its tables' rows until it has run once; then from the rows it
   // actually produced (x2 headroom) and its graph is captured again.  Any
@@ -2370,6 +2371,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* npf = getenv("GSM_NO_PROJ_FUSION")) c->use_proj_fusion = !(npf[0] == '1');
   if (const char* nb = getenv("GSM_NO_BATCH_GRAPH")) c->use_batch_graph = !(nb[0] == '1');
   if (const char* bp = getenv("GSM_BATCH_POLL")) c->batch_poll = !(bp[0] == '0');
+  if (const char* bq = getenv("GSM_BATCH_PDL")) c->batch_pdl = bq[0] == '1';
   if (const char* rh = getenv("GSM_NO_ROW_HINTS")) c->use_row_hints = !(rh[0] == '1');
   if (const char* sc = getenv("GSM_NO_SELF_CLEAN")) c->use_self_clean = !(sc[0] == '1');
   if (const char* fh = getenv("GSM_FUSE_HUGE")) c->fuse_huge = std::max<i64>(1, atoll(fh));
@@ -3678,7 +3680,7 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     // the bench workload; single-query latency is the same either way).
     for (int i = 0; i < n && ok; i++) {
       const bool pdl = ctxs[i]->use_pdl;
-      ctxs[i]->use_pdl = false;
+      ctxs[i]->use_pdl = pdl && ctxs[i]->batch_pdl;
       S[i].capture_only = true;
       S[i].pre_image = imgs[i];
       ok = launch_query(ctxs[i], qa[i], S[i]) == GSM_OK;
