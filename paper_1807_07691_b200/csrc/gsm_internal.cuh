@@ -1,5 +1,7 @@
 // gsm_internal.cuh — host-side objects behind the C ABI handles.
 #pragma once
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "gsm_common.cuh"
@@ -34,9 +36,31 @@ struct gsm_store {
 
 struct gsm_context;
 
+// Allocator whose resize() leaves new elements uninitialised: a decoded
+// result of 10^9 bytes is overwritten by its device copy right away, so
+// zero-filling it first would cost a full extra pass over host memory.
+template <class T>
+struct uninit_alloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = uninit_alloc<U>;
+  };
+  uninit_alloc() = default;
+  template <class U>
+  uninit_alloc(const uninit_alloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+
 // Host byte blob returned through the C ABI (decoded text, parsed triples).
 struct gsm_text {
-  std::vector<char> bytes;
+  std::vector<char, uninit_alloc<char>> bytes;
 };
 
 struct gsm_result {

@@ -59,42 +59,64 @@ def upload_dictionary(store) -> None:
     store._dict_on_device = True
 
 
+class _Text:
+    """A decoded TSV body held by the library (gsm_text): ``view`` is a
+    memoryview of its bytes, valid until ``close()``."""
+
+    def __init__(self, store, rows: np.ndarray):
+        from .storage import from_store
+
+        store = from_store(store)
+        upload_dictionary(store)
+        rows = np.ascontiguousarray(rows, dtype=np.uint32)
+        if rows.ndim != 2:
+            raise ValueError("rows must be a 2-D (n, k) array")
+        n, k = rows.shape
+        self._L = _lib.lib()
+        self._txt = C.c_void_p()
+        _lib.check(self._L.gsm_decode_rows(store._handle, rows.ctypes.data if rows.size else None,
+                                           n, k, C.byref(self._txt)))
+        data, nbytes = C.c_void_p(), C.c_int64()
+        _lib.check(self._L.gsm_text_data(self._txt, C.byref(data), C.byref(nbytes)))
+        self.nbytes = int(nbytes.value)
+        self.view = (memoryview((C.c_char * self.nbytes).from_address(data.value)).cast("B")
+                     if self.nbytes else memoryview(b""))
+
+    def close(self) -> None:
+        if self._txt:
+            self.view.release()
+            self._L.gsm_text_free(self._txt)
+            self._txt = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 def decode_rows(store, rows: np.ndarray) -> bytes:
     """TSV body of a (n, k) node-id table: per row the k rendered terms joined
     by tabs and a newline (cli.py:103-105).  Raises UnknownIdError for an id
     outside the dictionary (dictionary.py:84-87)."""
-    from .storage import from_store
-
-    store = from_store(store)
-    upload_dictionary(store)
-    rows = np.ascontiguousarray(rows, dtype=np.uint32)
-    if rows.ndim != 2:
-        raise ValueError("rows must be a 2-D (n, k) array")
-    n, k = rows.shape
-    L = _lib.lib()
-    txt = C.c_void_p()
-    _lib.check(L.gsm_decode_rows(store._handle, rows.ctypes.data if rows.size else None, n, k,
-                                 C.byref(txt)))
-    try:
-        data, nbytes = C.c_void_p(), C.c_int64()
-        _lib.check(L.gsm_text_data(txt, C.byref(data), C.byref(nbytes)))
-        return C.string_at(data, nbytes.value) if nbytes.value else b""
-    finally:
-        L.gsm_text_free(txt)
+    with _Text(store, rows) as t:
+        return t.view.tobytes()
 
 
 def write_tsv(result, store, fh) -> int:
     """Write what ``gsmat query`` prints (cli.py:101-105) to a binary file
-    object without building a Python str; returns the bytes written."""
+    object without building a Python str or bytes: the library's decoded
+    buffer is written as it is; returns the bytes written."""
     head = ("\t".join(result.schema) + "\n").encode("utf-8")
-    body = decode_rows(store, result.array)
     fh.write(head)
-    fh.write(body)
-    return len(head) + len(body)
+    with _Text(store, result.array) as t:
+        fh.write(t.view)
+        return len(head) + t.nbytes
 
 
 def result_tsv(result, store) -> str:
     """What ``gsmat query`` prints for a result (cli.py:101-105): the schema
     line, then one decoded line per row."""
-    body = decode_rows(store, result.array)
-    return "\t".join(result.schema) + "\n" + body.decode("utf-8")
+    with _Text(store, result.array) as t:
+        body = str(t.view, "utf-8")  # decoded straight from the library's buffer
+    return "\t".join(result.schema) + "\n" + body

@@ -44,6 +44,11 @@ def main():
             t0 = time.perf_counter()
             body = g.decode_rows(st, res.array)  # the TSV body as bytes
             ours = time.perf_counter() - t0
+            import io, os
+            with open(os.devnull, "wb") as fh:
+                t0 = time.perf_counter()
+                g.write_tsv(res, st, fh)  # straight from the library's buffer to the file
+                ours_file = time.perf_counter() - t0
             out = ("\t".join(res.schema) + "\n").encode() + body
             arr = res.array
             n = len(arr)
@@ -56,6 +61,8 @@ def main():
             head = out[: len(ref)]
             print(json.dumps({"query": name, "rows": n, "bytes": len(out), "ours_s": round(ours, 4),
                               "ours_rows_per_s": round(n / ours, 1),
+                              "write_tsv_s": round(ours_file, 4),
+                              "write_tsv_rows_per_s": round(n / ours_file, 1),
                               "cli_loop_rows_per_s": round(sample / loop, 1), "cli_loop_sample": sample,
                               "sample_identical": head == ref}), flush=True)
 
