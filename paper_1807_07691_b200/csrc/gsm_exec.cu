@@ -295,8 +295,15 @@ __device__ i64 lookback_block(const TileSync& ts, u32 t, i64 agg, LBShared& sh) 
 template <class P, int ITEMS = 1>
 __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, ExportArgs xa) {
   constexpr int TILE = TS_THREADS * ITEMS;  // rows per tile
-  __shared__ i64 s_pre[TILE + 1];
-  __shared__ u32 s_aux[TILE];
+  // Count-ahead (256-row tiles, NB = 2): a block counts its NEXT tile and
+  // publishes that tile's aggregate before it looks back and scatters the
+  // current one, so by the time it looks back its predecessors have
+  // published theirs (a steady tile spent ~3 µs of ~14 waiting in the
+  // look-back, profiles/r02 trace).  512-row tiles keep one buffer (the
+  // second would not fit the 48 KB of static shared memory).
+  constexpr int NB = ITEMS == 1 ? 2 : 1;
+  __shared__ i64 s_pre[NB][TILE + 1];
+  __shared__ u32 s_aux[NB][TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
   __shared__ LBShared s_lb;
   __shared__ u32 s_tile;
@@ -312,10 +319,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   // blocks are dispatched in index order, so look-back only ever waits on
   // running or finished tiles); later tiles come from the counter, offset by
   // the grid.  No atomic in front of a block's first tile.
-  if (tid == 0) {
-    s_tile = blockIdx.x;
-    s_nlong = 0;
-  }
+  if (tid == 0) s_tile = blockIdx.x;
   p.prepare(s_in);
   u32 wtag = 0;  // load-balanced scatter: round tag of the row-start marks
   if constexpr (P::kWindow) P::window_init();
@@ -326,18 +330,11 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   const i64 ntiles = (n + TILE - 1) / TILE;
   if (ntiles == 0 && blockIdx.x == 0 && tid == 0) p.finish(0);
   i64 e_acc = 0;
-  for (bool first = true; ntiles > 0; first = false) {
-    if (!first) {
-      // every tile was taken by some block's first grab: skip the atomic
-      if (ntiles <= (i64)gridDim.x) break;
-      if (tid == 0) {
-        s_tile = gridDim.x + atomicAdd(ts.counter, 1u);
-        s_nlong = 0;
-      }
-      __syncthreads();
-    }
-    const u32 t = s_tile;
-    if ((i64)t >= ntiles) break;
+
+  // count tile t into buffer bf: per-row counts -> exclusive prefix in
+  // s_pre[bf] (total at [TILE]), per-row state in s_aux[bf], the left
+  // columns staged for the window; then publish the tile's aggregate
+  auto count_tile = [&](u32 t, int bf) {
     trace_at(it, 1);
     const i64 base = (i64)t * TILE;
 #pragma unroll
@@ -356,19 +353,19 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
         if (r < n) c = p.count(s_in, r, aux, e_acc);
 #pragma unroll
         for (int cc = 0; cc < P::WIN_A; cc++)
-          if (cc < na) P::template left_tile<TILE>()[cc][rl] = lv[cc];
+          if (cc < na) P::template left_tiles<TILE, NB>()[bf][cc][rl] = lv[cc];
       } else {
         if (r < n) c = p.count(s_in, r, aux, e_acc);
       }
-      s_aux[rl] = aux;
-      s_pre[rl] = c;
+      s_aux[bf][rl] = aux;
+      s_pre[bf][rl] = c;
     }
     __syncthreads();
     trace_at(it, 2);
     i64 v[ITEMS], sum = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
-      v[i] = s_pre[tid * ITEMS + i];
+      v[i] = s_pre[bf][tid * ITEMS + i];
       sum += v[i];
     }
     i64 x = sum;
@@ -383,26 +380,36 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     for (int w = 0; w < warp; w++) run += s_wsum[w];
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
-      s_pre[tid * ITEMS + i] = run;
+      s_pre[bf][tid * ITEMS + i] = run;
       run += v[i];
     }
-    if (tid == TS_THREADS - 1) s_pre[TILE] = run;
+    if (tid == TS_THREADS - 1) s_pre[bf][TILE] = run;
     __syncthreads();
-    const i64 total = s_pre[TILE];
-    lb_publish(ts, t, total);  // successors can start summing right away
+    lb_publish(ts, t, s_pre[bf][TILE]);  // successors can start summing right away
     trace_at(it, 3);
+  };
+
+  // look back and scatter tile t (counted into buffer bf)
+  auto process_tile = [&](u32 t, int bf) {
+    const i64 base = (i64)t * TILE;
+    const i64 total = s_pre[bf][TILE];
+    const i64* pre = s_pre[bf];
+    const u32* auxv = s_aux[bf];
     // Tiles whose rows average < WARP_ROW candidates: load-balanced scatter
     // (does its own look-back, overlapped with its first loads).
     if constexpr (P::kWindow) {
       if (total > 0 && total <= (i64)WARP_ROW * TILE && p.window_ok()) {
-        const i64 gb = p.template scatter_balanced<TILE>(s_pre, s_aux, total, ts, t, s_lb, wtag, it);
+        const i64 gb = p.template scatter_balanced<TILE>(pre, auxv, total, ts, t, s_lb, wtag, it,
+                                                         P::template left_tiles<TILE, NB>()[bf]);
         if ((i64)t == ntiles - 1 && tid == 0) p.finish(gb + total);
         trace_at(it, 5);
         it++;
         __syncthreads();
-        continue;
+        return;
       }
     }
+    if (tid == 0) s_nlong = 0;
+    __syncthreads();
     const i64 gbase = lookback_block(ts, t, total, s_lb);
     trace_at(it, 4);
     // Scatter (thread tid owns tile rows tid, tid + TS_THREADS, ...).  Rows with fewer
@@ -413,10 +420,10 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
       const int rl = i * TS_THREADS + tid;
-      const i64 mine = s_pre[rl + 1] - s_pre[rl];
+      const i64 mine = pre[rl + 1] - pre[rl];
       if (mine > 0 && mine < WARP_ROW) {
-        const i64 pos = gbase + s_pre[rl];
-        const u32 aux = s_aux[rl];
+        const i64 pos = gbase + pre[rl];
+        const u32 aux = auxv[rl];
         for (i64 j = 0; j < mine; j++) p.emit(s_in, base + rl, aux, j, pos + j);
       } else if (mine >= WARP_ROW) {
         s_long[atomicAdd(&s_nlong, 1)] = rl;
@@ -425,9 +432,9 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     __syncthreads();
     for (int q = warp; q < s_nlong; q += TS_THREADS / 32) {
       const int r = s_long[q];
-      const i64 c = s_pre[r + 1] - s_pre[r];
-      const i64 pos = gbase + s_pre[r];
-      const u32 aux = s_aux[r];
+      const i64 c = pre[r + 1] - pre[r];
+      const i64 pos = gbase + pre[r];
+      const u32 aux = auxv[r];
       if (P::kDefer && p.dq.items && c >= (total >= p.dq.heavy ? (i64)DEFER_ROW : (i64)p.dq.min_len)) {
         defer_row(p, s_in, p.dq, base + r, aux, c, pos);
         continue;
@@ -448,6 +455,36 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     trace_at(it, 5);
     it++;
     __syncthreads();
+  };
+
+  // the next tile's index (every tile was taken by some block's first grab
+  // when ntiles <= gridDim: no atomic)
+  auto grab = [&]() -> u32 {
+    if (ntiles <= (i64)gridDim.x) return (u32)ntiles;
+    if (tid == 0) s_tile = gridDim.x + atomicAdd(ts.counter, 1u);
+    __syncthreads();
+    const u32 t = s_tile;
+    __syncthreads();  // s_tile is rewritten by the next grab
+    return t;
+  };
+
+  u32 t = blockIdx.x;
+  if (NB == 2) {
+    int bf = 0;
+    if ((i64)t < ntiles) count_tile(t, bf);
+    while ((i64)t < ntiles) {
+      const u32 tn = grab();
+      if ((i64)tn < ntiles) count_tile(tn, bf ^ 1);
+      process_tile(t, bf);
+      t = tn;
+      bf ^= 1;
+    }
+  } else {
+    while ((i64)t < ntiles) {
+      count_tile(t, 0);
+      process_tile(t, 0);
+      t = grab();
+    }
   }
   trace_at(3, 7);
   if (P::kAccumE) {
@@ -736,9 +773,11 @@ struct ExpandP {
   // tile's left columns staged in shared memory by the count phase.
   static constexpr int WIN = 2048, WIN_A = 8, SLOTS = WIN / TS_THREADS, MARK_BITS = 10;
   static constexpr u32 TAG_MAX = (1u << (32 - MARK_BITS)) - 1;
-  template <int TILE>
-  __device__ static u32 (*left_tile())[TILE] {
-    __shared__ u32 lt[WIN_A][TILE];
+  // the tile's left columns staged by the count phase, one buffer per tile
+  // in flight (NB = 2: the count-ahead schedule of k_tilescan)
+  template <int TILE, int NB>
+  __device__ static u32 (*left_tiles())[WIN_A][TILE] {
+    __shared__ u32 lt[NB][WIN_A][TILE];
     return lt;
   }
   __device__ static u32 (*marks())[WIN] {
@@ -769,11 +808,10 @@ struct ExpandP {
   // A = left arity for columnar output (0: runtime a); K = fused row-major width (0: columnar)
   template <int A, int K, int TILE>
   __device__ i64 balanced_rounds(const i64* pre, i64 total, const TileSync& ts, u32 t,
-                                 LBShared& lb, u32& wtag, int trace_it) const {
+                                 LBShared& lb, u32& wtag, int trace_it, u32 (*lt)[TILE]) const {
     static_assert(TILE <= (1 << (MARK_BITS - 1)), "marks hold row+1 in MARK_BITS bits");
     constexpr int ITEMS = TILE / TS_THREADS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    u32 (*lt)[TILE] = left_tile<TILE>();
     const i64* rsrc = row_src<TILE>();
     i64 gbase = 0;
     int q = 0;
@@ -850,7 +888,8 @@ struct ExpandP {
   }
   template <int TILE>
   __device__ i64 scatter_balanced(const i64* pre, const u32* auxv, i64 total, const TileSync& ts,
-                                  u32 t, LBShared& lb, u32& wtag, int trace_it = 0) const {
+                                  u32 t, LBShared& lb, u32& wtag, int trace_it,
+                                  u32 (*lt)[TILE]) const {
 #pragma unroll
     for (int i = 0; i < TILE / TS_THREADS; i++) {  // read after round 0's barrier
       const int rl = i * TS_THREADS + threadIdx.x;
@@ -858,18 +897,18 @@ struct ExpandP {
     }
     if (fz.stage) {
       switch (fz.k) {
-        case 1: return balanced_rounds<0, 1, TILE>(pre, total, ts, t, lb, wtag, trace_it);
-        case 2: return balanced_rounds<0, 2, TILE>(pre, total, ts, t, lb, wtag, trace_it);
-        case 3: return balanced_rounds<0, 3, TILE>(pre, total, ts, t, lb, wtag, trace_it);
-        default: return balanced_rounds<0, 4, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+        case 1: return balanced_rounds<0, 1, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
+        case 2: return balanced_rounds<0, 2, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
+        case 3: return balanced_rounds<0, 3, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
+        default: return balanced_rounds<0, 4, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
       }
     }
     switch (a) {
-      case 1: return balanced_rounds<1, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
-      case 2: return balanced_rounds<2, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
-      case 3: return balanced_rounds<3, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
-      case 4: return balanced_rounds<4, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
-      default: return balanced_rounds<0, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it);
+      case 1: return balanced_rounds<1, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
+      case 2: return balanced_rounds<2, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
+      case 3: return balanced_rounds<3, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
+      case 4: return balanced_rounds<4, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
+      default: return balanced_rounds<0, 0, TILE>(pre, total, ts, t, lb, wtag, trace_it, lt);
     }
   }
   // Fused row-major output of candidates [j0, j0+32) (value nv per lane).
