@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   // published theirs (a steady tile spent ~3 µs of ~14 waiting in the
   // look-back, profiles/r02 trace).  512-row tiles keep one buffer (the
   // second would not fit the 48 KB of static shared memory).
-  constexpr int NB = ITEMS == 1 ? 2 : 1;
+  constexpr int NB = (ITEMS == 1 || P::kWindow) ? 2 : 1;
   __shared__ i64 s_pre[NB][TILE + 1];
   __shared__ u32 s_aux[NB][TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
@@ -345,14 +345,15 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       if constexpr (P::kWindow) {
         // the tile's left columns, for the load-balanced scatter (issued
         // before the count's dependent lookups so the loads overlap)
-        u32 lv[P::WIN_A];
-        const int na = r < n ? p.staged_cols() : 0;
+        constexpr int WA = P::template win_a<TILE>();
+        u32 lv[WA];
+        const int na = r < n ? p.template staged_cols<TILE>() : 0;
 #pragma unroll
-        for (int cc = 0; cc < P::WIN_A; cc++)
+        for (int cc = 0; cc < WA; cc++)
           if (cc < na) lv[cc] = __ldg(s_in.col[cc] + r);
         if (r < n) c = p.count(s_in, r, aux, e_acc);
 #pragma unroll
-        for (int cc = 0; cc < P::WIN_A; cc++)
+        for (int cc = 0; cc < WA; cc++)
           if (cc < na) P::template left_tiles<TILE, NB>()[bf][cc][rl] = lv[cc];
       } else {
         if (r < n) c = p.count(s_in, r, aux, e_acc);
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     // Tiles whose rows average < WARP_ROW candidates: load-balanced scatter
     // (does its own look-back, overlapped with its first loads).
     if constexpr (P::kWindow) {
-      if (total > 0 && total <= (i64)WARP_ROW * TILE && p.window_ok()) {
+      if (total > 0 && total <= (i64)WARP_ROW * TILE && p.template window_ok<TILE>()) {
         const i64 gb = p.template scatter_balanced<TILE>(pre, auxv, total, ts, t, s_lb, wtag, it,
                                                          P::template left_tiles<TILE, NB>()[bf]);
         if ((i64)t == ntiles - 1 && tid == 0) p.finish(gb + total);
@@ -774,11 +775,24 @@ struct ExpandP {
   static constexpr int WIN = 2048, WIN_A = 8, SLOTS = WIN / TS_THREADS, MARK_BITS = 10;
   static constexpr u32 TAG_MAX = (1u << (32 - MARK_BITS)) - 1;
   // the tile's left columns staged by the count phase, one buffer per tile
-  // in flight (NB = 2: the count-ahead schedule of k_tilescan)
+  // in flight (NB = 2: the count-ahead schedule of k_tilescan).  512-row
+  // tiles stage 4 columns, in dynamic shared memory (lt_bytes; the static
+  // 48 KB would not hold both buffers)
+  template <int TILE>
+  __host__ __device__ static constexpr int win_a() { return TILE >= 512 ? 4 : WIN_A; }
   template <int TILE, int NB>
-  __device__ static u32 (*left_tiles())[WIN_A][TILE] {
-    __shared__ u32 lt[NB][WIN_A][TILE];
-    return lt;
+  __host__ __device__ static constexpr size_t lt_bytes() {
+    return TILE >= 512 ? sizeof(u32) * NB * win_a<TILE>() * TILE : 0;
+  }
+  template <int TILE, int NB>
+  __device__ static u32 (*left_tiles())[win_a<TILE>()][TILE] {
+    if constexpr (TILE >= 512) {
+      extern __shared__ __align__(16) unsigned char gsm_dyn_smem[];
+      return reinterpret_cast<u32 (*)[win_a<TILE>()][TILE]>(gsm_dyn_smem);
+    } else {
+      __shared__ u32 lt[NB][win_a<TILE>()][TILE];
+      return lt;
+    }
   }
   __device__ static u32 (*marks())[WIN] {
     __shared__ u32 mk[2][WIN];
@@ -793,8 +807,12 @@ struct ExpandP {
     u32* mk = &marks()[0][0];
     for (int i = threadIdx.x; i < 2 * WIN; i += TS_THREADS) mk[i] = 0;
   }
-  __device__ int staged_cols() const { return a <= WIN_A ? a : 0; }
-  __device__ bool window_ok() const { return a <= WIN_A && (!fz.stage || (fz.k >= 1 && fz.k <= 4)); }
+  template <int TILE>
+  __device__ int staged_cols() const { return a <= win_a<TILE>() ? a : 0; }
+  template <int TILE>
+  __device__ bool window_ok() const {
+    return a <= win_a<TILE>() && (!fz.stage || (fz.k >= 1 && fz.k <= 4));
+  }
   template <int TILE>
   __device__ static int find_row(const i64* pre, i64 slot) {
     int lo = 0, hi = TILE;  // largest lo with pre[lo] <= slot (pre[0] = 0)
@@ -2012,6 +2030,21 @@ namespace {
 // between the dependent steps of a plan.  Captured into graphs as
 // programmatic edges.
 template <typename... KArgs, typename... Args>
+cudaError_t launch_smem(bool pdl, size_t smem, void (*kern)(KArgs...), int grid, int block,
+                        cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
 cudaError_t launch(bool pdl, void (*kern)(KArgs...), int grid, int block, cudaStream_t st,
                    Args&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -2459,6 +2492,12 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   st = ctx_set_stage(c, std::min<size_t>((size_t)2 << 20, c->stage_max));
   if (st != GSM_OK) return fail(st);
   int occ = 0;
+  // 512-row expand tiles: static + dynamic shared memory above 48 KB
+  static const bool smem_opt_in = [] {
+    return cudaFuncSetAttribute(k_tilescan<ExpandP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ExpandP::lt_bytes<2 * TS_THREADS, 2>()) == cudaSuccess;
+  }();
+  if (!smem_opt_in) return fail(set_error(GSM_ERR_CUDA, "cudaFuncSetAttribute(k_tilescan<ExpandP, 2>)"));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tilescan<ExpandP>, TS_THREADS, 0);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -2883,6 +2922,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       L.avg_run = avg_run;
       L.items = c->tile_items > 0 ? c->tile_items
                                   : (lub >= (i64)16 * c->grid_ts * TS_TILE && avg_run <= 16 ? 2 : 1);
+      // 512-row tiles stage at most 4 left columns for their window scatter
+      if (L.items == 2 && a > ExpandP::win_a<2 * TS_THREADS>() && c->tile_items == 0) L.items = 1;
     }
     L.grid = L.kind == S_CROSS ? ex.grid_for_rows(ex.hinted(L.out, s), 256)
                                : ex.grid_for_rows(ex.hinted(cur, s - 1), TS_TILE * L.items);
@@ -3145,7 +3186,8 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
           slot++;
           if (L.items == 2)
-            GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP, 2>, L.grid, TS_THREADS, st, L.ep, ts, xm));
+            GSM_CUDA(launch_smem(c->use_pdl, ExpandP::lt_bytes<2 * TS_THREADS, 2>(),
+                                 k_tilescan<ExpandP, 2>, L.grid, TS_THREADS, st, L.ep, ts, xm));
           else
             GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP>, L.grid, TS_THREADS, st, L.ep, ts, xm));
           nk++;
