@@ -315,11 +315,11 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   pdl_wait();  // everything below reads the previous kernel's output
   pdl_trigger();
   ts.epoch = *ts.epoch_ptr;
-  // Block b's first tile is tile b (every block of the grid is resident, and
-  // blocks are dispatched in index order, so look-back only ever waits on
-  // running or finished tiles); later tiles come from the counter, offset by
-  // the grid.  No atomic in front of a block's first tile.
-  if (tid == 0) s_tile = blockIdx.x;
+  // Tiles come from an atomic counter in the order blocks get to them (a
+  // static first tile per block — tile b for block b — was 4% slower on the
+  // long-row expands: a late-starting block then holds back its successors'
+  // look-back); the first grab overlaps the descriptor load.
+  if (tid == 0) s_tile = atomicAdd(ts.counter, 1u);
   p.prepare(s_in);
   u32 wtag = 0;  // load-balanced scatter: round tag of the row-start marks
   if constexpr (P::kWindow) P::window_init();
@@ -462,14 +462,15 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   // when ntiles <= gridDim: no atomic)
   auto grab = [&]() -> u32 {
     if (ntiles <= (i64)gridDim.x) return (u32)ntiles;
-    if (tid == 0) s_tile = gridDim.x + atomicAdd(ts.counter, 1u);
+    if (tid == 0) s_tile = atomicAdd(ts.counter, 1u);
     __syncthreads();
     const u32 t = s_tile;
     __syncthreads();  // s_tile is rewritten by the next grab
     return t;
   };
 
-  u32 t = blockIdx.x;
+  u32 t = s_tile;  // the first grab (read after the barrier above)
+  __syncthreads();
   if (NB == 2) {
     int bf = 0;
     if ((i64)t < ntiles) count_tile(t, bf);
@@ -1204,8 +1205,8 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
   pdl_wait();
   pdl_trigger();
   ts.epoch = *ts.epoch_ptr;
-  if (tid == 0) {  // first tile = block index (see k_tilescan)
-    s_tile = blockIdx.x;
+  if (tid == 0) {  // the first grab overlaps the descriptor load
+    s_tile = atomicAdd(ts.counter, 1u);
     s_nlong = 0;
   }
   copy_desc(s_in, p.L, p.a);
@@ -1223,7 +1224,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       // every tile was taken by some block's first grab: skip the atomic
       if (ntiles <= (i64)gridDim.x) break;
       if (tid == 0) {
-        s_tile = gridDim.x + atomicAdd(ts.counter, 1u);
+        s_tile = atomicAdd(ts.counter, 1u);
         s_nlong = 0;
       }
       __syncthreads();
