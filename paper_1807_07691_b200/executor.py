@@ -237,6 +237,8 @@ def execute(
 
     L = _lib.lib()
     part, parts = partition
+    if chunks is not None and (part, parts) != (0, 1):
+        raise ValueError("chunks and partition cannot be combined")
     if chunks is not None:
         return _execute_chunked(dstore, query, steps, arr, proj_arr, nproj, budget, budget_mode,
                                 report, "rows", _pow2(chunks))
