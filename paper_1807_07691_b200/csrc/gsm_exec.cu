@@ -2503,6 +2503,9 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   c->grid_ts = sms * std::max(1, std::min(occ, 4));
+  // (tests: a tiny grid makes every block walk many tiles — the count-ahead
+  // schedule and cross-block look-back on small stores)
+  if (const char* gm = getenv("GSM_GRID_MAX")) c->grid_ts = std::max(1, std::min(c->grid_ts, atoi(gm)));
   *out = c;
   return GSM_OK;
 }
