@@ -221,6 +221,8 @@ def execute(
         raise ValueError(f"unknown mode {mode!r}")
     if not plan.steps:
         raise ValueError("cannot execute an empty plan")
+    if chunks is not None and tuple(partition) != (0, 1):
+        raise ValueError("chunks and partition cannot be combined")
     dstore = store if isinstance(store, DeviceStore) else from_store(store)
     if getattr(dstore, "shard", None) is not None and dstore.shard[1] > 1:
         raise ValueError(
@@ -237,8 +239,6 @@ def execute(
 
     L = _lib.lib()
     part, parts = partition
-    if chunks is not None and (part, parts) != (0, 1):
-        raise ValueError("chunks and partition cannot be combined")
     if chunks is not None:
         return _execute_chunked(dstore, query, steps, arr, proj_arr, nproj, budget, budget_mode,
                                 report, "rows", _pow2(chunks))

@@ -67,3 +67,42 @@ def test_chunk_counts_are_powers_of_two():
     assert ex._pow2(10**12) == ex._MAX_PARTS
     with pytest.raises(ValueError):
         ex._pow2(0)
+
+
+def test_first_chunk_count_from_the_overflow_message():
+    class _Ctx:  # a store whose context has 1 GiB of capacity
+        def context(self):
+            return None
+
+    import ctypes as C
+
+    calls = {}
+
+    def cap(ctx, out):
+        C.cast(out, C.POINTER(C.c_int64))[0] = 1 << 30
+        calls["n"] = calls.get("n", 0) + 1
+        return 0
+
+    L = _lib.lib()
+    orig = L.gsm_context_capacity
+    try:
+        L.gsm_context_capacity = cap
+        # 10^9 rows x 3 columns x 8 bytes (two arena halves) x 1.25 over 1 GiB -> 28 -> 32
+        msg = "intermediate result of 1000000000 rows x 3 columns exceeds device memory"
+        assert ex._first_parts(_Ctx(), msg) == 32
+        assert ex._first_parts(_Ctx(), "something else") == 2
+    finally:
+        L.gsm_context_capacity = orig
+    assert calls["n"] == 2
+
+
+def test_chunks_and_partition_do_not_combine():
+    class _Q:
+        projection = ["?x"]
+        distinct = False
+
+    class _P:
+        steps = [type("S", (), {"pattern": None})()]
+
+    with pytest.raises(ValueError):
+        ex.execute(_Q(), _P(), object(), partition=(0, 2), chunks=2)
