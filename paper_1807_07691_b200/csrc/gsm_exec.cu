@@ -292,7 +292,7 @@ __device__ i64 lookback_block(const TileSync& ts, u32 t, i64 agg, LBShared& sh) 
 //   P::finish(total)           publish the output row count
 //   P::kAccumE                 accumulate e into st->e (filters)
 // ---------------------------------------------------------------------------
-template <class P, int ITEMS = 1>
+template <class P, int ITEMS = 1, bool AHEAD = true>
 __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, ExportArgs xa) {
   constexpr int TILE = TS_THREADS * ITEMS;  // rows per tile
   // Count-ahead (256-row tiles, NB = 2): a block counts its NEXT tile and
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
   // published theirs (a steady tile spent ~3 µs of ~14 waiting in the
   // look-back, profiles/r02 trace).  512-row tiles keep one buffer (the
   // second would not fit the 48 KB of static shared memory).
-  constexpr int NB = (ITEMS == 1 || P::kWindow) ? 2 : 1;
+  constexpr int NB = AHEAD && (ITEMS == 1 || P::kWindow) ? 2 : 1;
   __shared__ i64 s_pre[NB][TILE + 1];
   __shared__ u32 s_aux[NB][TILE];
   __shared__ i64 s_wsum[TS_THREADS / 32];
@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
       if constexpr (P::kWindow) {
         // the tile's left columns, for the load-balanced scatter (issued
         // before the count's dependent lookups so the loads overlap)
-        constexpr int WA = P::template win_a<TILE>();
+        constexpr int WA = P::template win_a<TILE, NB>();
         u32 lv[WA];
-        const int na = r < n ? p.template staged_cols<TILE>() : 0;
+        const int na = r < n ? p.template staged_cols<TILE, NB>() : 0;
 #pragma unroll
         for (int cc = 0; cc < WA; cc++)
           if (cc < na) lv[cc] = __ldg(s_in.col[cc] + r);
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_tilescan(P p, TileSync ts, Ex
     // Tiles whose rows average < WARP_ROW candidates: load-balanced scatter
     // (does its own look-back, overlapped with its first loads).
     if constexpr (P::kWindow) {
-      if (total > 0 && total <= (i64)WARP_ROW * TILE && p.template window_ok<TILE>()) {
+      if (total > 0 && total <= (i64)WARP_ROW * TILE && p.template window_ok<TILE, NB>()) {
         const i64 gb = p.template scatter_balanced<TILE>(pre, auxv, total, ts, t, s_lb, wtag, it,
                                                          P::template left_tiles<TILE, NB>()[bf]);
         if ((i64)t == ntiles - 1 && tid == 0) p.finish(gb + total);
@@ -779,19 +779,23 @@ struct ExpandP {
   // in flight (NB = 2: the count-ahead schedule of k_tilescan).  512-row
   // tiles stage 4 columns, in dynamic shared memory (lt_bytes; the static
   // 48 KB would not hold both buffers)
-  template <int TILE>
-  __host__ __device__ static constexpr int win_a() { return TILE >= 512 ? 4 : WIN_A; }
+  // (512-row tiles with one buffer keep 8 static columns: left tables wider
+  // than 4 columns take that variant)
+  template <int TILE, int NB>
+  __host__ __device__ static constexpr bool dyn_lt() { return TILE >= 512 && NB == 2; }
+  template <int TILE, int NB>
+  __host__ __device__ static constexpr int win_a() { return dyn_lt<TILE, NB>() ? 4 : WIN_A; }
   template <int TILE, int NB>
   __host__ __device__ static constexpr size_t lt_bytes() {
-    return TILE >= 512 ? sizeof(u32) * NB * win_a<TILE>() * TILE : 0;
+    return dyn_lt<TILE, NB>() ? sizeof(u32) * NB * win_a<TILE, NB>() * TILE : 0;
   }
   template <int TILE, int NB>
-  __device__ static u32 (*left_tiles())[win_a<TILE>()][TILE] {
-    if constexpr (TILE >= 512) {
+  __device__ static u32 (*left_tiles())[win_a<TILE, NB>()][TILE] {
+    if constexpr (dyn_lt<TILE, NB>()) {
       extern __shared__ __align__(16) unsigned char gsm_dyn_smem[];
-      return reinterpret_cast<u32 (*)[win_a<TILE>()][TILE]>(gsm_dyn_smem);
+      return reinterpret_cast<u32 (*)[win_a<TILE, NB>()][TILE]>(gsm_dyn_smem);
     } else {
-      __shared__ u32 lt[NB][win_a<TILE>()][TILE];
+      __shared__ u32 lt[NB][win_a<TILE, NB>()][TILE];
       return lt;
     }
   }
@@ -808,11 +812,11 @@ struct ExpandP {
     u32* mk = &marks()[0][0];
     for (int i = threadIdx.x; i < 2 * WIN; i += TS_THREADS) mk[i] = 0;
   }
-  template <int TILE>
-  __device__ int staged_cols() const { return a <= win_a<TILE>() ? a : 0; }
-  template <int TILE>
+  template <int TILE, int NB>
+  __device__ int staged_cols() const { return a <= win_a<TILE, NB>() ? a : 0; }
+  template <int TILE, int NB>
   __device__ bool window_ok() const {
-    return a <= win_a<TILE>() && (!fz.stage || (fz.k >= 1 && fz.k <= 4));
+    return a <= win_a<TILE, NB>() && (!fz.stage || (fz.k >= 1 && fz.k <= 4));
   }
   template <int TILE>
   __device__ static int find_row(const i64* pre, i64 slot) {
@@ -1197,6 +1201,10 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
   __shared__ u32 s_lcnt[TS_TILE];
   __shared__ uint2 s_surv[GSURV];
   __shared__ u32 s_nsurv;
+  __shared__ unsigned char s_bside[TS_TILE];  // long row walks the filter segment (pairx)
+  // the group's post filtering is one intersection-shaped pair filter
+  const bool pairx = p.npost == 1 && p.f[p.npre].mode == F_PAIR && p.f[p.npre].kc < p.a &&
+                     p.f[p.npre].tc == p.a;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   i64 acc[2 * MAXGS];  // this thread's (E, rows) contribution to each fused step
   for (int k = 0; k < 2 * MAXGS; k++) acc[k] = 0;
@@ -1290,6 +1298,13 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
       // row-invariant filter segments looked up once.  Survivors are kept
       // (row, candidate) in shared memory when they fit, so the emit pass
       // does not evaluate the filters again.
+      //
+      // A single pair filter keyed on a left column whose target is the
+      // candidate is a sorted-run intersection of the expand's run A and the
+      // filter's segment B: walk the shorter side and search the other
+      // (LUBM-1000 c6: |A| ~ 3,200 alumni of a university, |B| ~ a few
+      // advisees).  The filter's counters stay exact: E = |A| x |B| per row
+      // (every candidate would have searched B), rows = the survivors.
       u32 myl = 0;
       if (tid < nlong) {
         const int rl = s_long[tid];
@@ -1298,6 +1313,12 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
         for (int h = 0; h < HOIST && h < p.npost; h++) {
           const FSpec& f = p.f[p.npre + h];
           if (f.kc < p.a) s_rsg[tid][h] = seg_lookup(f.R, __ldg(s_in.col[f.kc] + base + rl));
+        }
+        s_bside[tid] = 0;
+        if (pairx && s_rsg[tid][0].y < myl) {
+          s_bside[tid] = 1;
+          acc[2 * p.f[p.npre].slot] += (i64)myl * s_rsg[tid][0].y;
+          myl = s_rsg[tid][0].y;
         }
       }
       u32 xs = myl;
@@ -1323,8 +1344,17 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
           else hi = mid - 1;
         }
         const int rl = s_long[lo];
-        const u32 cand = __ldg(p.X.dst + s_aux[rl] + (f - s_lpre[lo]));
-        if (gpost_h(p, s_in, base + rl, cand, s_rsg[lo], s_acc)) {
+        u32 cand;
+        bool keep;
+        if (s_bside[lo]) {  // walk B, search A
+          cand = __ldg(p.f[p.npre].R.dst + s_rsg[lo][0].x + (f - s_lpre[lo]));
+          keep = sorted_contains(p.X.dst + s_aux[rl], s_len[rl], cand);
+          acc[2 * p.f[p.npre].slot + 1] += keep;
+        } else {
+          cand = __ldg(p.X.dst + s_aux[rl] + (f - s_lpre[lo]));
+          keep = gpost_h(p, s_in, base + rl, cand, s_rsg[lo], s_acc);
+        }
+        if (keep) {
           atomicAdd(&s_lcnt[lo], 1u);
           const u32 k = atomicAdd(&s_nsurv, 1u);
           if (k < GSURV) s_surv[k] = make_uint2((u32)lo, cand);
@@ -1392,9 +1422,16 @@ __global__ void __launch_bounds__(TS_THREADS, 4) k_group(GroupP p, TileSync ts, 
             else hi = mid - 1;
           }
           const int rl = s_long[lo];
-          const u32 cand = __ldg(p.X.dst + s_aux[rl] + (f - s_lpre[lo]));
-          if (gpost_h(p, s_in, base + rl, cand, s_rsg[lo], nullptr))
-            gwrite(p, s_in, base + rl, cand, gbase + s_pre[rl] + atomicAdd(&s_lcnt[lo], 1u));
+          u32 cand;
+          bool keep;
+          if (s_bside[lo]) {
+            cand = __ldg(p.f[p.npre].R.dst + s_rsg[lo][0].x + (f - s_lpre[lo]));
+            keep = sorted_contains(p.X.dst + s_aux[rl], s_len[rl], cand);
+          } else {
+            cand = __ldg(p.X.dst + s_aux[rl] + (f - s_lpre[lo]));
+            keep = gpost_h(p, s_in, base + rl, cand, s_rsg[lo], nullptr);
+          }
+          if (keep) gwrite(p, s_in, base + rl, cand, gbase + s_pre[rl] + atomicAdd(&s_lcnt[lo], 1u));
         }
       }
     }
@@ -2495,7 +2532,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   int occ = 0;
   // 512-row expand tiles: static + dynamic shared memory above 48 KB
   static const bool smem_opt_in = [] {
-    return cudaFuncSetAttribute(k_tilescan<ExpandP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(k_tilescan<ExpandP, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ExpandP::lt_bytes<2 * TS_THREADS, 2>()) == cudaSuccess;
   }();
   if (!smem_opt_in) return fail(set_error(GSM_ERR_CUDA, "cudaFuncSetAttribute(k_tilescan<ExpandP, 2>)"));
@@ -2927,7 +2964,6 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
       L.items = c->tile_items > 0 ? c->tile_items
                                   : (lub >= (i64)16 * c->grid_ts * TS_TILE && avg_run <= 16 ? 2 : 1);
       // 512-row tiles stage at most 4 left columns for their window scatter
-      if (L.items == 2 && a > ExpandP::win_a<2 * TS_THREADS>() && c->tile_items == 0) L.items = 1;
     }
     L.grid = L.kind == S_CROSS ? ex.grid_for_rows(ex.hinted(L.out, s), 256)
                                : ex.grid_for_rows(ex.hinted(cur, s - 1), TS_TILE * L.items);
@@ -3190,8 +3226,16 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
           TileSync ts{c->d_status, dC + slot, c->d_block->epochs + slot, 0};
           slot++;
           if (L.items == 2)
-            GSM_CUDA(launch_smem(c->use_pdl, ExpandP::lt_bytes<2 * TS_THREADS, 2>(),
-                                 k_tilescan<ExpandP, 2>, L.grid, TS_THREADS, st, L.ep, ts, xm));
+          {
+            // count-ahead 512-row tiles stage 4 left columns; wider tables
+            // take the one-buffer variant (8 columns, static shared memory)
+            if (L.ep.a <= ExpandP::win_a<2 * TS_THREADS, 2>())
+              GSM_CUDA(launch_smem(c->use_pdl, ExpandP::lt_bytes<2 * TS_THREADS, 2>(),
+                                   k_tilescan<ExpandP, 2, true>, L.grid, TS_THREADS, st, L.ep, ts, xm));
+            else
+              GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP, 2, false>, L.grid, TS_THREADS, st, L.ep,
+                              ts, xm));
+          }
           else
             GSM_CUDA(launch(c->use_pdl, k_tilescan<ExpandP>, L.grid, TS_THREADS, st, L.ep, ts, xm));
           nk++;
