@@ -45,16 +45,20 @@ _MODES = ("gpu", "sequential", "parallel")
 class BindingTable:
     """An n-ary relation over variables, bag semantics (executor.py:40-49)."""
 
-    def __init__(self, schema, rows=None, sorted_by=None, array=None):
+    def __init__(self, schema, rows=None, sorted_by=None, array=None, view=None):
         self.schema = tuple(schema)
         self.sorted_by = sorted_by
         self._rows = list(rows) if rows is not None else None
         self._array = array
+        # (buffer, offset, rows, columns): the rows already sit in a host
+        # buffer shared by a batch's results; the (n, k) view of them is made
+        # when first asked for
+        self._view = view
 
     @property
     def rows(self) -> list[tuple[int, ...]]:
         if self._rows is None:
-            a = self._array
+            a = self._array if self._view is None else self.array
             if a is None:
                 self._rows = []
             elif a.shape[1] == 0:
@@ -67,17 +71,25 @@ class BindingTable:
     def rows(self, value) -> None:
         self._rows = list(value)
         self._array = None
+        self._view = None
 
     @property
     def array(self) -> np.ndarray:
         if self._array is None:
-            rows = self._rows or []
-            self._array = np.asarray(rows, dtype=np.uint64).reshape(len(rows), len(self.schema))
+            if self._view is not None:
+                buf, off, r, k = self._view
+                self._array = buf[off:off + r * k].reshape(r, k)
+                self._view = None
+            else:
+                rows = self._rows or []
+                self._array = np.asarray(rows, dtype=np.uint64).reshape(len(rows), len(self.schema))
         return self._array
 
     def __len__(self) -> int:
         if self._rows is not None:
             return len(self._rows)
+        if self._view is not None:
+            return self._view[2]
         return 0 if self._array is None else int(self._array.shape[0])
 
     def __eq__(self, other) -> bool:
@@ -690,26 +702,25 @@ def execute_batch(items, store, mode: str = "gpu", row_budget: int = DEFAULT_ROW
         _lib.raise_status(st, msg)
     nr = prep.nrows_np.tolist()
     nc = prep.ncols_np.tolist()
-    arrays = []
+    results = []
     grown = False
-    for i, (r, k, off) in enumerate(zip(nr, nc, prep.offsets)):
+    for i, (sch, r, k, off) in enumerate(zip(prep.schemas, nr, nc, prep.offsets)):
         if outs[i]:  # did not fit its slice: copy it now, give the slice room next time
             a = np.empty((r, k), dtype=np.uint32)
             st = L.gsm_result_copy(outs[i], a.ctypes.data) if a.size else _lib.GSM_OK
             L.gsm_result_free(outs[i])
             outs[i] = None
             _lib.check(st)
-            arrays.append(a)
+            results.append(BindingTable(sch, array=a))
             grown = True
-        else:
-            arrays.append(buf[off:off + r * k].reshape(r, k))
+        else:  # already in its slice of buf: the (n, k) view is made on first use
+            results.append(BindingTable(sch, view=(buf, off, r, k)))
     if grown:
         _size_slices(prep, [r * max(k, 1) for r, k in zip(nr, nc)])
     if reports is not None:
         for i in range(n):
             rep_struct, bufs = rep_bufs[i]
             _fill_report(reports[i], prep.steps[i], rep_struct, *bufs)
-    results = [BindingTable(sch, array=arr) for sch, arr in zip(prep.schemas, arrays)]
     if batch_timing is not None:
         batch_timing.append(ms.value / 1e3)
     return results
