@@ -39,7 +39,7 @@ def main():
         from paper_1807_07691_b200 import _lib
         L = _lib.lib()
         acc = {}
-        for name in ("gsm_execute_batch", "gsm_results_shape", "gsm_results_copy"):
+        for name in ("gsm_execute_batch_into", "gsm_result_copy", "gsm_result_free"):
             f = getattr(L, name)
 
             def wrap(*a, _f=f, _n=name):
