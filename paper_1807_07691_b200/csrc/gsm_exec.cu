@@ -3799,7 +3799,12 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       drop_imgs();
       return false;
     }
-    bool ok = cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
+    // The batch's device time is taken between event nodes at the graph's
+    // entry and exit (GPU timestamps of its first and last node), so the
+    // host's graph submission is not counted as device time (it is in the
+    // caller's wall clock).
+    bool ok = cudaEventRecordWithFlags(c0->ev_b0, s0, cudaEventRecordExternal) == cudaSuccess;
+    ok = ok && cudaEventRecord(c0->ev_fork, s0) == cudaSuccess;
     int forked = 1;  // streams joined to the capture (ctxs[0]'s is the origin)
     for (; forked < n && ok; forked++) ok = cudaStreamWaitEvent(ctxs[forked]->stream, c0->ev_fork, 0) == cudaSuccess;
     if (!ok) forked--;
@@ -3827,6 +3832,7 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
                      cudaStreamWaitEvent(s0, ctxs[i]->ev_done, 0) == cudaSuccess;
       ok = ok && j;
     }
+    ok = ok && cudaEventRecordWithFlags(c0->ev_b1, s0, cudaEventRecordExternal) == cudaSuccess;
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(s0, &g);
     cudaGraphExec_t ge = nullptr;
@@ -3906,7 +3912,6 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       count_launch(S[i].kernels);
     }
   }
-  if (timed && cudaEventRecord(c0->ev_b0, s0) != cudaSuccess) return false;
   const auto tg0 = std::chrono::steady_clock::now();
   if (cudaGraphLaunch(it->second.exec, s0) != cudaSuccess) {
     cudaGetLastError();
@@ -3917,7 +3922,6 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     ctxs[i]->installed = it->second.metas[i].self_clean ? it->second.metas[i].image_id : 0;
   it->second.resolved = true;  // every member's k_init has run at least once
   note_graph_launch(std::chrono::duration<double>(std::chrono::steady_clock::now() - tg0).count());
-  if (timed) cudaEventRecord(c0->ev_b1, s0);
   for (int i = 0; i < n; i++) S[i].sync_stream = s0;
   return true;
 }
