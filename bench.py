@@ -277,11 +277,13 @@ def run_ours(args):
     import torch
 
     rank, world, local = _dist()
+    if args.share_gpu:  # every rank on cuda:0 (multi-rank test on a one-GPU box; gloo)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.backend)
     import paper_1807_07691_b200 as g
     from paper_1807_07691_b200 import _lib
 
@@ -414,10 +416,10 @@ def run_ours(args):
             lat[name] = round(1e3 * statistics.median(st_["lat"][name] for st_ in steps), 4)
 
         if world > 1:
-            t = torch.tensor([dev_s, wall_s, dev_seq, wall_seq], dtype=torch.float64,
-                             device=f"cuda:{local}")
+            red_dev = f"cuda:{local}" if args.backend == "nccl" else "cpu"
+            t = torch.tensor([dev_s, wall_s, dev_seq, wall_seq], dtype=torch.float64, device=red_dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            r = torch.tensor([rows], dtype=torch.float64, device=f"cuda:{local}")
+            r = torch.tensor([rows], dtype=torch.float64, device=red_dev)
             torch.distributed.all_reduce(r)
             dev_s, wall_s, dev_seq, wall_seq = (float(x) for x in t)
             rows_all = float(r[0])

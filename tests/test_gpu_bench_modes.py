@@ -46,3 +46,19 @@ def test_bench_distributed_modes(mode, workload, extra):
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
     if mode == "sharded":
         assert line["exchanged_bytes_per_step"] > 0
+
+
+@pytest.mark.timeout(900)
+def test_bench_replica_mode_two_ranks():
+    """The default multi-GPU mode (what `bench.py --gpus N` runs under
+    torchrun): every rank serves its own copy of the query stream, timing is
+    the max over ranks and `value` the whole job's rows over it."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(REPO / "bench.py"),
+           "--gpus", "2", "--backend", "gloo", "--share-gpu", "--univ", "2", "--steps", "3",
+           "--warmup", "3", "--no-cpu-baseline", "--no-probe"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=850)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak"
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
