@@ -2626,6 +2626,10 @@ struct ExecState {
   // Batch capture: the caller holds c->stream inside a stream capture; only
   // issue the launch sequence into it and describe it in `meta`.
   bool capture_only = false;
+  // a one-query timed batch: the context's ev_b0 / ev_b1 are recorded as the
+  // first and last nodes of the query's own sequence (device time without
+  // the host's graph submission, as for batch graphs)
+  bool span_events = false;
   char* pre_image = nullptr;  // batch capture: the d_image buffer to use
   bool zc = false;            // counters and result rows written straight to pinned host memory
   bool big = false;           // this plan's last result outgrew the staging buffer
@@ -2665,7 +2669,8 @@ static std::string query_key(gsm_context* c, const QueryArgs& qa, ExecState& S) 
   auto put = [&key](const void* p, size_t b) { key.append(reinterpret_cast<const char*>(p), b); };
   put(qa.steps, sizeof(gsm_pattern) * (size_t)qa.n);
   put(qa.proj, sizeof(int32_t) * (size_t)qa.n_proj);
-  const i64 scal[] = {qa.n, qa.n_proj, qa.distinct != 0, S.allow_fuse, S.timing, qa.budget, qa.part, qa.parts};
+  const i64 scal[] = {qa.n,     qa.n_proj, qa.distinct != 0, S.allow_fuse, S.timing,
+                      qa.budget, qa.part,   qa.parts,         S.span_events};
   put(scal, sizeof scal);
   auto lb = c->last_bytes.find(key);
   size_t g = 65536;
@@ -3161,6 +3166,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // this plan's image, left clean by its previous replay)
   auto issue = [&](bool warm) -> gsm_status {
     int nk = 0;
+    if (S.span_events) GSM_CUDA(record(c->ev_b0));
     if (timing) GSM_CUDA(record(c->ev_q0));
     // the query block: a replayed graph copies its device image in k_init;
     // otherwise it is uploaded here
@@ -3305,6 +3311,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
     if (!S.zc)
       GSM_CUDA(cudaMemcpyAsync(c->h_stage, c->d_stage, STAGE_HEAD + ((distinct || S.big) ? 0 : c->guess),
                                cudaMemcpyDeviceToHost, st));
+    if (S.span_events) GSM_CUDA(record(c->ev_b1));
     kernels = nk;
     return GSM_OK;
   };
@@ -4003,7 +4010,11 @@ static gsm_status batch_impl(gsm_context* const* ctxs, int32_t n_queries, const 
   }
   // Fast path: the whole batch as one prepared graph launch.
   const bool as_graph = launch_batch_graph(ctxs, n_queries, qa, S, timed);
-  if (!as_graph) {
+  if (!as_graph && timed && n_queries == 1) {  // one query: its own entry/exit event nodes
+    S[0].span_events = true;
+    st[0] = begin_query(ctxs[0], qa[0], S[0]);
+    if (st[0] != GSM_OK) msg[0] = gsm_last_error();
+  } else if (!as_graph) {
     if (timed) {  // all streams start after ev_b0 ...
       GSM_CUDA(cudaSetDevice(ctxs[0]->device));
       GSM_CUDA(cudaEventRecord(ctxs[0]->ev_b0, ctxs[0]->stream));
