@@ -3730,6 +3730,12 @@ gsm_status gsm_execute_seeded(gsm_context* c, const uint32_t* seed_rows, int64_t
 
 namespace {
 double g_graph_launch_s = 0;  // host time inside cudaGraphLaunch (GSM_HOST_TIMING)
+// launch_batch_graph phases (GSM_HOST_TIMING): validation, keys, lookup + replay set-up
+double g_lbg_phase[3] = {0, 0, 0};
+bool g_lbg_timing = getenv("GSM_HOST_TIMING") && getenv("GSM_HOST_TIMING")[0] == '1';
+double lbg_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 void note_graph_launch(double s) { g_graph_launch_s += s; }
 // Make sure the next `need` epochs of a context need no status re-zeroing
 // (reserve_epochs' wrap enqueues a memset on the context's own stream, which a
@@ -3751,6 +3757,7 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
                         std::vector<ExecState>& S, bool timed) {
   gsm_context* c0 = ctxs[0];
   if (n < 2 || !c0->use_batch_graph) return false;
+  const double tp0 = g_lbg_timing ? lbg_now() : 0.0;
   for (int i = 0; i < n; i++) {
     if (!ctxs[i]->use_graphs || ctxs[i]->device != c0->device || qa[i].seed_k >= 0) return false;
     if (validate_query(ctxs[i], qa[i]) != GSM_OK) return false;
@@ -3758,6 +3765,7 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
   if (cudaSetDevice(c0->device) != cudaSuccess) return false;
   for (int i = 0; i < n; i++)  // install + the self-cleaning end: 2 x the launches' epochs
     if (epoch_headroom(ctxs[i], 2 * (GSM_MAX_STEPS + 4)) != GSM_OK) return false;
+  const double tp1 = g_lbg_timing ? lbg_now() : 0.0;
   std::string bkey;
   std::vector<std::string> keys((size_t)n);
   for (int i = 0; i < n; i++) {
@@ -3770,7 +3778,7 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     bkey += keys[i];
   }
   cudaStream_t s0 = c0->stream;
-
+  const double tp2 = g_lbg_timing ? lbg_now() : 0.0;
   auto it = c0->batches.find(bkey);
   if (it != c0->batches.end()) {
     bool ok = true;
@@ -3827,7 +3835,7 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       ok = launch_query(ctxs[i], qa[i], S[i]) == GSM_OK;
       S[i].capture_only = false;
       ctxs[i]->use_pdl = pdl;
-      if (ok)
+      if (ok && c0->batch_poll)
         ok = cudaEventRecordWithFlags(ctxs[i]->ev_ext, ctxs[i]->stream, cudaEventRecordExternal) ==
              cudaSuccess;
     }
@@ -3919,6 +3927,12 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
       count_launch(S[i].kernels);
     }
   }
+  if (g_lbg_timing) {
+    const double tp3 = lbg_now();
+    g_lbg_phase[0] += tp1 - tp0;
+    g_lbg_phase[1] += tp2 - tp1;
+    g_lbg_phase[2] += tp3 - tp2;
+  }
   const auto tg0 = std::chrono::steady_clock::now();
   if (cudaGraphLaunch(it->second.exec, s0) != cudaSuccess) {
     cudaGetLastError();
@@ -3965,6 +3979,9 @@ struct HostTimes {
               "%.1f us), rest %.1f us\n",
               calls, 1e6 * launch / calls, 1e6 * graph_launch / calls, 1e6 * wait / calls,
               1e6 * completing / calls, 1e6 * copying / calls, 1e6 * complete / calls);
+    if (on && calls)
+      fprintf(stderr, "  batch graph set-up: validation %.1f us, keys %.1f us, lookup + replay %.1f us\n",
+              1e6 * g_lbg_phase[0] / calls, 1e6 * g_lbg_phase[1] / calls, 1e6 * g_lbg_phase[2] / calls);
   }
 } g_host_times;
 double now_s() {
