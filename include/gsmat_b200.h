@@ -180,6 +180,16 @@ gsm_status gsm_execute(gsm_context* ctx, const gsm_pattern* steps, int32_t n_ste
                        int64_t row_budget, int32_t budget_mode, int64_t part_index,
                        int64_t part_count, gsm_report* report, gsm_result** out);
 
+/* gsm_execute that also hands the rows over: when the result (n_rows x
+ * n_cols ids, always set on success) fits dst_cap ids it is copied into dst
+ * and *out is NULL; otherwise *out holds it as in gsm_execute.  One call for
+ * what `execute` returns (executor.py:296-368: the projected rows). */
+gsm_status gsm_execute_into(gsm_context* ctx, const gsm_pattern* steps, int32_t n_steps,
+                            const int32_t* proj, int32_t n_proj, int32_t distinct,
+                            int64_t row_budget, int32_t budget_mode, int64_t part_index,
+                            int64_t part_count, gsm_report* report, uint32_t* dst,
+                            int64_t dst_cap, int64_t* n_rows, int32_t* n_cols, gsm_result** out);
+
 /* Sharded mode, one step at a time: like gsm_execute, but
  * step 0 is the caller's binding table instead of a scan — `seed_rows` is a
  * DEVICE pointer to n_seed x seed_k row-major uint32 ids whose columns bind

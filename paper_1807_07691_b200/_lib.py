@@ -68,6 +68,7 @@ EXPORTS = (
     "gsm_sort_triples",
     "gsm_context_capacity",
     "gsm_execute_batch_into",
+    "gsm_execute_into",
     "gsm_result_fingerprint",
 )
 
@@ -166,6 +167,11 @@ def lib() -> C.CDLL:
                 [vp, P(Pattern), i32, P(i32), i32, i32, i64, i32, i64, i64, P(Report), P(vp)],
             ),
             "gsm_execute_batch": (i32, [P(vp), i32, P(Query), P(i32), P(vp), P(C.c_float)]),
+            "gsm_execute_into": (
+                i32,
+                [vp, P(Pattern), i32, P(i32), i32, i32, i64, i32, i64, i64, P(Report), vp, i64,
+                 P(i64), P(i32), P(vp)],
+            ),
             "gsm_execute_batch_into": (
                 i32, [P(vp), i32, P(Query), P(i32), P(vp), P(i64), P(i64), P(i32), P(vp),
                       P(C.c_float)]),

@@ -4142,6 +4142,22 @@ gsm_status gsm_execute_batch(gsm_context* const* ctxs, int32_t n_queries, const 
                     nullptr);
 }
 
+gsm_status gsm_execute_into(gsm_context* c, const gsm_pattern* steps, int32_t n, const int32_t* proj,
+                            int32_t n_proj, int32_t distinct, int64_t budget, int32_t budget_mode,
+                            int64_t part, int64_t parts, gsm_report* rep, uint32_t* dst,
+                            int64_t dst_cap, int64_t* n_rows, int32_t* n_cols, gsm_result** out) {
+  if (!n_rows || !n_cols || !out) return set_error(GSM_ERR_VALUE, "bad arguments");
+  *n_rows = 0;
+  *n_cols = 0;
+  gsm_status st = gsm_execute(c, steps, n, proj, n_proj, distinct, budget, budget_mode, part, parts,
+                              rep, out);
+  if (st != GSM_OK) return st;
+  uint32_t* const d[1] = {dst};
+  const int64_t cap[1] = {dst_cap};
+  deliver(*out, dst ? d : nullptr, cap, 0, n_rows, n_cols);
+  return GSM_OK;
+}
+
 gsm_status gsm_execute_batch_into(gsm_context* const* ctxs, int32_t n_queries,
                                   const gsm_query* queries, gsm_status* statuses,
                                   uint32_t* const* dst, const int64_t* dst_cap, int64_t* n_rows,

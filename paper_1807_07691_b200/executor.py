@@ -254,17 +254,26 @@ def execute(
     if chunks is not None:
         return _execute_chunked(dstore, query, steps, arr, proj_arr, nproj, budget, budget_mode,
                                 report, "rows", _pow2(chunks))
-    res = C.c_void_p()
-    st = L.gsm_execute(
+    # the rows land in a host buffer sized by this plan's previous result
+    # (gsm_execute_into); a larger result comes back as a handle
+    pd = getattr(plan, "__dict__", None)
+    hint = pd.get("_gsm_ids", 0) if pd is not None else 0
+    cap = hint + hint // 8
+    buf = np.empty(max(cap, 1), dtype=np.uint32)
+    res, nrows, ncols = C.c_void_p(), C.c_int64(0), C.c_int32(0)
+    st = L.gsm_execute_into(
         dstore.context(), arr, n, proj_arr, nproj, 1 if query.distinct else 0, budget,
         budget_mode, int(part), int(parts), C.byref(rep_struct) if rep_struct is not None else None,
-        C.byref(res),
+        buf.ctypes.data, cap, C.byref(nrows), C.byref(ncols), C.byref(res),
     )
     if st == _lib.GSM_ERR_DEVICE_MEMORY and (part, parts) == (0, 1):
         return _execute_chunked(dstore, query, steps, arr, proj_arr, nproj, budget, budget_mode,
                                 report, "rows", _first_parts(dstore, _lib.last_error()))
     _lib.check(st)
-    out = _fetch(L, res)
+    r, k = int(nrows.value), int(ncols.value)
+    out = _fetch(L, res) if res.value else buf[:r * k].reshape(r, k)
+    if pd is not None:
+        pd["_gsm_ids"] = r * max(k, 1)
     if report is not None:
         _fill_report(report, steps, rep_struct, *bufs)
     return BindingTable(tuple(query.projection), array=out)
