@@ -27,6 +27,8 @@ query at a time with and without reports, per-query latency) run after them.
                  worker_count=os.cpu_count()); value = the faster
 * scale_lubm     configs[2] (LUBM-style U=1000) in the same run: per-query
                  device time and parity against the C oracle
+* scale_watdiv   configs[3] (WatDiv-style scale 1000, ~100M triples, one GPU)
+                 likewise; C2 (11.5G result rows) through execute_summary
 
 Multi-GPU (torchrun): every rank holds a replica of the store and serves its
 own copy of the query stream (weak scaling, no data-path collective); timing
@@ -83,6 +85,9 @@ def _args():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--scale-univ", type=int, default=1000,
                     help="configs[2]: LUBM-style scale run in the same invocation (N=1); 0 = skip")
+    ap.add_argument("--scale-watdiv", type=int, default=1000,
+                    help="configs[3]: WatDiv-style scale run in the same invocation (N=1; 1000 ~ "
+                         "100M triples); 0 = skip")
     ap.add_argument("--scale-reps", type=int, default=3)
     ap.add_argument("--oracle-guard", type=int, default=400_000_000,
                     help="the C oracle materialises every intermediate: above this many rows in a "
@@ -288,9 +293,10 @@ def run_ours(args):
     from paper_1807_07691_b200 import _lib
 
     with tempfile.TemporaryDirectory() as tmp:
-        scale_gen = None
+        scale_gen = wd_gen = None
         if world == 1 and not args.only_probe:
             scale_gen = _start_scale_gen(args, Path(tmp))
+            wd_gen = _start_watdiv_gen(args, Path(tmp))
         store_dir = _gen_store(Path(tmp), args.univ, args.seed)
         store = g.load(store_dir, device=local)
         queries = []
@@ -477,10 +483,14 @@ def run_ours(args):
         cpu = None
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 measurement
             cpu = cpu_baseline_port(store, queries, args.cpu_seconds)
-        scale = None
-        if scale_gen is not None:
+        scale = scale_wd = None
+        if scale_gen is not None or wd_gen is not None:
             store.close()
+        if scale_gen is not None:
             scale = run_scale(g, args, peaks, scale_gen, flush)
+        if wd_gen is not None:
+            scale_wd = run_scale(g, args, peaks, wd_gen, flush, qdirs=WATDIV_QDIRS, summary=("C2",),
+                                 label=f"configs[3]: WatDiv-style scale {args.scale_watdiv}")
 
         value = rows_all / dev_s if dev_s > 0 else 0.0
         line = {
@@ -518,6 +528,7 @@ def run_ours(args):
             "roofline_probe": probe,
             "cpu_baseline": cpu,
             "scale_lubm": scale,
+            "scale_watdiv": scale_wd,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
@@ -527,6 +538,21 @@ def run_ours(args):
 
 
 SCALE_QDIRS = (REPO / "datagen" / "queries" / "lubm", REPO / "datagen" / "queries" / "lubm_complex")
+
+
+WATDIV_QDIRS = (REPO / "datagen" / "queries" / "watdiv",)
+
+
+def _start_watdiv_gen(args, tmp: Path):
+    """configs[3]'s store (WatDiv-style, ~100M triples at scale 1000),
+    generated in the background like configs[2]'s."""
+    if args.scale_watdiv <= 0:
+        return None
+    out = tmp / f"watdiv{args.scale_watdiv}"
+    proc = subprocess.Popen([str(REPO / "oracle" / "_build" / "gsmgen"), "watdiv", "--scale",
+                             str(args.scale_watdiv), "--seed", str(args.seed), "--out", str(out)],
+                            stdout=subprocess.DEVNULL, stderr=subprocess.PIPE)
+    return proc, out, time.perf_counter()
 
 
 def _start_scale_gen(args, tmp: Path):
@@ -580,7 +606,7 @@ def _oracle_check(orc, prep, plan, q, guard: int, gpu_steps):
     return None, None, None, "not run (every join order materialises > guard rows)"
 
 
-def run_scale(g, args, peaks, gen, flush):
+def run_scale(g, args, peaks, gen, flush, qdirs=None, summary=(), label=None):
     """BASELINE.json configs[2] under the driver's clock: LUBM-style U=1000
     (~125M triples) on one GPU, Q1-Q14 plus the complex cyclic / snowflake
     queries (datagen/queries/lubm_complex).  Per query: median device
@@ -605,12 +631,41 @@ def run_scale(g, args, peaks, gen, flush):
     t0 = time.perf_counter()
     store = g.load(store_dir)
     t_load = time.perf_counter() - t0
+    dev_bytes = store.device_bytes()
     qs = []
-    for d in SCALE_QDIRS:
+    for d in (qdirs or SCALE_QDIRS):
         for f in sorted(d.glob("*.rq")):
             q = g.bind_constants(g.parse_query(f.read_text()), store.dictionary)
             qs.append((f.stem, q, g.make_plan(q, store.stats)))
     budget = 1 << 62
+    # results larger than host memory (WatDiv C2: a 38.6G-row intermediate,
+    # 11.5G result rows): execute_summary through left-row chunks, twice
+    # with different chunk counts (a dropped or doubled row would change the
+    # fingerprint); the oracle cannot materialise them
+    summaries = {}
+    for name, q, plan in [x for x in qs if x[0] in summary]:
+        rep = g.ExecutionReport()
+        tw = time.perf_counter()
+        s1 = g.execute_summary(q, plan, store, row_budget=budget, report=rep)
+        wall = time.perf_counter() - tw
+        rep2 = g.ExecutionReport()
+        s2 = g.execute_summary(q, plan, store, row_budget=budget, report=rep2,
+                               chunks=max(2, 2 * rep.chunks))
+        jr = _join_rows(rep.steps)
+        summaries[name] = {"mode": "execute_summary (left-row chunks, rows not materialised on the "
+                                   "host)", "result_rows": s1.rows,
+                           "fingerprint": [s1.rows, s1.sum, s1.xor], "chunks": rep.chunks,
+                           "ms": round(1e3 * rep.device_seconds, 3), "e2e_ms": round(1e3 * wall, 3),
+                           "join_rows": jr,
+                           "join_rows_per_s": round(jr / rep.device_seconds, 1) if rep.device_seconds else 0.0,
+                           "step_rows": [x.rows for x in rep.steps],
+                           "rechunked": {"chunks": rep2.chunks,
+                                         "same_fingerprint": s2.fingerprint == s1.fingerprint,
+                                         "same_step_rows": [x.rows for x in rep2.steps]
+                                         == [x.rows for x in rep.steps]},
+                           "parity": "oracle not run (beyond host RAM); re-chunked fingerprint agrees: "
+                                     + str(s2.fingerprint == s1.fingerprint)}
+    qs = [x for x in qs if x[0] not in summary]
     first = {}
     for name, q, plan in qs:  # sizes the arena and caches the plan's graph
         rep = g.ExecutionReport()
@@ -670,11 +725,16 @@ def run_scale(g, args, peaks, gen, flush):
     t_orc = time.perf_counter() - t_orc0
     pool.shutdown()
     store.close()
+    per.update(summaries)
     gbs = tot_bytes / (tot_ms / 1e3) / 1e9 if tot_ms else 0.0
-    return {"workload": f"configs[2]: LUBM-style U={args.scale_univ} ({store.triple_count} triples), "
-                        f"{len(qs)} queries (Q1-Q14 + complex c1-c8), 1 GPU",
+    workload = (f"{label} ({store.triple_count} triples), {len(qs) + len(summaries)} queries, 1 GPU"
+                if label else
+                f"configs[2]: LUBM-style U={args.scale_univ} ({store.triple_count} triples), "
+                f"{len(qs)} queries (Q1-Q14 + complex c1-c8), 1 GPU")
+    return {"workload": workload,
             "triples": store.triple_count, "gen_s": round(t_gen, 1), "load_s": round(t_load, 2),
-            "l2": "flushed before every timed run; store (~4 GB on the device) >> L2",
+            "l2": f"flushed before every timed run; store ({dev_bytes / 1e9:.1f} GB on "
+                  "the device) >> L2",
             "queries": per,
             "total": {"ms": round(tot_ms, 3), "join_rows": tot_rows,
                       "join_rows_per_s": round(tot_rows / (tot_ms / 1e3), 1) if tot_ms else 0.0,
@@ -684,8 +744,8 @@ def run_scale(g, args, peaks, gen, flush):
                        "oracle": "C restatement of the reference executor (oracle/gsm_oracle.c), "
                                  "bag fingerprint (count, sum, xor of row hashes) + per-step counters "
                                  "when it ran the plan's order", "oracle_wall_s": round(t_orc, 1)},
-            "reference": "not run: the Python reference needs ~70 GB of host RAM and ~30 min to "
-                         "build a 125M-triple store (SURVEY.md §7)"}
+            "reference": "not run: the Python reference needs ~550 MB of host RAM and ~13 s per "
+                         "million triples to build a store (SURVEY.md §7)"}
 
 
 def cpu_baseline_port(store, queries, seconds):
