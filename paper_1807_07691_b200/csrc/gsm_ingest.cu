@@ -179,9 +179,9 @@ struct DevBuf {
 // First-occurrence dense ids (1-based) of n occurrences whose canonical bytes
 // are bytes[off[i], off[i] + len[i]).  first_occ[id - 1] = the occurrence
 // that introduced the term.
-gsm_status encode_terms(const unsigned char* d_bytes, const std::vector<u64>& off,
-                        const std::vector<u32>& len, cudaStream_t st, std::vector<u32>& ids,
-                        std::vector<u32>& first_occ) {
+template <class VOff, class VLen>
+gsm_status encode_terms(const unsigned char* d_bytes, const VOff& off, const VLen& len, cudaStream_t st,
+                        std::vector<u32>& ids, std::vector<u32>& first_occ) {
   const u64 n = off.size();
   ids.assign(n, 0);
   first_occ.clear();
@@ -450,25 +450,35 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
     T += c.s.size();
     nb += c.bytes.size();
   }
-  std::vector<char> bytes;
-  bytes.reserve(nb);
-  std::vector<u64> noff(2 * T), poff(T);
-  std::vector<u32> nlen(2 * T), plen(T);
+  // the chunks' term bytes and offsets gathered into one array, each chunk
+  // by its own thread (bases from a prefix over the chunks)
+  std::vector<char, uninit_alloc<char>> bytes(nb);
+  std::vector<u64, uninit_alloc<u64>> noff(2 * T), poff(T);
+  std::vector<u32, uninit_alloc<u32>> nlen(2 * T), plen(T);
   {
-    u64 t = 0;
-    for (auto& c : chunks) {
-      const u64 base = bytes.size();
-      bytes.insert(bytes.end(), c.bytes.begin(), c.bytes.end());
-      for (size_t i = 0; i < c.s.size(); i++, t++) {
-        noff[2 * t] = base + c.s[i].off;
-        nlen[2 * t] = c.s[i].len;
-        noff[2 * t + 1] = base + c.o[i].off;
-        nlen[2 * t + 1] = c.o[i].len;
-        poff[t] = base + c.p[i].off;
-        plen[t] = c.p[i].len;
-      }
-      std::vector<char>().swap(c.bytes);
+    std::vector<u64> bbase(chunks.size() + 1, 0), tbase(chunks.size() + 1, 0);
+    for (size_t k = 0; k < chunks.size(); k++) {
+      bbase[k + 1] = bbase[k] + chunks[k].bytes.size();
+      tbase[k + 1] = tbase[k] + chunks[k].s.size();
     }
+    std::vector<std::thread> th;
+    for (size_t k = 0; k < chunks.size(); k++)
+      th.emplace_back([&, k] {
+        nt::Chunk& c = chunks[k];
+        const u64 base = bbase[k];
+        if (!c.bytes.empty()) memcpy(bytes.data() + base, c.bytes.data(), c.bytes.size());
+        u64 t = tbase[k];
+        for (size_t i = 0; i < c.s.size(); i++, t++) {
+          noff[2 * t] = base + c.s[i].off;
+          nlen[2 * t] = c.s[i].len;
+          noff[2 * t + 1] = base + c.o[i].off;
+          nlen[2 * t + 1] = c.o[i].len;
+          poff[t] = base + c.p[i].off;
+          plen[t] = c.p[i].len;
+        }
+        std::vector<char>().swap(c.bytes);
+      });
+    for (auto& x : th) x.join();
   }
   GSM_CUDA(cudaSetDevice(device));
   cudaStream_t cs;

@@ -2,6 +2,7 @@
 #include "gsm_ntparse.h"
 
 #include <cstring>
+#include <thread>
 
 namespace gsm {
 namespace nt {
@@ -32,8 +33,12 @@ bool is_space_cp(uint32_t cp) {
          cp == 0x202F || cp == 0x205F || cp == 0x3000;
 }
 
+// ASCII members of Python's \s (str patterns): \t \n \v \f \r, 0x1C-0x1F, ' '.
+inline bool ascii_space(unsigned char c) { return (c >= 0x09 && c <= 0x0D) || (c >= 0x1C && c <= 0x20); }
+
 // Length of the whitespace character at i (0 if none).
 int space_at(const unsigned char* s, size_t i, size_t n) {
+  if (s[i] < 0x80) return ascii_space(s[i]) ? 1 : 0;
   uint32_t cp;
   const int l = utf8_cp(s, i, n, cp);
   return l && is_space_cp(cp) ? l : 0;
@@ -45,9 +50,15 @@ size_t skip_ws(const unsigned char* s, size_t i, size_t n) {
   return i;
 }
 
-bool iri_char_ok(unsigned char c) {
-  return c > 0x20 && !strchr("<>\"{}|^`\\", c);
-}
+// IRI body characters ([^<>"{}|^`\\\x00-\x20]), as a table
+struct IriTable {
+  bool ok[256];
+  IriTable() {
+    for (int c = 0; c < 256; c++) ok[c] = c > 0x20 && !strchr("<>\"{}|^`\\", c);
+  }
+};
+const IriTable kIri;
+inline bool iri_char_ok(unsigned char c) { return kIri.ok[c]; }
 
 // <IRI> at i: body [b, e), returns the position after '>' or 0 on failure.
 size_t parse_iri(const unsigned char* s, size_t i, size_t n, size_t& b, size_t& e) {
@@ -358,11 +369,29 @@ void parse_range(const char* cbuf, size_t begin, size_t end, int64_t first_line,
   int64_t line = first_line;
   size_t i = begin;
   std::string msg;
+  // term bytes are a little less than the input; a statement is >= ~20 bytes
+  out.bytes.reserve(end - begin);
+  for (auto* col : {&out.s, &out.p, &out.o}) col->reserve((end - begin) / 48 + 16);
   while (i < end) {
-    size_t j = i;
-    while (j < end && buf[j] != '\n' && buf[j] != '\r') j++;
-    // invalid UTF-8 is a decode error in the reference (text-mode read)
+    // line end: the first '\n', or an earlier '\r' (universal newlines)
+    const void* nl = memchr(buf + i, '\n', end - i);
+    size_t j = nl ? (size_t)(static_cast<const unsigned char*>(nl) - buf) : end;
+    if (const void* cr = memchr(buf + i, '\r', j - i)) j = (size_t)(static_cast<const unsigned char*>(cr) - buf);
+    // invalid UTF-8 is a decode error in the reference (text-mode read);
+    // ASCII runs are checked 8 bytes at a time
     for (size_t k = i; k < j;) {
+      if (k + 8 <= j) {
+        uint64_t w;
+        memcpy(&w, buf + k, 8);
+        if (!(w & 0x8080808080808080ull)) {
+          k += 8;
+          continue;
+        }
+      }
+      if (buf[k] < 0x80) {
+        k++;
+        continue;
+      }
       uint32_t cp;
       int l = utf8_cp(buf, k, j, cp);
       if (!l) {
@@ -394,14 +423,33 @@ void split_lines(const char* buf, size_t n, int parts, std::vector<size_t>& boun
     if (b > bounds.back()) bounds.push_back(b);
   }
   bounds.push_back(n);
-  // line numbers: terminators before each boundary
-  first_lines.assign(bounds.size() - 1, 1);
-  int64_t lines = 1;
-  for (size_t r = 0; r + 1 < bounds.size(); r++) {
-    first_lines[r] = lines;
-    for (size_t i = bounds[r]; i < bounds[r + 1]; i++)
-      if (buf[i] == '\n' || (buf[i] == '\r' && !(i + 1 < n && buf[i + 1] == '\n'))) lines++;
-  }
+  // line numbers: terminators before each boundary ('\n', and '\r' not
+  // followed by '\n'), counted per range on its own thread
+  const size_t nr = bounds.size() - 1;
+  std::vector<int64_t> cnt(nr, 0);
+  auto count = [&](size_t r) {
+    const unsigned char* u = reinterpret_cast<const unsigned char*>(buf);
+    int64_t c = 0;
+    for (size_t i = bounds[r]; i < bounds[r + 1];) {
+      const void* q = memchr(u + i, '\n', bounds[r + 1] - i);
+      if (!q) break;
+      c++;
+      i = (size_t)(static_cast<const unsigned char*>(q) - u) + 1;
+    }
+    for (size_t i = bounds[r]; i < bounds[r + 1];) {
+      const void* q = memchr(u + i, '\r', bounds[r + 1] - i);
+      if (!q) break;
+      const size_t k = (size_t)(static_cast<const unsigned char*>(q) - u);
+      if (!(k + 1 < n && u[k + 1] == '\n')) c++;
+      i = k + 1;
+    }
+    cnt[r] = c;
+  };
+  std::vector<std::thread> th;
+  for (size_t r = 1; r + 1 < nr + 1; r++) th.emplace_back(count, r - 1);  // the last range's count is not needed
+  for (auto& t : th) t.join();
+  first_lines.assign(nr, 1);
+  for (size_t r = 1; r < nr; r++) first_lines[r] = first_lines[r - 1] + cnt[r - 1];
 }
 
 }  // namespace nt

@@ -110,6 +110,42 @@ def test_parse_files_and_line_numbers():
         parse_ntriples_line("<a> <b>", lineno=3)
 
 
+def test_parse_multiline_threads_match_reference(tmp_path):
+    """Whole files of fuzzed statements with mixed line terminators (\n,
+    \r\n, lone \r), split over many parser threads (ASCII fast paths,
+    per-range line counting): the same triples as the reference's
+    read_ntriples, and the same first error with its line number."""
+    if not reference_available():
+        pytest.skip("reference package not installed")
+    from gsmat import qparser
+    from gsmat.errors import ParseError
+
+    rng = random.Random(5)
+    for trial in range(12):
+        lines = []
+        while len(lines) < 400:
+            line = _random_line(rng)
+            if _ref_parse(line, 1)[0] == "ok" or (trial % 3 == 2 and rng.random() < 0.01):
+                lines.append(line)
+        term = ["\n", "\r\n", "\r"]
+        data = "".join(ln + rng.choice(term) for ln in lines).encode()
+        path = tmp_path / f"t{trial}.nt"
+        path.write_bytes(data)
+        try:
+            with open(path, encoding="utf-8") as fh:
+                ref = ("ok", list(qparser.read_ntriples(fh)))
+        except ParseError as e:
+            ref = ("err", str(e))
+        except Exception:
+            continue
+        for threads in (1, 3, 7, 16):
+            try:
+                ours = ("ok", g.parse_ntriples(data, threads=threads))
+            except g.ParseError as e:
+                ours = ("err", str(e))
+            assert ours == ref, (trial, threads)
+
+
 def _same_store(a, b):
     names = sorted(p.name for p in a.iterdir())
     assert names == sorted(p.name for p in b.iterdir())
