@@ -17,8 +17,9 @@
 //   device build: (p, s, o) radix-sorted (two stable passes), adjacent
 //          duplicates dropped, per-predicate runs; again as (p, o, s); run
 //          heads give distinct subjects / objects
-//   host   persist: nodes.dict / preds.dict (escape_term), meta, stats.tsv,
-//          p<ID>.so / p<ID>.os (u64 LE pairs)
+//   host   persist: nodes.dict / preds.dict (escape_term, in slices on the
+//          parse threads), meta, stats.tsv, p<ID>.so / p<ID>.os (u64 LE
+//          pairs); every file written by its own thread
 #include <cub/cub.cuh>
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -26,6 +27,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <string>
 #include <thread>
@@ -309,7 +312,10 @@ gsm_status build_orientation(const std::vector<u64>& key, const std::vector<u32>
 
 // dictionary.escape_term (dictionary.py:18-25)
 void escape_term(std::string& out, const char* p, u32 n) {
-  for (u32 i = 0; i < n; i++) {
+  u32 plain = 0;  // leading run without '\\', '\n', '\r', '\t': appended at once
+  while (plain < n && p[plain] != '\\' && p[plain] != '\n' && p[plain] != '\r' && p[plain] != '\t') plain++;
+  out.append(p, plain);
+  for (u32 i = plain; i < n; i++) {
     const char c = p[i];
     if (c == '\\') out += "\\\\";
     else if (c == '\n') out += "\\n";
@@ -317,13 +323,6 @@ void escape_term(std::string& out, const char* p, u32 n) {
     else if (c == '\t') out += "\\t";
     else out += c;
   }
-}
-
-bool write_file(const std::string& path, const void* data, size_t n) {
-  FILE* f = fopen(path.c_str(), "wb");
-  if (!f) return false;
-  bool ok = n == 0 || fwrite(data, 1, n, f) == n;
-  return fclose(f) == 0 && ok;
 }
 
 // Parse the whole input with `threads` host threads.
@@ -440,8 +439,29 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
     }
   } unmap{buf, n};
   if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  // GSM_INGEST_TIMING=1: phase times on stderr
+  const bool timing = getenv("GSM_INGEST_TIMING") && getenv("GSM_INGEST_TIMING")[0] == '1';
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t_last = now();
+  std::string phases;
+  auto phase = [&](const char* name) {
+    if (!timing) return;
+    const auto t = now();
+    char b[64];
+    snprintf(b, sizeof b, " %s %.1f ms", name, 1e3 * std::chrono::duration<double>(t - t_last).count());
+    phases += b;
+    t_last = t;
+  };
+  struct Report {
+    const bool& on;
+    std::string& ph;
+    ~Report() {
+      if (on) fprintf(stderr, "gsm ingest phases:%s\n", ph.c_str());
+    }
+  } report{timing, phases};
   std::vector<nt::Chunk> chunks;
   gsm_status st = parse_all(buf, n, threads, chunks);
+  phase("parse");
   if (st != GSM_OK) return st;
 
   // occurrences in input order: nodes s0, o0, s1, o1, ...; predicates p0, p1, ...
@@ -480,6 +500,7 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
       });
     for (auto& x : th) x.join();
   }
+  phase("gather");
   GSM_CUDA(cudaSetDevice(device));
   cudaStream_t cs;
   GSM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -496,7 +517,9 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
   if (!bytes.empty()) GSM_CUDA(cudaMemcpyAsync(d_bytes, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, cs));
   std::vector<u32> node_ids, node_first, pred_ids, pred_first;
   if ((st = encode_terms(d_bytes, noff, nlen, cs, node_ids, node_first)) != GSM_OK) return st;
+  phase("encode_nodes");
   if ((st = encode_terms(d_bytes, poff, plen, cs, pred_ids, pred_first)) != GSM_OK) return st;
+  phase("encode_preds");
   const u32 n_nodes = (u32)node_first.size(), n_preds = (u32)pred_first.size();
 
   // triples -> sorted, deduplicated so / os pair images
@@ -510,47 +533,92 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
   if ((st = build_orientation(kso, pred_ids, n_preds, cs, so_pairs, so_rows, so_heads)) != GSM_OK) return st;
   std::vector<u64>().swap(kso);
   if ((st = build_orientation(kos, pred_ids, n_preds, cs, os_pairs, os_rows, os_heads)) != GSM_OK) return st;
+  phase("sort");
 
-  // persist (storage.py:203-219)
+  // persist (storage.py:203-219): the dictionaries rendered in slices and
+  // every file written on its own thread (the pair files are most of the bytes)
   const std::string dir(out_dir);
   mkdir(dir.c_str(), 0777);
-  {
-    std::string s;
-    for (u32 r = 0; r < n_nodes; r++) {
-      const u64 occ = node_first[r];
-      escape_term(s, bytes.data() + noff[occ], nlen[occ]);
-      s += '\n';
-    }
-    if (!write_file(dir + "/nodes.dict", s.data(), s.size())) return set_error(GSM_ERR_VALUE, "cannot write nodes.dict");
-    s.clear();
-    for (u32 r = 0; r < n_preds; r++) {
-      const u64 occ = pred_first[r];
-      escape_term(s, bytes.data() + poff[occ], plen[occ]);
-      s += '\n';
-    }
-    if (!write_file(dir + "/preds.dict", s.data(), s.size())) return set_error(GSM_ERR_VALUE, "cannot write preds.dict");
-  }
   u64 triples = 0;
   for (u32 p = 1; p <= n_preds; p++) triples += so_rows[p];
+  const int nslice = std::max(1, std::min(threads, 64));
+  std::vector<std::string> node_txt(nslice);
   {
-    std::string meta = "GSMAT1\n" + std::to_string(triples) + "\n" + std::to_string(n_preds) + "\n" +
-                       std::to_string(n_nodes) + "\n";
-    if (!write_file(dir + "/meta", meta.data(), meta.size())) return set_error(GSM_ERR_VALUE, "cannot write meta");
-    std::string stats;
-    for (u32 p = 1; p <= n_preds; p++)
-      stats += std::to_string(p) + "\t" + std::to_string(so_rows[p]) + "\t" + std::to_string(so_heads[p]) +
-               "\t" + std::to_string(os_heads[p]) + "\n";
-    if (!write_file(dir + "/stats.tsv", stats.data(), stats.size())) return set_error(GSM_ERR_VALUE, "cannot write stats.tsv");
+    std::vector<std::thread> th;
+    for (int k = 0; k < nslice; k++)
+      th.emplace_back([&, k] {
+        const u32 r0 = (u32)((u64)n_nodes * k / nslice), r1 = (u32)((u64)n_nodes * (k + 1) / nslice);
+        std::string& s = node_txt[k];
+        for (u32 r = r0; r < r1; r++) {
+          const u64 occ = node_first[r];
+          escape_term(s, bytes.data() + noff[occ], nlen[occ]);
+          s += '\n';
+        }
+      });
+    for (auto& x : th) x.join();
   }
-  u64 at_so = 0, at_os = 0;
-  for (u32 p = 1; p <= n_preds; p++) {
-    const std::string base = dir + "/p" + std::to_string(p);
-    if (!write_file(base + ".so", so_pairs.data() + 2 * at_so, 16 * so_rows[p]) ||
-        !write_file(base + ".os", os_pairs.data() + 2 * at_os, 16 * os_rows[p]))
-      return set_error(GSM_ERR_VALUE, "cannot write pair files");
-    at_so += so_rows[p];
-    at_os += os_rows[p];
+  std::string pred_txt;
+  for (u32 r = 0; r < n_preds; r++) {
+    const u64 occ = pred_first[r];
+    escape_term(pred_txt, bytes.data() + poff[occ], plen[occ]);
+    pred_txt += '\n';
   }
+  std::string meta = "GSMAT1\n" + std::to_string(triples) + "\n" + std::to_string(n_preds) + "\n" +
+                     std::to_string(n_nodes) + "\n";
+  std::string stats;
+  for (u32 p = 1; p <= n_preds; p++)
+    stats += std::to_string(p) + "\t" + std::to_string(so_rows[p]) + "\t" + std::to_string(so_heads[p]) + "\t" +
+             std::to_string(os_heads[p]) + "\n";
+  // jobs: (path, pieces); a file's pieces are written in order
+  struct Job {
+    std::string path;
+    std::vector<std::pair<const void*, size_t>> pieces;
+  };
+  std::vector<Job> jobs;
+  {
+    Job nd{dir + "/nodes.dict", {}};
+    for (auto& t : node_txt) nd.pieces.emplace_back(t.data(), t.size());
+    jobs.push_back(std::move(nd));
+    jobs.push_back(Job{dir + "/preds.dict", {{pred_txt.data(), pred_txt.size()}}});
+    jobs.push_back(Job{dir + "/meta", {{meta.data(), meta.size()}}});
+    jobs.push_back(Job{dir + "/stats.tsv", {{stats.data(), stats.size()}}});
+    u64 at_so = 0, at_os = 0;
+    for (u32 p = 1; p <= n_preds; p++) {
+      const std::string base = dir + "/p" + std::to_string(p);
+      jobs.push_back(Job{base + ".so", {{so_pairs.data() + 2 * at_so, 16 * so_rows[p]}}});
+      jobs.push_back(Job{base + ".os", {{os_pairs.data() + 2 * at_os, 16 * os_rows[p]}}});
+      at_so += so_rows[p];
+      at_os += os_rows[p];
+    }
+  }
+  std::atomic<size_t> next{0};
+  std::atomic<int> failed{-1};
+  {
+    std::vector<std::thread> th;
+    for (int k = 0; k < std::max(1, std::min(threads, (int)jobs.size())); k++)
+      th.emplace_back([&] {
+        for (size_t j; (j = next.fetch_add(1)) < jobs.size();) {
+          FILE* f = fopen(jobs[j].path.c_str(), "wb");
+          bool ok = f != nullptr;
+          for (auto& pc : jobs[j].pieces)
+            ok = ok && (pc.second == 0 || fwrite(pc.first, 1, pc.second, f) == pc.second);
+          if (f) ok = fclose(f) == 0 && ok;
+          if (!ok) {
+            int expect = -1;
+            failed.compare_exchange_strong(expect, (int)j);
+          }
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  if (failed.load() >= 0) {
+    const std::string& path = jobs[(size_t)failed.load()].path;
+    const std::string nm = path.substr(path.rfind('/') + 1);
+    if (nm == "nodes.dict" || nm == "preds.dict" || nm == "meta" || nm == "stats.tsv")
+      return set_error(GSM_ERR_VALUE, "cannot write " + nm);
+    return set_error(GSM_ERR_VALUE, "cannot write pair files");
+  }
+  phase("persist");
   if (counts) {
     counts[0] = (int64_t)triples;
     counts[1] = n_preds;
