@@ -162,16 +162,33 @@ __device__ __forceinline__ void export_if_last(const ExportArgs& x) {
     __threadfence();
     const volatile i64* src = reinterpret_cast<const volatile i64*>(x.src);
     i64* dst = reinterpret_cast<i64*>(x.dst);
+    if (!x.img) {
+      for (int i = threadIdx.x; i < x.n * 4; i += blockDim.x) dst[i] = src[i];
+      return;
+    }
+    // Self-cleaning: the first image words, the epoch counter and the
+    // counters to export are loaded together (one round trip, not three);
+    // the block is reset only after every counter has been read.
+    constexpr int IMG_REG = 4;
+    uint4 im[IMG_REG];
+#pragma unroll
+    for (int k = 0; k < IMG_REG; k++) {
+      const int w = threadIdx.x + k * blockDim.x;
+      if (w < x.words16) im[k] = x.img[w];
+    }
+    const u32 base = (threadIdx.x == 0 && x.n_epochs > 0) ? *x.ctr : 0u;
     for (int i = threadIdx.x; i < x.n * 4; i += blockDim.x) dst[i] = src[i];
-    if (x.img) {
-      __syncthreads();  // the counters are exported before the block is reset
-      for (int w = threadIdx.x; w < x.words16; w += blockDim.x) x.blk[w] = x.img[w];
-      __syncthreads();
-      if (threadIdx.x == 0 && x.n_epochs > 0) {
-        const u32 base = *x.ctr;
-        for (int e = 0; e < x.n_epochs; e++) x.epochs[e] = base + 1 + (u32)e;
-        *x.ctr = base + (u32)x.n_epochs;
-      }
+    __syncthreads();  // the counters are exported before the block is reset
+#pragma unroll
+    for (int k = 0; k < IMG_REG; k++) {
+      const int w = threadIdx.x + k * blockDim.x;
+      if (w < x.words16) x.blk[w] = im[k];
+    }
+    for (int w = threadIdx.x + IMG_REG * blockDim.x; w < x.words16; w += blockDim.x) x.blk[w] = x.img[w];
+    __syncthreads();  // the image's epoch slots are overwritten below
+    if (threadIdx.x == 0 && x.n_epochs > 0) {
+      for (int e = 0; e < x.n_epochs; e++) x.epochs[e] = base + 1 + (u32)e;
+      *x.ctr = base + (u32)x.n_epochs;
     }
   }
 }
