@@ -463,6 +463,15 @@ def run_ours(args):
                     "us_per_step": round(1e6 * tt / max(1, nl), 3),
                     "classes": {k: {"bytes": int(v[0]), "steps": v[2], "ms": round(1e3 * v[1], 3)}
                                 for k, v in cls.items()}}
+            # the same algorithmic bytes over the timed region of `value`:
+            # every join step of the 14 queries / the batch's device time
+            if dev_s > 0:
+                ab = tb / dev_s / 1e9
+                roof["batched_step"] = {
+                    "timed_region": "the timed batch steps (value): all join steps of the 14 "
+                                    "concurrent queries / batch device time",
+                    "bytes_per_step": int(tb / args.steps), "achieved": round(ab, 2),
+                    "frac": round(ab / peaks["hbm_gbs"], 5)}
 
         probe = None
         if not args.no_probe:

@@ -182,11 +182,15 @@ struct DevBuf {
 // First-occurrence dense ids (1-based) of n occurrences whose canonical bytes
 // are bytes[off[i], off[i] + len[i]).  first_occ[id - 1] = the occurrence
 // that introduced the term.
-template <class VOff, class VLen>
+// Host vectors the device overwrites whole: not zero-filled first.
+template <class T>
+using hvec = std::vector<T, uninit_alloc<T>>;
+
+template <class VOff, class VLen, class VIds>
 gsm_status encode_terms(const unsigned char* d_bytes, const VOff& off, const VLen& len, cudaStream_t st,
-                        std::vector<u32>& ids, std::vector<u32>& first_occ) {
+                        VIds& ids, VIds& first_occ) {
   const u64 n = off.size();
-  ids.assign(n, 0);
+  ids.resize(n);
   first_occ.clear();
   if (n == 0) return GSM_OK;
   if (n >= 0xFFFFFFFFull) return set_error(GSM_ERR_VALUE, "more than 2^32 term occurrences");
@@ -253,9 +257,9 @@ gsm_status encode_terms(const unsigned char* d_bytes, const VOff& off, const VLe
 
 // One orientation: sort (p, key<<32|val) with two stable radix passes, drop
 // adjacent duplicates, write the pair images and per-predicate counters.
-gsm_status build_orientation(const std::vector<u64>& key, const std::vector<u32>& pid, u32 max_pid,
-                             cudaStream_t st, std::vector<u64>& pairs, std::vector<u64>& rows,
-                             std::vector<u64>& heads) {
+template <class VKey, class VPid, class VPairs>
+gsm_status build_orientation(const VKey& key, const VPid& pid, u32 max_pid, cudaStream_t st, VPairs& pairs,
+                             std::vector<u64>& rows, std::vector<u64>& heads) {
   const u64 T = key.size();
   rows.assign((size_t)max_pid + 1, 0);
   heads.assign((size_t)max_pid + 1, 0);
@@ -515,7 +519,7 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
     ~FreeGuard() { cudaFree(p); }
   } fg{d_bytes};
   if (!bytes.empty()) GSM_CUDA(cudaMemcpyAsync(d_bytes, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, cs));
-  std::vector<u32> node_ids, node_first, pred_ids, pred_first;
+  hvec<u32> node_ids, node_first, pred_ids, pred_first;
   if ((st = encode_terms(d_bytes, noff, nlen, cs, node_ids, node_first)) != GSM_OK) return st;
   phase("encode_nodes");
   if ((st = encode_terms(d_bytes, poff, plen, cs, pred_ids, pred_first)) != GSM_OK) return st;
@@ -523,15 +527,16 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
   const u32 n_nodes = (u32)node_first.size(), n_preds = (u32)pred_first.size();
 
   // triples -> sorted, deduplicated so / os pair images
-  std::vector<u64> kso(T), kos(T);
+  hvec<u64> kso(T), kos(T);
   for (u64 t = 0; t < T; t++) {
     const u64 s = node_ids[2 * t], o = node_ids[2 * t + 1];
     kso[t] = (s << 32) | o;
     kos[t] = (o << 32) | s;
   }
-  std::vector<u64> so_pairs, os_pairs, so_rows, so_heads, os_rows, os_heads;
+  hvec<u64> so_pairs, os_pairs;
+  std::vector<u64> so_rows, so_heads, os_rows, os_heads;
   if ((st = build_orientation(kso, pred_ids, n_preds, cs, so_pairs, so_rows, so_heads)) != GSM_OK) return st;
-  std::vector<u64>().swap(kso);
+  hvec<u64>().swap(kso);
   if ((st = build_orientation(kos, pred_ids, n_preds, cs, os_pairs, os_rows, os_heads)) != GSM_OK) return st;
   phase("sort");
 
