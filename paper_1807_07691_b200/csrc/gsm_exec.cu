@@ -2197,6 +2197,7 @@ struct gsm_context {
   // SM slots other queries of a batch need (GSM_NO_ROW_HINTS=1: off).
   bool use_row_hints = true;
   bool use_self_clean = true;  // GSM_NO_SELF_CLEAN=1: every replay starts with k_init
+  bool batch_order = true;     // GSM_BATCH_ORDER=0: batch members captured in input order
   std::unordered_map<std::string, std::vector<i64>> row_hints;  // plan key -> rows per step
   int tile_items = 0;           // expand tile rows per thread: 0 = by size, 1 or 2 (GSM_TILE_ITEMS)
   // post filters also fuse into an expand expected to output at least this
@@ -2501,6 +2502,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* bq = getenv("GSM_BATCH_PDL")) c->batch_pdl = bq[0] == '1';
   if (const char* rh = getenv("GSM_NO_ROW_HINTS")) c->use_row_hints = !(rh[0] == '1');
   if (const char* sc = getenv("GSM_NO_SELF_CLEAN")) c->use_self_clean = !(sc[0] == '1');
+  if (const char* bo = getenv("GSM_BATCH_ORDER")) c->batch_order = bo[0] != '0';
   if (const char* fh = getenv("GSM_FUSE_HUGE")) c->fuse_huge = std::max<i64>(1, atoll(fh));
   if (const char* ti = getenv("GSM_TILE_ITEMS")) c->tile_items = std::min(2, std::max(0, atoi(ti)));
   if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
@@ -3844,7 +3846,16 @@ bool launch_batch_graph(gsm_context* const* ctxs, int n, std::vector<QueryArgs>&
     // dependents sit on SMs waiting for their predecessor and take the slots
     // the other queries' kernels need (measured: batch 0.096 -> 0.086 ms on
     // the bench workload; single-query latency is the same either way).
-    for (int i = 0; i < n && ok; i++) {
+    // Members are captured longest plan first: the graph's branches are
+    // submitted in capture order, so the chains that decide the batch's
+    // span (most steps) start before the short ones (GSM_BATCH_ORDER=0:
+    // input order).
+    std::vector<int> order((size_t)n);
+    for (int i = 0; i < n; i++) order[i] = i;
+    if (c0->batch_order)
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return qa[a].n > qa[b].n; });
+    for (int oi = 0; oi < n && ok; oi++) {
+      const int i = order[oi];
       const bool pdl = ctxs[i]->use_pdl;
       ctxs[i]->use_pdl = pdl && ctxs[i]->batch_pdl;
       S[i].capture_only = true;
