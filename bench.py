@@ -245,36 +245,50 @@ def _step_bytes(kind: str, L: int, a: int, E: int, O: int, out_a: int) -> int:
     return 0
 
 
-def query_bytes(rep, n_proj: int | None = None) -> int:
-    """Algorithmic HBM bytes of a query's join steps,
-    counting only what the kernels had to move: a step that ran inside the
-    previous step's kernel (``rep.fused``, one k_group launch) does not read
-    its left table from HBM, and the step before it does not write it.  The
-    last step writes the projected width when the projection is narrower
-    (the projection is fused into the last join or packed from k columns)."""
+def step_bytes(rep, i: int, n_proj: int | None = None) -> int:
+    """Algorithmic HBM bytes of join step i of a report,
+    counting only what the kernels had to move:
+    * a step that ran inside the previous step's kernel (``rep.fused``, one
+      k_group launch) does not read its left table from HBM, and the step
+      before it does not write it;
+    * a filter fused behind an expand is evaluated on the candidates inside
+      the kernel; when it is a run intersection the kernel walks the
+      shorter of the two runs per left row, which the report does not
+      give, so neither the expand's candidate reads nor the filter's
+      per-candidate lookups are billed — only the segment lookup per left
+      row of the group (a lower bound: LUBM-1000 c6 has 2.3G candidate rows
+      that no kernel reads one by one);
+    * the last step writes the projected width when the projection is
+      narrower (fused into the last join or packed from k columns)."""
     n = len(rep.steps)
     fused = list(rep.fused) if getattr(rep, "fused", None) else [0] * n
-    total = 0
-    for i in range(1, n):
-        kind = rep.kinds[i]
-        if kind not in ("expand", "filter", "cross"):
-            continue
-        L, a = rep.steps[i - 1].rows, rep.arities[i - 1]
-        E, O, out_a = rep.steps[i].prealloc_total, rep.steps[i].rows, rep.arities[i]
-        if i == n - 1 and n_proj is not None:
-            out_a = min(out_a, n_proj)
-        if kind == "expand":
-            b = 16 * L + W_ID * E
-        elif kind == "filter":
-            b = 16 * L + W_ID * L
+    kind = rep.kinds[i]
+    if kind not in ("expand", "filter", "cross"):
+        return 0
+    L, a = rep.steps[i - 1].rows, rep.arities[i - 1]
+    E, O, out_a = rep.steps[i].prealloc_total, rep.steps[i].rows, rep.arities[i]
+    if i == n - 1 and n_proj is not None:
+        out_a = min(out_a, n_proj)
+    nxt_fused_filter = i + 1 < n and fused[i + 1] and rep.kinds[i + 1] == "filter"
+    if kind == "expand":
+        b = 16 * L + (0 if nxt_fused_filter else W_ID * E)
+    elif kind == "filter":
+        if fused[i] and rep.kinds[i - 1] == "expand":
+            b = 16 * rep.steps[i - 2].rows
         else:
-            b = 0
-        if not fused[i]:
-            b += W_ID * L * a if kind != "cross" else 0
-        if not (i + 1 < n and fused[i + 1]):
-            b += W_ID * O * out_a
-        total += b
-    return total
+            b = 16 * L + W_ID * L
+    else:
+        b = 0
+    if not fused[i]:
+        b += W_ID * L * a if kind != "cross" else 0
+    if not (i + 1 < n and fused[i + 1]):
+        b += W_ID * O * out_a
+    return b
+
+
+def query_bytes(rep, n_proj: int | None = None) -> int:
+    """Algorithmic HBM bytes of a query's join steps (step_bytes summed)."""
+    return sum(step_bytes(rep, i, n_proj) for i in range(1, len(rep.steps)))
 
 
 def run_ours(args):
@@ -408,10 +422,7 @@ def run_ours(args):
                 k = rep.kinds[i]
                 if k not in ("expand", "filter", "cross"):
                     continue
-                L = rep.steps[i - 1].rows
-                a = rep.arities[i - 1]
-                b = _step_bytes(k, L, a, rep.steps[i].prealloc_total, rep.steps[i].rows,
-                                rep.arities[i])
+                b = step_bytes(rep, i)
                 c = cls.setdefault(k, [0.0, 0.0, 0])
                 c[0] += b
                 c[1] += rep.steps[i].seconds
