@@ -2198,6 +2198,7 @@ struct gsm_context {
   bool use_row_hints = true;
   bool use_self_clean = true;  // GSM_NO_SELF_CLEAN=1: every replay starts with k_init
   bool batch_order = true;     // GSM_BATCH_ORDER=0: batch members captured in input order
+  size_t zc_bytes = ZC_BYTES;  // GSM_ZC_BYTES: zero-copy limit of fused-projection results
   std::unordered_map<std::string, std::vector<i64>> row_hints;  // plan key -> rows per step
   int tile_items = 0;           // expand tile rows per thread: 0 = by size, 1 or 2 (GSM_TILE_ITEMS)
   // post filters also fuse into an expand expected to output at least this
@@ -2503,6 +2504,7 @@ gsm_status gsm_context_create(gsm_store* store, int64_t arena_bytes, gsm_context
   if (const char* rh = getenv("GSM_NO_ROW_HINTS")) c->use_row_hints = !(rh[0] == '1');
   if (const char* sc = getenv("GSM_NO_SELF_CLEAN")) c->use_self_clean = !(sc[0] == '1');
   if (const char* bo = getenv("GSM_BATCH_ORDER")) c->batch_order = bo[0] != '0';
+  if (const char* zb = getenv("GSM_ZC_BYTES")) c->zc_bytes = std::min<size_t>(ZC_PACK_BYTES, strtoull(zb, nullptr, 10));
   if (const char* fh = getenv("GSM_FUSE_HUGE")) c->fuse_huge = std::max<i64>(1, atoll(fh));
   if (const char* ti = getenv("GSM_TILE_ITEMS")) c->tile_items = std::min(2, std::max(0, atoi(ti)));
   if (const char* sm = getenv("GSM_STAGE_MAX")) c->stage_max = std::max<size_t>(4096, strtoull(sm, nullptr, 10));
@@ -3104,7 +3106,7 @@ static gsm_status launch_query(gsm_context* c, const QueryArgs& qa, ExecState& S
   // row with coalesced stores, so they stay zero-copy up to ZC_PACK_BYTES;
   // the joins' fused projections scatter, so their limit is ZC_BYTES.
   const bool packs = launches.empty() && !distinct && qa.seed_k < 0 && n_proj >= 1 && n_proj <= 2;
-  const size_t zc_lim = packs ? ZC_PACK_BYTES : ZC_BYTES;
+  const size_t zc_lim = packs ? ZC_PACK_BYTES : c->zc_bytes;
   S.zc = c->guess <= zc_lim;
   const size_t stage_lim = S.zc ? std::min<size_t>(c->stage_bytes, zc_lim) : c->stage_bytes;
   const i64 stage_cap = n_proj ? (i64)(stage_lim / (4 * (size_t)n_proj)) : ((i64)1 << 62);
