@@ -160,14 +160,31 @@ int bits_for(u64 maxv) {
   return b;
 }
 
+// Stream-ordered temporaries from the device's default memory pool, which
+// keeps freed blocks (release threshold raised once): a build allocates and
+// frees ~40 multi-MB buffers, which plain cudaMalloc / cudaFree (a device
+// synchronisation each) made a visible part of the encode and sort phases.
+void keep_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done[device] = true;
+}
 struct DevBuf {
+  cudaStream_t st;
   std::vector<void*> ptrs;
+  explicit DevBuf(cudaStream_t s) : st(s) {}
   ~DevBuf() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, st);
   }
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
-    cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(count * sizeof(T), 16));
+    cudaError_t e = cudaMallocAsync((void**)p, std::max<size_t>(count * sizeof(T), 16), st);
     if (e == cudaSuccess) ptrs.push_back(*p);
     return e;
   }
@@ -194,7 +211,7 @@ gsm_status encode_terms(const unsigned char* d_bytes, const VOff& off, const VLe
   first_occ.clear();
   if (n == 0) return GSM_OK;
   if (n >= 0xFFFFFFFFull) return set_error(GSM_ERR_VALUE, "more than 2^32 term occurrences");
-  DevBuf b;
+  DevBuf b(st);
   u64 *d_off, *d_h, *d_h2;
   u32 *d_len, *d_idx, *d_idx2, *d_head, *d_gid, *d_coll, *d_first, *d_gkey, *d_first2, *d_gkey2, *d_rank, *d_ids;
   IG_CUDA(b.alloc(&d_off, n));
@@ -265,7 +282,7 @@ gsm_status build_orientation(const VKey& key, const VPid& pid, u32 max_pid, cuda
   heads.assign((size_t)max_pid + 1, 0);
   pairs.clear();
   if (T == 0) return GSM_OK;
-  DevBuf b;
+  DevBuf b(st);
   u64 *d_k, *d_k2, *d_k3, *d_pairs;
   u32 *d_p, *d_p2, *d_p3;
   unsigned char* d_keep;
@@ -513,12 +530,18 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
     ~StreamGuard() { cudaStreamDestroy(s); }
   } sg{cs};
   unsigned char* d_bytes = nullptr;
-  GSM_CUDA(cudaMalloc(&d_bytes, std::max<size_t>(bytes.size(), 16)));
+  keep_pool(device);
+  GSM_CUDA(cudaMallocAsync(&d_bytes, std::max<size_t>(bytes.size(), 16), cs));
   struct FreeGuard {
     void* p;
-    ~FreeGuard() { cudaFree(p); }
-  } fg{d_bytes};
+    cudaStream_t s;
+    ~FreeGuard() { cudaFreeAsync(p, s); }
+  } fg{d_bytes, cs};
   if (!bytes.empty()) GSM_CUDA(cudaMemcpyAsync(d_bytes, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, cs));
+  if (timing) {  // (phase split only: the copy otherwise overlaps the next host work)
+    GSM_CUDA(cudaStreamSynchronize(cs));
+    phase("h2d_terms");
+  }
   hvec<u32> node_ids, node_first, pred_ids, pred_first;
   if ((st = encode_terms(d_bytes, noff, nlen, cs, node_ids, node_first)) != GSM_OK) return st;
   phase("encode_nodes");
