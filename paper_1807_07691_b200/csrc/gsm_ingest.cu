@@ -203,11 +203,12 @@ struct DevBuf {
 template <class T>
 using hvec = std::vector<T, uninit_alloc<T>>;
 
+// d_ids_out != nullptr: the ids are copied there (device) instead of to `ids`.
 template <class VOff, class VLen, class VIds>
 gsm_status encode_terms(const unsigned char* d_bytes, const VOff& off, const VLen& len, cudaStream_t st,
-                        VIds& ids, VIds& first_occ) {
+                        VIds& ids, VIds& first_occ, u32* d_ids_out = nullptr) {
   const u64 n = off.size();
-  ids.resize(n);
+  ids.resize(d_ids_out ? 0 : n);
   first_occ.clear();
   if (n == 0) return GSM_OK;
   if (n >= 0xFFFFFFFFull) return set_error(GSM_ERR_VALUE, "more than 2^32 term occurrences");
@@ -267,17 +268,31 @@ gsm_status encode_terms(const unsigned char* d_bytes, const VOff& off, const VLe
   count_launch(4);
   first_occ.resize(G);
   IG_CUDA(cudaMemcpyAsync(first_occ.data(), d_first2, 4 * G, cudaMemcpyDeviceToHost, st));
-  IG_CUDA(cudaMemcpyAsync(ids.data(), d_ids, 4 * n, cudaMemcpyDeviceToHost, st));
+  if (d_ids_out) IG_CUDA(cudaMemcpyAsync(d_ids_out, d_ids, 4 * n, cudaMemcpyDeviceToDevice, st));
+  else IG_CUDA(cudaMemcpyAsync(ids.data(), d_ids, 4 * n, cudaMemcpyDeviceToHost, st));
   IG_CUDA(cudaStreamSynchronize(st));
   return GSM_OK;
 }
 
+// Sort keys of both orientations from the interleaved (s, o) node ids.
+__global__ void k_pair_keys(const u32* __restrict__ ids, u64 T, u64* __restrict__ kso, u64* __restrict__ kos) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += stride) {
+    const u64 sv = ids[2 * t], ov = ids[2 * t + 1];
+    kso[t] = (sv << 32) | ov;
+    kos[t] = (ov << 32) | sv;
+  }
+}
+
 // One orientation: sort (p, key<<32|val) with two stable radix passes, drop
 // adjacent duplicates, write the pair images and per-predicate counters.
+// d_key_src / d_pid_src != nullptr: T keys / pids already on the device
+// (key / pid are then not read).
 template <class VKey, class VPid, class VPairs>
 gsm_status build_orientation(const VKey& key, const VPid& pid, u32 max_pid, cudaStream_t st, VPairs& pairs,
-                             std::vector<u64>& rows, std::vector<u64>& heads) {
-  const u64 T = key.size();
+                             std::vector<u64>& rows, std::vector<u64>& heads,
+                             const u64* d_key_src = nullptr, const u32* d_pid_src = nullptr, u64 T_dev = 0) {
+  const u64 T = d_key_src ? T_dev : key.size();
   rows.assign((size_t)max_pid + 1, 0);
   heads.assign((size_t)max_pid + 1, 0);
   pairs.clear();
@@ -294,8 +309,13 @@ gsm_status build_orientation(const VKey& key, const VPid& pid, u32 max_pid, cuda
   IG_CUDA(b.alloc(&d_p2, T));
   IG_CUDA(b.alloc(&d_keep, T));
   IG_CUDA(b.alloc(&d_nsel, 1));
-  IG_CUDA(cudaMemcpyAsync(d_k, key.data(), 8 * T, cudaMemcpyHostToDevice, st));
-  IG_CUDA(cudaMemcpyAsync(d_p, pid.data(), 4 * T, cudaMemcpyHostToDevice, st));
+  if (d_key_src) {
+    IG_CUDA(cudaMemcpyAsync(d_k, d_key_src, 8 * T, cudaMemcpyDeviceToDevice, st));
+    IG_CUDA(cudaMemcpyAsync(d_p, d_pid_src, 4 * T, cudaMemcpyDeviceToDevice, st));
+  } else {
+    IG_CUDA(cudaMemcpyAsync(d_k, key.data(), 8 * T, cudaMemcpyHostToDevice, st));
+    IG_CUDA(cudaMemcpyAsync(d_p, pid.data(), 4 * T, cudaMemcpyHostToDevice, st));
+  }
   // (key) then stable by p  ->  sorted by (p, key)
   size_t t1 = 0, t2 = 0, t3 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t1, d_k, d_k2, d_p, d_p2, (int64_t)T, 0, 64, st);
@@ -543,24 +563,35 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
     phase("h2d_terms");
   }
   hvec<u32> node_ids, node_first, pred_ids, pred_first;
-  if ((st = encode_terms(d_bytes, noff, nlen, cs, node_ids, node_first)) != GSM_OK) return st;
+  // node / predicate ids stay on the device: the sort keys are built there
+  DevBuf keys(cs);
+  u32 *d_nids, *d_pids;
+  u64 *d_kso, *d_kos;
+  GSM_CUDA(keys.alloc(&d_nids, 2 * T));
+  GSM_CUDA(keys.alloc(&d_pids, T));
+  GSM_CUDA(keys.alloc(&d_kso, T));
+  GSM_CUDA(keys.alloc(&d_kos, T));
+  if ((st = encode_terms(d_bytes, noff, nlen, cs, node_ids, node_first, d_nids)) != GSM_OK) return st;
   phase("encode_nodes");
-  if ((st = encode_terms(d_bytes, poff, plen, cs, pred_ids, pred_first)) != GSM_OK) return st;
+  if ((st = encode_terms(d_bytes, poff, plen, cs, pred_ids, pred_first, d_pids)) != GSM_OK) return st;
   phase("encode_preds");
   const u32 n_nodes = (u32)node_first.size(), n_preds = (u32)pred_first.size();
 
   // triples -> sorted, deduplicated so / os pair images
-  hvec<u64> kso(T), kos(T);
-  for (u64 t = 0; t < T; t++) {
-    const u64 s = node_ids[2 * t], o = node_ids[2 * t + 1];
-    kso[t] = (s << 32) | o;
-    kos[t] = (o << 32) | s;
+  if (T > 0) {
+    k_pair_keys<<<gridn(T), 256, 0, cs>>>(d_nids, T, d_kso, d_kos);
+    GSM_CUDA(cudaGetLastError());
+    count_launch();
   }
+  const hvec<u64> no_keys;
   hvec<u64> so_pairs, os_pairs;
   std::vector<u64> so_rows, so_heads, os_rows, os_heads;
-  if ((st = build_orientation(kso, pred_ids, n_preds, cs, so_pairs, so_rows, so_heads)) != GSM_OK) return st;
-  hvec<u64>().swap(kso);
-  if ((st = build_orientation(kos, pred_ids, n_preds, cs, os_pairs, os_rows, os_heads)) != GSM_OK) return st;
+  if ((st = build_orientation(no_keys, pred_ids, n_preds, cs, so_pairs, so_rows, so_heads, d_kso, d_pids, T)) !=
+      GSM_OK)
+    return st;
+  if ((st = build_orientation(no_keys, pred_ids, n_preds, cs, os_pairs, os_rows, os_heads, d_kos, d_pids, T)) !=
+      GSM_OK)
+    return st;
   phase("sort");
 
   // persist (storage.py:203-219): the dictionaries rendered in slices and
