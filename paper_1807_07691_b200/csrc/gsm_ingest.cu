@@ -513,7 +513,24 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
   }
   // the chunks' term bytes and offsets gathered into one array, each chunk
   // by its own thread (bases from a prefix over the chunks)
+  GSM_CUDA(cudaSetDevice(device));
+  cudaStream_t cs;
+  GSM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{cs};
+  unsigned char* d_bytes = nullptr;
+  keep_pool(device);
+  GSM_CUDA(cudaMallocAsync(&d_bytes, std::max<size_t>(nb, 16), cs));
+  struct FreeGuard {
+    void* p;
+    cudaStream_t s;
+    ~FreeGuard() { cudaFreeAsync(p, s); }
+  } fg{d_bytes, cs};
+  GSM_CUDA(cudaStreamSynchronize(cs));  // d_bytes is written from the gather threads' streams
   std::vector<char, uninit_alloc<char>> bytes(nb);
+  std::vector<cudaError_t> h2d_err(chunks.size(), cudaSuccess);
   std::vector<u64, uninit_alloc<u64>> noff(2 * T), poff(T);
   std::vector<u32, uninit_alloc<u32>> nlen(2 * T), plen(T);
   {
@@ -527,7 +544,19 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
       th.emplace_back([&, k] {
         nt::Chunk& c = chunks[k];
         const u64 base = bbase[k];
-        if (!c.bytes.empty()) memcpy(bytes.data() + base, c.bytes.data(), c.bytes.size());
+        if (!c.bytes.empty()) {
+          // this chunk's term bytes to the device from its own thread (the
+          // pageable copies' staging runs on all gather threads at once)
+          cudaStream_t ts = nullptr;
+          cudaError_t e = cudaSetDevice(device);
+          if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking);
+          if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_bytes + base, c.bytes.data(), c.bytes.size(), cudaMemcpyHostToDevice, ts);
+          memcpy(bytes.data() + base, c.bytes.data(), c.bytes.size());
+          if (e == cudaSuccess) e = cudaStreamSynchronize(ts);
+          if (ts) cudaStreamDestroy(ts);
+          h2d_err[k] = e;
+        }
         u64 t = tbase[k];
         for (size_t i = 0; i < c.s.size(); i++, t++) {
           noff[2 * t] = base + c.s[i].off;
@@ -542,26 +571,7 @@ gsm_status gsm_build_store(const char* nt_path, const char* out_dir, int32_t dev
     for (auto& x : th) x.join();
   }
   phase("gather");
-  GSM_CUDA(cudaSetDevice(device));
-  cudaStream_t cs;
-  GSM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
-  } sg{cs};
-  unsigned char* d_bytes = nullptr;
-  keep_pool(device);
-  GSM_CUDA(cudaMallocAsync(&d_bytes, std::max<size_t>(bytes.size(), 16), cs));
-  struct FreeGuard {
-    void* p;
-    cudaStream_t s;
-    ~FreeGuard() { cudaFreeAsync(p, s); }
-  } fg{d_bytes, cs};
-  if (!bytes.empty()) GSM_CUDA(cudaMemcpyAsync(d_bytes, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, cs));
-  if (timing) {  // (phase split only: the copy otherwise overlaps the next host work)
-    GSM_CUDA(cudaStreamSynchronize(cs));
-    phase("h2d_terms");
-  }
+  for (cudaError_t e : h2d_err) GSM_CUDA(e);
   hvec<u32> node_ids, node_first, pred_ids, pred_first;
   // node / predicate ids stay on the device: the sort keys are built there
   DevBuf keys(cs);
