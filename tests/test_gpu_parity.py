@@ -291,7 +291,7 @@ def test_execution_variants_agree(store_factory):
     for variant in ("", "GSM_NO_GRAPHS", "GSM_NO_PDL", "GSM_NO_FUSION", "GSM_NO_DEFER",
                     "GSM_NO_PROJ_FUSION", "GSM_NO_BATCH_GRAPH", "GSM_STAGE_MAX=65536", "GSM_TILE_ITEMS=2", "GSM_FUSE_HUGE=1", "GSM_NO_INTERSECT",
                     "GSM_NO_ROW_HINTS", "GSM_NO_SELF_CLEAN", "GSM_BATCH_POLL=0", "GSM_GRID_MAX=3",
-                    "GSM_GRID_MAX=2,GSM_TILE_ITEMS=2", "GSM_BATCH_ORDER=0",
+                    "GSM_GRID_MAX=2,GSM_TILE_ITEMS=2", "GSM_BATCH_ORDER=0", "GSM_ZC_BYTES=0",
                     "GSM_NO_GRAPHS,GSM_NO_PDL,GSM_NO_FUSION,GSM_NO_DEFER,GSM_NO_PROJ_FUSION"):
         env = dict(os.environ)
         for item in filter(None, variant.split(",")):
