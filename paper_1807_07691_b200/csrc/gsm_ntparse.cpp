@@ -122,9 +122,11 @@ void put_utf8(std::vector<char>& o, uint32_t cp) {
 bool unescape_literal(const unsigned char* s, size_t b, size_t e, std::vector<char>& o, std::string& msg) {
   for (size_t i = b; i < e;) {
     const unsigned char c = s[i];
-    if (c != '\\') {
-      o.push_back((char)c);
-      i++;
+    if (c != '\\') {  // the run up to the next backslash, appended at once
+      const void* bs = memchr(s + i, '\\', e - i);
+      const size_t j = bs ? (size_t)(static_cast<const unsigned char*>(bs) - s) : e;
+      o.insert(o.end(), s + i, s + j);
+      i = j;
       continue;
     }
     const unsigned char x = s[i + 1];  // the lexical scan guarantees a char follows
